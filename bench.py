@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Headline benchmark: Stokes ALM voxel-iterations/s at 256^3 fp64 (BASELINE.json).
+
+Workload (BASELINE cfg 3): one 256^3 random polydisperse sphere packing per GPU
+(SURVEY §8d generator, seed = rank // 3), load case g_p = e_{rank % 3}, the
+reference's default (adaptive) penalties, eps = 1e-5.  A "step" is one ADMM
+iteration of the device loop (stokes.py:375-417).  Multi-GPU is the ensemble
+sharding of §8e: one independent cell per rank, no data-path collective
+(scaling "weak"); the time is the max over ranks of CUDA-event durations.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the CPU restatement of the reference (oracle/, the
+reference being pure numpy/scipy for 3D) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Stokes ALM voxel-iters/s at 256³ fp64, 1/2/4/8 GPU; % HBM roofline vs CPU ref"
+UNIT = "voxel-iter/s"
+B_ALG_ITER = 417.0  # canonical algorithmic bytes per Stokes voxel-iteration
+FALLBACK_HBM = 6650.0
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling around the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(tempfile.mkstemp(prefix="clocks_", suffix=".csv")[1])
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def stop(self, t0, t1):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 10:
+                continue
+            rows.append(parts)
+        self.path.unlink(missing_ok=True)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        # keep the samples taken while the timed region ran (by sample order: the
+        # sampler started before warm-up; use the last samples covering t1 - t0)
+        n_keep = max(1, int((t1 - t0) / 0.1) + 1)
+        sel = rows[-(n_keep + 2):-1] if len(rows) > n_keep + 2 else rows
+        sm = sorted(float(r[2]) for r in sel if r[2].replace(".", "").isdigit())
+        smax = max((float(r[3]) for r in sel if r[3].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in sel for k in range(4) if r[6 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(sel)}
+
+
+# ---------------------------------------------------------------- reference (CPU) arm
+def cpu_stokes_rate(n, seed, g, budget_s, max_iters):
+    """Oracle (CPU restatement of the reference, numpy + scipy.fft, all host
+    threads) on the same cell: voxel-iters/s over the loop alone."""
+    import numpy as np
+
+    from oracle import poreflow_oracle as O
+    import paper_2312_15554_b200 as pf
+
+    ind = pf.random_packing_geometry(n, seed=seed)
+    tm = {}
+    O.solve_stokes(ind.values, g, 1e-5, 1e-5, max_iter=1, timer=tm)  # warm-up + speed estimate
+    k = int(max(1, min(max_iters, budget_s / max(tm["loop_s"], 1e-3))))
+    tm = {}
+    O.solve_stokes(ind.values, g, 1e-5, 1e-5, max_iter=k, timer=tm)
+    del np
+    return n ** 3 * k / tm["loop_s"], k, tm["loop_s"]
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    n = args.n
+    rate, k, secs = cpu_stokes_rate(n, 0, (1.0, 0.0, 0.0), args.cpu_budget, max(1, args.steps))
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": k, "warmup": 1, "ms_per_step": 1e3 * secs / k, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"stokes_admm_random_packing_{n}^3", "grid": [n, n, n], "load_case": "e1",
+                   "penalties": "reference default (adaptive)", "eps": 1e-5},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{k} ADMM iteration(s) of the {n}^3 cell after 1 warm-up iteration "
+                                   f"(loop time only; numpy + scipy.fft workers={cores})"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+STAGES = ("S1_spectral", "Z2D_cufft", "S3_local", "finalize", "S4_form_r", "D2Z_cufft")
+
+
+def stage_bytes(n_real, n_half, d=3):
+    """Algorithmic bytes per launch of each stage."""
+    w = 8
+    return {
+        "S1_spectral": n_half * 16 * (1 + d + 1) + n_half * 16 * (d + 1 + 1),  # Q,R,Dprev in; U,Q,D out
+        "Z2D_cufft": d * (n_half * 16 + n_real * w),
+        "S3_local": n_real * (w * (5 * d) + 1) + n_real * w * (4 * d),  # 5d words + H in; 4d words out
+        "finalize": 0,
+        "S4_form_r": n_real * w * (2 * d) + n_real * w * d,
+        "D2Z_cufft": d * (n_real * w + n_half * 16),
+    }
+
+
+def run_ours(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2312_15554_b200 as pf
+    from paper_2312_15554_b200 import _native as N
+
+    n = args.n
+    seed, case = rank // 3, rank % 3
+    g = [0.0, 0.0, 0.0]
+    g[case] = 1.0
+    ind = pf.random_packing_geometry(n, seed=seed)
+    cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=tuple(g), max_iter=10**7)
+    pen = pf.PenaltyParams()
+    prof_iters = 3
+    rows = args.warmup + args.steps + prof_iters + 1
+    state = pf.DeviceAdmmState.zeros(ind.grid, dev)
+    solver = pf.StokesSolver(ind, cfg, pen, state, dev, history_rows=rows)
+    solver.begin()
+    solver.iterate(args.warmup, poll=False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local_rank).start() if rank == 0 else None
+    time.sleep(0.3 if clocks else 0.0)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
+    start.record()
+    solver.iterate(args.steps, poll=False)
+    stop.record()
+    torch.cuda.synchronize()
+    t1 = time.time()
+    ms = start.elapsed_time(stop)
+    if dist:
+        dist.barrier()
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop(t0, t1) if clocks else None
+    # per-stage launch times on the same stream (CUDA events; no graph)
+    stage_ms = (ctypes.c_double * 6)()
+    N.check(N.load().pf_stokes_profile(solver.plan.handle, prof_iters, stage_ms))
+    res = solver.end()
+    assert not res.converged and res.iterations == args.warmup + args.steps + prof_iters, (
+        "bench cell converged inside the timed window; raise the grid size or lower eps")
+    value = world * n ** 3 * args.steps / (ms / 1e3)
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = peak_hbm()
+    n_real, n_half = n ** 3, n * n * (n // 2 + 1)
+    sb = stage_bytes(n_real, n_half)
+    stages = {}
+    for k, name in enumerate(STAGES):
+        t_ms = float(stage_ms[k])
+        stages[name] = {"ms": t_ms, "alg_bytes": sb[name],
+                        "GB_s": (sb[name] / (t_ms * 1e-3) / 1e9) if t_ms > 0 and sb[name] else None}
+    ours = [s for s in STAGES if "cufft" not in s and s != "finalize"]
+    dom = max(ours, key=lambda s: stages[s]["ms"])
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic_per_launch.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(dom)
+        except Exception:
+            traffic = None
+    achieved = stages[dom]["GB_s"]
+    iter_ms_profile = sum(float(stage_ms[k]) for k in range(6))
+
+    # end-to-end through the public numpy API: host indicator in, host state out
+    e2e_iters = args.steps
+    solid_host = np.array(ind.values)
+    e2e_ind = pf.IndicatorField(pf.UnitCellGrid((n, n, n)), solid_host)
+    torch.cuda.synchronize()
+    te0 = time.perf_counter()
+    st_h, rep_h = pf.solve_stokes(e2e_ind, pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=tuple(g),
+                                                                          max_iter=e2e_iters), pen)
+    torch.cuda.synchronize()
+    te1 = time.perf_counter()
+    assert rep_h.iterations == e2e_iters
+    e2e_value = n ** 3 * e2e_iters / (te1 - te0)
+    h2d = n ** 3  # uint8 indicator (zero initial state is created on device)
+    d2h = (4 * 3 + 1) * 8 * n ** 3 + e2e_iters * 15 * 8
+    del st_h
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, k_cpu, secs = cpu_stokes_rate(n, seed, tuple(g), args.cpu_budget, 100)
+        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{k_cpu} ADMM iteration(s) of the same {n}^3 cell on the host (loop time only, "
+                         f"{secs:.1f} s; numpy + scipy.fft, all host threads)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"stokes_admm_random_packing_{n}^3", "grid": [n, n, n],
+                   "cells": world, "load_cases": "e_{rank%3}", "packing_seed": "rank//3",
+                   "penalties": "reference default (adaptive)", "eps": 1e-5,
+                   "parallelism": f"ensemble{world} (one independent cell per GPU)",
+                   "l2": "inputs larger than L2 (~25 x 128 MiB fields per cell), no flush"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": peak_src},
+        "iteration_roofline": {"alg_bytes_per_voxel_iter": B_ALG_ITER,
+                               "achieved_GB_s": B_ALG_ITER * value / world / 1e9,
+                               "frac": B_ALG_ITER * value / world / 1e9 / peak},
+        "stages": stages, "stage_profile_ms_per_iter": iter_ms_profile,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_iters,
+                "d2h_bytes_per_step": d2h / e2e_iters, "iterations": e2e_iters,
+                "api": "paper_2312_15554_b200.solve_stokes (numpy in/out)"},
+        "gpu_launches": 4 * args.steps,
+        "library_launches_note": "plus 2 cuFFT executions (batch 3) per iteration",
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,194 @@
+/*
+ * poreflow_b200 — C ABI of the B200-native FFT micromechanics solver
+ * (Stokes ADMM + comparison-medium transport of arXiv 2312.15554).
+ *
+ * The drop-in seam of the reference is the Python solver API of package
+ * `poreflow` (reference: pkg/src/poreflow/__init__.py:11-102) plus its kernel
+ * plugin contract `backends.kernels_for(dim)` (pkg/src/poreflow/backends/
+ * __init__.py:43-47, pure.py:26-115).  The reference has no C ABI of its own;
+ * these entry points are what its Python layer binds through ctypes
+ * (INTEGRATION.md shows the stub).  Every entry point:
+ *   - takes plain pointers and sizes (device pointers unless stated "host"),
+ *   - returns an int status (PF_OK == 0); nothing throws across the ABI,
+ *   - records a message retrievable with pf_last_error() (thread-local).
+ * Field layout follows the reference (pure.py:8-10): scalars are C-order
+ * grids (last axis fastest), vectors carry a leading component axis,
+ * spectral arrays are complex128 interleaved (re, im).
+ */
+#ifndef POREFLOW_B200_H
+#define POREFLOW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_ERR_ARG 1   /* invalid argument / validation failure  -> ValueError */
+#define PF_ERR_CUDA 2  /* CUDA runtime failure                   -> RuntimeError */
+#define PF_ERR_CUFFT 3 /* cuFFT failure                          -> RuntimeError */
+#define PF_ERR_STATE 4 /* call out of sequence                   -> RuntimeError */
+
+#define PF_SYMBOLS_EXACT 0   /* spectral.py:26 "exact"   */
+#define PF_SYMBOLS_CENTRAL 1 /* spectral.py:27 "central" */
+
+#define PF_STOKES_COLUMNS 15   /* stokes.py:38-43   */
+#define PF_TRANSPORT_COLUMNS 4 /* transport.py:28   */
+
+typedef struct pf_plan pf_plan;
+
+/* Library version (major*10000 + minor*100 + patch) and last error text. */
+int pf_version(void);
+const char* pf_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Plan: one grid (UnitCellGrid, grid.py:25-71), its symbol tables
+ * (make_symbols, spectral.py:72-98), cuFFT plans and solver scratch.
+ * `dims` (host, ndim entries, 1 <= ndim <= 3, every entry >= 4 per
+ * grid.py:36-39).  `stream` is a cudaStream_t the plan orders itself after
+ * (may be NULL = legacy default stream).  Not thread-safe: one plan per
+ * host thread / stream, mirroring the "independent solver instances"
+ * contract (tests/test_backends.py:131-149).
+ * ---------------------------------------------------------------------- */
+int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode, int device,
+                   void* stream);
+int pf_plan_destroy(pf_plan* plan);
+int pf_plan_set_stream(pf_plan* plan, void* stream);
+/* Replace the symbol tables of one logical axis (host arrays of dims[axis]
+ * doubles: kappa_j and the 1D Laplacian term, spectral.py:78-86).  The
+ * Python host layer passes numpy's own tables so the device sees the
+ * reference's bits; pf_plan_create fills them with libm otherwise. */
+int pf_plan_set_symbol_tables(pf_plan* plan, int axis, const double* kappa_host,
+                              const double* lap1d_host);
+/* Bytes of device scratch the plan currently holds (buffers + cuFFT work). */
+int pf_plan_device_bytes(const pf_plan* plan, size_t* bytes);
+
+/* ------------------------------------------------------------------------
+ * Stokes ADMM — replaces poreflow.stokes.solve_stokes (stokes.py:313-427)
+ * for non-degenerate cells (the all-solid fast path, stokes.py:336-353, and
+ * the warm-start validation, 355-361, stay in the host wrapper).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  double nu;                   /* StokesConfig.nu                    stokes.py:91  */
+  double pressure_gradient[3]; /* StokesConfig.pressure_gradient     stokes.py:92  */
+  double eps_abs, eps_rel;     /*                                    stokes.py:93-94 */
+  int64_t max_iter;            /*                                    stokes.py:95  */
+  double alpha, beta, b;       /* PenaltyParams                      stokes.py:57-59 */
+  int32_t adaptive;            /*                                    stokes.py:60  */
+  double growth[3];            /*                                    stokes.py:61  */
+  double ratio_threshold[3];   /*                                    stokes.py:62  */
+  double floor[3];             /*                                    stokes.py:63  */
+} pf_stokes_params;
+
+typedef struct {
+  int64_t iterations;        /* ConvergenceReport.iterations                 */
+  int32_t converged;         /* ConvergenceReport.converged                  */
+  int32_t done;              /* loop finished (converged or max_iter)        */
+  double final_penalties[3]; /* meta["final_penalties"]  stokes.py:425       */
+} pf_stokes_result;
+
+/* solid: uint8 0/1 grid.  u, u_tilde, a, lam: ndim x grid f64; q: grid f64.
+ * In: initial state (zeros or warm start).  Out: final state (AdmmState).
+ * history: max_iter x 15 f64 rows (REPORT_COLUMNS order); rows
+ * [0, iterations) are written.  All device pointers, resident on the plan's
+ * device, must stay valid until pf_stokes_end returns. */
+int pf_stokes_solve(pf_plan* plan, const pf_stokes_params* params, const uint8_t* solid, double* u,
+                    double* u_tilde, double* q, double* a, double* lam, double* history,
+                    pf_stokes_result* result);
+
+/* Split form of pf_stokes_solve for device-resident drivers and benchmarks:
+ * begin = setup (spectral copies, stokes.py:363-370); iterate = run up to
+ * n_iter more iterations of the loop body (stokes.py:375-417) as CUDA graphs
+ * with a device-side done flag (poll = 0: enqueue all n_iter iterations and
+ * return without host synchronisation); end = write q, fill result. */
+int pf_stokes_begin(pf_plan* plan, const pf_stokes_params* params, const uint8_t* solid, double* u,
+                    double* u_tilde, double* q, double* a, double* lam, double* history);
+int pf_stokes_iterate(pf_plan* plan, int64_t n_iter, int poll, pf_stokes_result* result);
+int pf_stokes_end(pf_plan* plan, pf_stokes_result* result);
+/* Measurement hook (bench.py): run n_iter iterations without graphs, with CUDA
+ * events between stages; stage_ms (host, 6 doubles) receives the mean time of
+ * S1 spectral | Z2D | S3 local | finalize | S4 form-R | D2Z, in ms. */
+int pf_stokes_profile(pf_plan* plan, int64_t n_iter, double* stage_ms);
+
+/* ------------------------------------------------------------------------
+ * Transport — replaces poreflow.transport.solve_transport
+ * (transport.py:180-268) including build_coefficients (101-128).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  double pe, eta, a0, b0, eps;     /* TransportConfig   transport.py:44-49 */
+  double composition_gradient[3];  /*                   transport.py:45    */
+  int64_t max_iter;                /*                   transport.py:50    */
+} pf_transport_params;
+
+typedef struct {
+  int64_t iterations;
+  int32_t converged;
+  int32_t diverged;
+  int32_t reason; /* 0 none, 1 non-finite residual, 2 growth guard (transport.py:243-255) */
+  int32_t done;
+  double b0_vec[3]; /* MediumCoefficients.b0_vec   transport.py:123-127 */
+  double u_bar[3];  /* MediumCoefficients.u_bar    transport.py:116     */
+} pf_transport_result;
+
+/* u: ndim x grid velocity (read only).  chi: grid, grad_chi: ndim x grid —
+ * in: initial state, out: final state.  history: max_iter x 4 rows. */
+int pf_transport_solve(pf_plan* plan, const pf_transport_params* params, const uint8_t* solid,
+                       const double* u, double* chi, double* grad_chi, double* history,
+                       pf_transport_result* result);
+int pf_transport_begin(pf_plan* plan, const pf_transport_params* params, const uint8_t* solid,
+                       const double* u, double* chi, double* grad_chi, double* history,
+                       pf_transport_result* result);
+int pf_transport_iterate(pf_plan* plan, int64_t n_iter, int poll, pf_transport_result* result);
+int pf_transport_end(pf_plan* plan, pf_transport_result* result);
+
+/* ------------------------------------------------------------------------
+ * Effective properties — effective.py:32-108, grid.py:108-110.
+ * Results are written to HOST memory.
+ * ---------------------------------------------------------------------- */
+/* Pore mean of ncomp stacked fields f (ncomp x grid).  effective.py:32-40 */
+int pf_pore_average(pf_plan* plan, const uint8_t* solid, const double* f, int ncomp,
+                    double* out_host);
+/* Solid-voxel count (porosity = 1 - count/n, grid.py:108-110). */
+int pf_solid_count(pf_plan* plan, const uint8_t* solid, int64_t* count_host);
+/* u_solutions: host array of ndim device pointers (each ndim x grid).
+ * K: host ndim x ndim.  effective.py:43-72 */
+int pf_permeability(pf_plan* plan, const uint8_t* solid, const double* const* u_solutions,
+                    double* K_host);
+/* chi / grad_chi: host arrays of ndim device pointers.  effective.py:75-108 */
+int pf_diffusivity(pf_plan* plan, const uint8_t* solid, const double* const* u_solutions,
+                   const double* const* chi, const double* const* grad_chi, double pe,
+                   double* D_host);
+
+/* ------------------------------------------------------------------------
+ * Kernel plugin — the five functions of backends/pure.py:26-115 on device
+ * pointers, full-spectrum layout (what backends.kernels_for() returns).
+ * dims: host, ndim entries.  kappas: host array of ndim device pointers to
+ * the per-axis symbol tables.  Complex arrays are interleaved complex128.
+ * `solid` is the f64 0/1 field (as in pure.py).  stream may be NULL.
+ * ---------------------------------------------------------------------- */
+int pf_k_stokes_velocity_update(int ndim, const int64_t* dims, const double* q_hat,
+                                const double* a_hat, const double* ut_hat,
+                                const double* const* kappas, const double* lap,
+                                const double* kappa_sq, double nu, double beta, double b,
+                                const double* g_p_host, double* u_hat, void* stream);
+int pf_k_aux_velocity_update(int ndim, const int64_t* dims, const double* u, const double* a,
+                             const double* lam, const double* solid, double alpha, double b,
+                             double* u_tilde, void* stream);
+int pf_k_multiplier_update(int ndim, const int64_t* dims, const double* a, const double* lam,
+                           const double* u, const double* u_tilde, const double* solid,
+                           double alpha, double b, double* a_new, double* lam_new, void* stream);
+int pf_k_transport_polarization(int ndim, const int64_t* dims, const double* grad_chi,
+                                const double* diffusivity, const double* advection,
+                                const double* forcing, double a0, const double* b0_vec_host,
+                                const double* g_chi_host, double* w, double* s, void* stream);
+int pf_k_transport_mode_update(int ndim, const int64_t* dims, const double* w_hat,
+                               const double* s_hat, const double* const* kappas,
+                               const double* lap, double a0, const double* b0_vec_host,
+                               double* chi_hat, double* grad_hat, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POREFLOW_B200_H */

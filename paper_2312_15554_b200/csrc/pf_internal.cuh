@@ -1,0 +1,231 @@
+// Internal declarations shared by the poreflow_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/poreflow_b200.h"
+
+namespace pf {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+const char* cufft_name(cufftResult r);
+
+#define PF_CK_CUDA(expr)                                                                 \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      ::pf::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return PF_ERR_CUDA;                                                                \
+    }                                                                                    \
+  } while (0)
+
+#define PF_CK_FFT(expr)                                                                  \
+  do {                                                                                   \
+    cufftResult _r = (expr);                                                             \
+    if (_r != CUFFT_SUCCESS) {                                                           \
+      ::pf::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr, ::pf::cufft_name(_r)); \
+      return PF_ERR_CUFFT;                                                               \
+    }                                                                                    \
+  } while (0)
+
+#define PF_CK(expr)                 \
+  do {                              \
+    int _s = (expr);                \
+    if (_s != PF_OK) return _s;     \
+  } while (0)
+
+#define PF_ARG(cond, ...)                 \
+  do {                                    \
+    if (!(cond)) {                        \
+      ::pf::set_error(__VA_ARGS__);       \
+      return PF_ERR_ARG;                  \
+    }                                     \
+  } while (0)
+
+// ---------------------------------------------------------------- launch geometry
+constexpr int kThreads = 256;
+constexpr int kSMs = 148;
+constexpr int kMaxBlocks = kSMs * 8;  // 8 x 256-thread CTAs fill an SM (2048 threads)
+constexpr int kFinalizeThreads = 512;
+
+inline int blocks_for(int64_t work) {
+  int64_t b = (work + kThreads - 1) / kThreads;
+  if (b < 1) b = 1;
+  return (int)(b > kMaxBlocks ? kMaxBlocks : b);
+}
+
+// ---------------------------------------------------------------- grid geometry
+// Logical grid of d axes embedded in padded 3D (n0, n1, n2) with leading 1s;
+// logical axis j <-> padded axis 3-d+j.  Half spectrum is (n0, n1, n2h).
+struct Geom {
+  int d;
+  int n[3];     // padded dims
+  int n2h;      // n[2]/2 + 1
+  int64_t nr;   // real points
+  int64_t nh;   // half-spectrum modes
+  double inv_n; // 1/nr
+  double dn;    // (double) nr
+};
+
+// Device-side solver control block (one per plan; lives in device memory).
+struct Ctrl {
+  double alpha, beta, b;  // current penalties (Stokes)
+  double best;            // running minimum of r1+r2 (transport)
+  int64_t iter;           // completed iterations
+  int32_t done, converged, diverged, reason;
+};
+
+// Stokes constants that do not change during a solve.
+struct StokesConst {
+  double nu, eps_rel;
+  double tol_vec, tol_sca;  // sqrt(n_vec)*eps_abs, sqrt(n_sca)*eps_abs (host-computed)
+  double g[3];              // pressure gradient (logical components)
+  double growth[3], thr[3], floor_[3];
+  int64_t max_iter;
+  int adaptive;
+};
+
+struct TransportConst {
+  double pe, eta, a0, eps_tol1, eps_tol2;  // tolerances sqrt(n)*eps, sqrt(dn)*eps
+  double g[3], b0v[3];
+  double ubar_dot_g;  // float(u_bar @ g_chi)   transport.py:121
+  int64_t max_iter;
+};
+
+struct Graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int iters = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    iters = 0;
+  }
+};
+
+}  // namespace pf
+
+struct pf_plan {
+  pf::Geom g;
+  int mode;
+  int device;
+  cudaStream_t user_stream;  // caller's stream (torch current stream)
+  cudaStream_t work;         // plan-owned stream (graph capture needs a non-legacy stream)
+  cudaEvent_t ev_user, ev_work, ev_poll[2];
+  // per padded axis symbol tables (device), length n[p]
+  double* kap[3];
+  double* ell[3];
+  std::vector<double> h_kap[3], h_ell[3];
+  // cuFFT: forward D2Z / inverse Z2D for batch 1, d, d+1, d*d
+  cufftHandle fwd[4], inv[4];
+  int batch_of[4];
+  void* fft_work;
+  size_t fft_work_bytes;
+  // scratch
+  double2* specA;  // (d+1) * nh
+  double2* specB;  // (d+1) * nh
+  double2* spec1;  // nh
+  double2* spec2;  // nh
+  double* realA;   // (d+1) * nr
+  double* realB;   // (d+1) * nr
+  double* partials;  // 16 * kMaxBlocks
+  pf::Ctrl* ctrl;     // device
+  pf::Ctrl* h_ctrl;   // pinned host, 2 slots for double-buffered polling
+  double* h_small;    // pinned host scratch (64 doubles)
+  size_t scratch_bytes;
+  // active solve state
+  int active;  // 0 none, 1 stokes, 2 transport
+  pf::Graph graph;
+  // stokes bindings
+  const uint8_t* s_solid;
+  double *s_u, *s_ut, *s_q, *s_a, *s_lam, *s_hist;
+  pf::StokesConst sc;
+  // transport bindings
+  const double* t_u;
+  double *t_chi, *t_grad, *t_hist;
+  pf::TransportConst tc;
+  pf_transport_result t_res;
+};
+
+namespace pf {
+
+int plan_ensure_scratch(pf_plan* p);
+int plan_fft(pf_plan* p, bool forward, int batch, void* in, void* out);
+int enter(pf_plan* p);  // order plan->work after user stream
+int leave(pf_plan* p);  // order user stream after plan->work
+int run_chunks(pf_plan* p, int64_t n_iter, int poll, int (*enqueue)(pf_plan*), Ctrl* out_ctrl);
+int symbol_tables_for(int mode, int n, std::vector<double>& kap, std::vector<double>& ell);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+// i*k*a for real k
+__device__ __forceinline__ double2 cik(double k, double2 a) { return make_double2(-(k * a.y), k * a.x); }
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// numpy complex division (loops.c.src Smith variant) — bitwise what the
+// reference computes for f_hat / denom (pure.py:109).
+__device__ __forceinline__ double2 cdiv_np(double2 a, double2 b) {
+  double ar = fabs(b.x), ai = fabs(b.y);
+  if (ar >= ai) {
+    if (ar == 0.0 && ai == 0.0) return make_double2(a.x / ar, a.y / ai);
+    double rat = b.y / b.x;
+    double scl = 1.0 / (b.x + b.y * rat);
+    return make_double2((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
+  } else {
+    double rat = b.x / b.y;
+    double scl = 1.0 / (b.y + b.x * rat);
+    return make_double2((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+  }
+}
+
+// Block-wide sum of NQ per-thread values; thread 0 returns the totals in v.
+template <int NQ>
+__device__ __forceinline__ void block_sum(double (&v)[NQ]) {
+  __shared__ double sh[NQ][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double x = v[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) sh[q][wid] = x;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double x = lane < nw ? sh[q][lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      v[q] = x;
+    }
+  }
+  __syncthreads();
+}
+
+// Deterministic block partials -> totals: partials laid out [q][nblk].
+template <int NQ>
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nblk, double (&tot)[NQ]) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) s += part[(int64_t)q * nblk + i];
+    tot[q] = s;
+  }
+  block_sum<NQ>(tot);
+}
+
+__device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }
+
+}  // namespace pf

@@ -1,0 +1,473 @@
+// Stokes augmented-Lagrangian (ADMM) loop on device — reference
+// pkg/src/poreflow/stokes.py:313-427.
+//
+// Per iteration (half-spectrum canonical pipeline):
+//   S1 k_stokes_spectral  : Green's operator (pure.py:26-56) on R^ = FFT(b u~ - a)
+//                           and Q^; writes U^/n, D^ = i k.U^ (div, stokes.py:381),
+//                           Q^' = Q^ - beta D^ with Q^'(0) = 0 (stokes.py:408-409),
+//                           and the Parseval sums of |D^|^2, |D^ - D^_prev|^2, |Q^'|^2.
+//   S2 cuFFT Z2D (batch d): U^/n -> u'
+//   S3 k_stokes_local     : u~' (pure.py:59-61), a', lam' (pure.py:64-68) and six
+//                           real-space squared norms (stokes.py:254-277).
+//   F  k_stokes_finalize  : residual pairs + tolerances (stokes.py:247-284), the
+//                           history row (398-403), convergence (413-415), and
+//                           residual balancing (adapt_penalties, 287-310).
+//   S4 k_form_r           : R = b' u~' - a' (next iteration's right-hand side,
+//                           stokes.py:405-407 by linearity of the transform).
+//   S5 cuFFT D2Z (batch d): R -> R^
+// Every kernel returns immediately once ctrl->done is set.
+#include <cmath>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+
+struct Tables {
+  const double* kap[3];
+  const double* ell[3];
+};
+
+static Tables tables_of(const pf_plan* p) {
+  Tables t;
+  for (int i = 0; i < 3; ++i) {
+    t.kap[i] = p->kap[i];
+    t.ell[i] = p->ell[i];
+  }
+  return t;
+}
+
+__device__ __forceinline__ void mode_index(const Geom& g, uint32_t m, int (&idx)[3]) {
+  const uint32_t n2h = (uint32_t)g.n2h, n1 = (uint32_t)g.n[1];
+  const uint32_t t = m / n2h;
+  idx[2] = (int)(m - t * n2h);
+  idx[1] = (int)(t % n1);
+  idx[0] = (int)(t / n1);
+}
+
+// Parseval weight on the half spectrum: 1 on the k2 = 0 and k2 = Nyquist planes.
+__device__ __forceinline__ double parseval_w(const Geom& g, int i2) {
+  return (i2 == 0 || ((g.n[2] & 1) == 0 && i2 == g.n[2] / 2)) ? 1.0 : 2.0;
+}
+
+// ---------------------------------------------------------------------- S1
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_stokes_spectral(
+    Geom g, Tables T, const double nu, const double gx, const double gy, const double gz,
+    double2* __restrict__ Qh, const double2* __restrict__ Rh, double2* __restrict__ Dh,
+    double2* __restrict__ Uh, const Ctrl* __restrict__ ctrl, double* __restrict__ part) {
+  if (ctrl->done) return;
+  const double beta = ctrl->beta, b = ctrl->b;
+  const double gp[3] = {gx, gy, gz};
+  double acc[3] = {0.0, 0.0, 0.0};
+  const uint32_t nh = (uint32_t)g.nh;
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < nh; m += gridDim.x * blockDim.x) {
+    int idx[3];
+    mode_index(g, m, idx);
+    double kc[D];
+    double L = 0.0, ksq = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const int ax = 3 - D + c;
+      kc[c] = __ldg(T.kap[ax] + idx[ax]);
+      L = L + __ldg(T.ell[ax] + idx[ax]);
+      ksq = ksq + kc[c] * kc[c];
+    }
+    const double2 q = Qh[m];
+    double2 r[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double2 rc = Rh[(size_t)c * nh + m];
+      r[c] = make_double2(kc[c] * q.y + rc.x, -(kc[c] * q.x) + rc.y);  // -i k q + R^
+      if (m == 0) r[c].x = r[c].x + g.dn * gp[c];                         // n g_p at k = 0
+    }
+    const double A = nu * L + b;
+    double2 kr = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < D; ++c) kr = cadd(kr, cscale(kc[c], r[c]));
+    const double f = beta / (A + beta * ksq);
+    const double2 corr = cscale(f, kr);
+    const double invA = 1.0 / A;
+    double2 dv = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double2 u = csub(r[c], cscale(kc[c], corr));
+      u = make_double2(u.x * invA, u.y * invA);
+      dv = cadd(dv, cik(kc[c], u));
+      Uh[(size_t)c * nh + m] = make_double2(u.x * g.inv_n, u.y * g.inv_n);
+    }
+    double2 qn = csub(q, cscale(beta, dv));
+    if (m == 0) qn = make_double2(0.0, 0.0);
+    const double2 dprev = Dh[m];
+    const double w = parseval_w(g, idx[2]);
+    acc[0] += w * cabs2(dv);
+    acc[1] += w * cabs2(csub(dv, dprev));
+    acc[2] += w * cabs2(qn);
+    Qh[m] = qn;
+    Dh[m] = dv;
+  }
+  block_sum<3>(acc);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 3; ++k) part[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// ---------------------------------------------------------------------- S3
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_stokes_local(
+    const int64_t n, const double* __restrict__ un, double* __restrict__ u, double* __restrict__ ut,
+    double* __restrict__ a, double* __restrict__ lam, const uint8_t* __restrict__ H,
+    const Ctrl* __restrict__ ctrl, double* __restrict__ part) {
+  if (ctrl->done) return;
+  const double alpha = ctrl->alpha, b = ctrl->b;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    const double h = (double)H[x];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const int64_t i = c * n + x;
+      const double u1 = un[i], u0 = u[i], t0 = ut[i], a0 = a[i], l0 = lam[i];
+      const double t1 = ((a0 + b * u1) - h * l0) / (b + alpha * h);  // pure.py:61
+      const double a1 = a0 + b * (u1 - t1);                          // pure.py:66
+      const double l1 = l0 + alpha * (h * t1);                       // pure.py:67
+      const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
+      acc[0] += s0 * s0;   // |H u~'|           r_p1
+      acc[1] += s1 * s1;   // |H (u~' - u~)|    r_d1 / alpha
+      acc[2] += l1 * l1;   // |lam'|
+      acc[3] += s3 * s3;   // |u' - u~'|        r_p3
+      acc[4] += s4 * s4;   // |u' - u|          r_d3 / b
+      acc[5] += a1 * a1;   // |a'|
+      u[i] = u1;
+      ut[i] = t1;
+      a[i] = a1;
+      lam[i] = l1;
+    }
+  }
+  block_sum<6>(acc);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) part[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// ---------------------------------------------------------------------- F
+__global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
+    Ctrl* __restrict__ ctrl, const double* __restrict__ part3, int nb3, const double* __restrict__ part1,
+    int nb1, double* __restrict__ hist, const StokesConst C, const double inv_n) {
+  if (ctrl->done) return;
+  double S[6], P[3];
+  reduce_partials<6>(part3, nb3, S);
+  reduce_partials<3>(part1, nb1, P);
+  if (threadIdx.x != 0) return;
+  const double alpha = ctrl->alpha, beta = ctrl->beta, b = ctrl->b;
+  const double er = C.eps_rel;
+  double rp[3], rd[3], tp[3], td[3];
+  rp[0] = sqrt(S[0]);
+  rd[0] = alpha * sqrt(S[1]);
+  const double ln = sqrt(S[2]);
+  tp[0] = C.tol_vec + er * pymax(rp[0], ln);
+  td[0] = C.tol_vec + er * ln;
+  rp[1] = sqrt(P[0] * inv_n);
+  rd[1] = beta * sqrt(P[1] * inv_n);
+  const double qn = sqrt(P[2] * inv_n);
+  tp[1] = C.tol_sca + er * pymax(rp[1], qn);
+  td[1] = C.tol_sca + er * qn;
+  rp[2] = sqrt(S[3]);
+  rd[2] = b * sqrt(S[4]);
+  const double an = sqrt(S[5]);
+  tp[2] = C.tol_vec + er * pymax(rp[2], an);
+  td[2] = C.tol_vec + er * an;
+  const int64_t it = ctrl->iter + 1;
+  double* row = hist + (it - 1) * PF_STOKES_COLUMNS;
+  for (int k = 0; k < 3; ++k) {
+    row[4 * k + 0] = rp[k];
+    row[4 * k + 1] = tp[k];
+    row[4 * k + 2] = rd[k];
+    row[4 * k + 3] = td[k];
+  }
+  row[12] = alpha;
+  row[13] = beta;
+  row[14] = b;
+  ctrl->iter = it;
+  bool passed = true;
+  for (int k = 0; k < 3; ++k) passed = passed && (rp[k] <= tp[k] && rd[k] <= td[k]);
+  if (passed) {
+    ctrl->converged = 1;
+    ctrl->done = 1;
+    return;
+  }
+  if (C.adaptive) {  // adapt_penalties, stokes.py:299-310
+    double v[3] = {alpha, beta, b};
+    for (int k = 0; k < 3; ++k) {
+      if (rp[k] == 0.0 && rd[k] == 0.0) continue;
+      const double grow = rd[k] == 0.0 ? INFINITY : rp[k] / rd[k];
+      const double shrink = rp[k] == 0.0 ? INFINITY : rd[k] / rp[k];
+      if (grow > C.thr[k])
+        v[k] = C.growth[k] * v[k];
+      else if (shrink > C.thr[k])
+        v[k] = pymax(v[k] / C.growth[k], C.floor_[k]);
+    }
+    ctrl->alpha = v[0];
+    ctrl->beta = v[1];
+    ctrl->b = v[2];
+  }
+  if (it >= C.max_iter) ctrl->done = 1;
+}
+
+// ---------------------------------------------------------------------- S4
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_form_r(const int64_t n, const double* __restrict__ ut,
+                                                     const double* __restrict__ a, double* __restrict__ R,
+                                                     const Ctrl* __restrict__ ctrl, int gated) {
+  if (gated && ctrl->done) return;
+  const double b = ctrl->b;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) R[c * n + x] = b * ut[c * n + x] - a[c * n + x];
+  }
+}
+
+// ---------------------------------------------------------------------- setup helpers
+// D^ = sum_c i k_c U^_c of the initial velocity (div_prev, stokes.py:370).
+template <int D>
+__global__ void k_div_spectrum(Geom g, Tables T, const double2* __restrict__ Uh, double2* __restrict__ Dh) {
+  const uint32_t nh = (uint32_t)g.nh;
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < nh; m += gridDim.x * blockDim.x) {
+    int idx[3];
+    mode_index(g, m, idx);
+    double2 dv = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const int ax = 3 - D + c;
+      dv = cadd(dv, cik(__ldg(T.kap[ax] + idx[ax]), Uh[(size_t)c * nh + m]));
+    }
+    Dh[m] = dv;
+  }
+}
+
+__global__ void k_zero_mode(double2* Qh) { Qh[0] = make_double2(0.0, 0.0); }
+
+__global__ void k_scale_copy(int64_t nh, const double2* __restrict__ src, double2* __restrict__ dst, double s) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nh; m += (int64_t)gridDim.x * blockDim.x)
+    dst[m] = make_double2(src[m].x * s, src[m].y * s);
+}
+
+__global__ void k_ctrl_init(Ctrl* c, double alpha, double beta, double b) {
+  c->alpha = alpha;
+  c->beta = beta;
+  c->b = b;
+  c->best = INFINITY;
+  c->iter = 0;
+  c->done = c->converged = c->diverged = c->reason = 0;
+}
+
+// ---------------------------------------------------------------------- host side
+// One loop iteration.  With `ev` (7 events) the stage boundaries are recorded
+// for pf_stokes_profile: S1 | Z2D | S3 | F | S4 | D2Z.
+template <int D>
+static int enqueue_stokes_t(pf_plan* p, cudaEvent_t* ev = nullptr) {
+  const Geom& g = p->g;
+  const int64_t n = g.nr, nh = g.nh;
+  const int nb1 = blocks_for(nh), nb3 = blocks_for(n);
+  double* part1 = p->partials;                   // 3 x nb1
+  double* part3 = p->partials + 3 * kMaxBlocks;  // 6 x nb3
+  double2* Rh = p->specA;
+  double2* Uh = p->specB;
+  double2* Qh = p->spec1;
+  double2* Dh = p->spec2;
+  double* un = p->realA;
+  double* R = p->realB;
+  const StokesConst& C = p->sc;
+  auto mark = [&](int i) -> int {
+    if (ev) PF_CK_CUDA(cudaEventRecord(ev[i], p->work));
+    return PF_OK;
+  };
+  PF_CK(mark(0));
+  k_stokes_spectral<D><<<nb1, kThreads, 0, p->work>>>(g, tables_of(p), C.nu, C.g[0], C.g[1], C.g[2], Qh, Rh, Dh,
+                                                      Uh, p->ctrl, part1);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(1));
+  PF_CK(plan_fft(p, false, D, Uh, un));
+  PF_CK(mark(2));
+  k_stokes_local<D><<<nb3, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid, p->ctrl,
+                                                   part3);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(3));
+  k_stokes_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, part3, nb3, part1, nb1, p->s_hist, C, g.inv_n);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(4));
+  k_form_r<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 1);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(5));
+  PF_CK(plan_fft(p, true, D, R, Rh));
+  PF_CK(mark(6));
+  return PF_OK;
+}
+
+static int enqueue_stokes(pf_plan* p) {
+  switch (p->g.d) {
+    case 1: return enqueue_stokes_t<1>(p);
+    case 2: return enqueue_stokes_t<2>(p);
+    default: return enqueue_stokes_t<3>(p);
+  }
+}
+
+static int enqueue_stokes_ev(pf_plan* p, cudaEvent_t* ev) {
+  switch (p->g.d) {
+    case 1: return enqueue_stokes_t<1>(p, ev);
+    case 2: return enqueue_stokes_t<2>(p, ev);
+    default: return enqueue_stokes_t<3>(p, ev);
+  }
+}
+
+template <int D>
+static int stokes_setup_t(pf_plan* p, double b0) {
+  const Geom& g = p->g;
+  const int64_t n = g.nr, nh = g.nh;
+  // Q^ = FFT(q), gauge Q^(0) = 0 (stokes.py:363, 367)
+  PF_CK(plan_fft(p, true, 1, p->s_q, p->spec1));
+  k_zero_mode<<<1, 1, 0, p->work>>>(p->spec1);
+  // D^_prev = i k . FFT(u)  (stokes.py:370)
+  PF_CK(plan_fft(p, true, D, p->s_u, p->specB));
+  k_div_spectrum<D><<<blocks_for(nh), kThreads, 0, p->work>>>(g, tables_of(p), p->specB, p->spec2);
+  // R^ = FFT(b u~ - a)  (stokes.py:368-369)
+  k_form_r<D><<<blocks_for(n), kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, p->realB, p->ctrl, 0);
+  PF_CK(plan_fft(p, true, D, p->realB, p->specA));
+  PF_CK_CUDA(cudaGetLastError());
+  (void)b0;
+  return PF_OK;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
+                    double* a, double* lam, double* history) {
+  PF_ARG(p && P && solid && u && ut && q && a && lam && history, "null argument");
+  PF_ARG(P->b > 0.0, "coupling penalty b must be positive for the zero mode");
+  PF_ARG(P->nu > 0.0, "viscosity must be positive");
+  PF_ARG(P->max_iter >= 1, "max_iter must be at least 1");
+  PF_CK(enter(p));
+  PF_CK(plan_ensure_scratch(p));
+  if (p->active != 1) p->graph.reset();
+  p->active = 1;
+  p->s_solid = solid;
+  p->s_u = u;
+  p->s_ut = ut;
+  p->s_q = q;
+  p->s_a = a;
+  p->s_lam = lam;
+  p->s_hist = history;
+  StokesConst& C = p->sc;
+  const int d = p->g.d;
+  C.nu = P->nu;
+  C.eps_rel = P->eps_rel;
+  C.tol_vec = std::sqrt((double)(d * p->g.nr)) * P->eps_abs;
+  C.tol_sca = std::sqrt((double)p->g.nr) * P->eps_abs;
+  for (int k = 0; k < 3; ++k) {
+    C.g[k] = k < d ? P->pressure_gradient[k] : 0.0;
+    C.growth[k] = P->growth[k];
+    C.thr[k] = P->ratio_threshold[k];
+    C.floor_[k] = P->floor[k];
+  }
+  C.max_iter = P->max_iter;
+  C.adaptive = P->adaptive;
+  // Graph kernels capture StokesConst and the state pointers by value.
+  p->graph.reset();
+  k_ctrl_init<<<1, 1, 0, p->work>>>(p->ctrl, P->alpha, P->beta, P->b);
+  PF_CK_CUDA(cudaGetLastError());
+  switch (d) {
+    case 1: PF_CK(stokes_setup_t<1>(p, P->b)); break;
+    case 2: PF_CK(stokes_setup_t<2>(p, P->b)); break;
+    default: PF_CK(stokes_setup_t<3>(p, P->b)); break;
+  }
+  return PF_OK;
+}
+
+int pf_stokes_iterate(pf_plan* p, int64_t n_iter, int poll, pf_stokes_result* res) {
+  PF_ARG(p, "null plan");
+  if (p->active != 1) {
+    set_error("pf_stokes_iterate without pf_stokes_begin");
+    return PF_ERR_STATE;
+  }
+  Ctrl c;
+  PF_CK(enter(p));
+  PF_CK(run_chunks(p, n_iter, poll, enqueue_stokes, &c));
+  PF_CK(leave(p));
+  if (res && c.iter >= 0) {
+    res->iterations = c.iter;
+    res->converged = c.converged;
+    res->done = c.done;
+    res->final_penalties[0] = c.alpha;
+    res->final_penalties[1] = c.beta;
+    res->final_penalties[2] = c.b;
+  }
+  return PF_OK;
+}
+
+int pf_stokes_end(pf_plan* p, pf_stokes_result* res) {
+  PF_ARG(p, "null plan");
+  if (p->active != 1) {
+    set_error("pf_stokes_end without pf_stokes_begin");
+    return PF_ERR_STATE;
+  }
+  // q = Re ifft(Q^): copy (Z2D overwrites its input), fold 1/n, transform.
+  const int64_t nh = p->g.nh;
+  k_scale_copy<<<blocks_for(nh), kThreads, 0, p->work>>>(nh, p->spec1, p->specB, p->g.inv_n);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
+  PF_CK_CUDA(cudaMemcpyAsync(&p->h_ctrl[0], p->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, p->work));
+  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  const Ctrl c = p->h_ctrl[0];
+  if (res) {
+    res->iterations = c.iter;
+    res->converged = c.converged;
+    res->done = c.done;
+    res->final_penalties[0] = c.alpha;
+    res->final_penalties[1] = c.beta;
+    res->final_penalties[2] = c.b;
+  }
+  p->active = 0;
+  PF_CK(leave(p));
+  return PF_OK;
+}
+
+int pf_stokes_profile(pf_plan* p, int64_t n_iter, double* stage_ms) {
+  PF_ARG(p && stage_ms && n_iter >= 1, "bad argument");
+  if (p->active != 1) {
+    set_error("pf_stokes_profile without pf_stokes_begin");
+    return PF_ERR_STATE;
+  }
+  PF_CK(enter(p));
+  cudaEvent_t ev[7];
+  for (int i = 0; i < 7; ++i) PF_CK_CUDA(cudaEventCreate(&ev[i]));
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  int st = PF_OK;
+  for (int64_t it = 0; it < n_iter && st == PF_OK; ++it) {
+    st = enqueue_stokes_ev(p, ev);
+    if (st != PF_OK) break;
+    if (cudaEventSynchronize(ev[6]) != cudaSuccess) {
+      set_error("event sync failed");
+      st = PF_ERR_CUDA;
+      break;
+    }
+    for (int k = 0; k < 6; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      acc[k] += ms;
+    }
+  }
+  for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+  PF_CK(st);
+  for (int k = 0; k < 6; ++k) stage_ms[k] = acc[k] / (double)n_iter;
+  return leave(p);
+}
+
+int pf_stokes_solve(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
+                    double* a, double* lam, double* history, pf_stokes_result* res) {
+  PF_CK(pf_stokes_begin(p, P, solid, u, ut, q, a, lam, history));
+  pf_stokes_result r{};
+  PF_CK(pf_stokes_iterate(p, P->max_iter, 1, &r));
+  return pf_stokes_end(p, res);
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+"""Device plumbing: CUDA device selection, plan cache, host<->device moves.
+
+PyTorch supplies device memory and the current stream; the compute is the
+native library.  One ``Plan`` per (grid, symbol mode, device, host thread):
+plans are not thread-safe, mirroring the reference's "independent solver
+instances" contract (tests/test_backends.py:131-149).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native as N
+
+_SYMBOL_CODES = {"exact": N.PF_SYMBOLS_EXACT, "central": N.PF_SYMBOLS_CENTRAL}
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def require_cuda(device=None):
+    """The CUDA device to use; raises when none is available (no CPU fallback)."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("poreflow_b200 needs a CUDA device (B200, sm_100a); none is visible")
+    N.load()
+    if device is None:
+        return t.device("cuda", t.cuda.current_device())
+    dev = t.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"poreflow_b200 computes on CUDA devices only, got {dev}")
+    return t.device("cuda", dev.index if dev.index is not None else t.cuda.current_device())
+
+
+class Plan:
+    """Owns one ``pf_plan*``: grid geometry, symbol tables, cuFFT plans, scratch."""
+
+    def __init__(self, dims, mode: str, device):
+        from .spectral import symbol_tables
+
+        t = torch()
+        self.dims = tuple(int(n) for n in dims)
+        self.mode = mode
+        self.device = device
+        lib = N.load()
+        h = ctypes.c_void_p()
+        with t.cuda.device(device):
+            stream = t.cuda.current_stream(device).cuda_stream
+            N.check(lib.pf_plan_create(ctypes.byref(h), len(self.dims), N.i64_array(self.dims),
+                                       _SYMBOL_CODES[mode], device.index, ctypes.c_void_p(stream)))
+        self.handle = h
+        # numpy's own tables, so the device uses the reference's bits (spectral.py:78-86)
+        for ax, (kap, lap1) in enumerate(symbol_tables(self.dims, mode)):
+            kap = np.ascontiguousarray(kap, dtype=np.float64)
+            lap1 = np.ascontiguousarray(lap1, dtype=np.float64)
+            N.check(lib.pf_plan_set_symbol_tables(h, ax, kap.ctypes.data, lap1.ctypes.data))
+
+    def bind_stream(self):
+        t = torch()
+        stream = t.cuda.current_stream(self.device).cuda_stream
+        N.check(N.load().pf_plan_set_stream(self.handle, ctypes.c_void_p(stream)))
+        return self.handle
+
+    def device_bytes(self) -> int:
+        out = ctypes.c_size_t()
+        N.check(N.load().pf_plan_device_bytes(self.handle, ctypes.byref(out)))
+        return int(out.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.load().pf_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_plans = threading.local()
+
+
+def get_plan(dims, mode: str, device=None) -> Plan:
+    device = require_cuda(device)
+    cache = getattr(_plans, "cache", None)
+    if cache is None:
+        cache = _plans.cache = {}
+    key = (tuple(int(n) for n in dims), mode, device.index)
+    plan = cache.get(key)
+    if plan is None:
+        plan = cache[key] = Plan(dims, mode, device)
+    return plan
+
+
+def release_plans() -> None:
+    """Free every plan (and its device scratch) owned by this host thread."""
+    cache = getattr(_plans, "cache", None) or {}
+    for p in cache.values():
+        p.close()
+    cache.clear()
+
+
+def to_device(arr, device, dtype=None):
+    """numpy array / torch tensor -> contiguous CUDA tensor (copy for numpy)."""
+    t = torch()
+    if isinstance(arr, t.Tensor):
+        x = arr.to(device=device, dtype=dtype or arr.dtype)
+        return x.contiguous()
+    a = np.ascontiguousarray(arr, dtype=dtype and _np_dtype(dtype))
+    return t.from_numpy(a).to(device=device, non_blocking=False)
+
+
+def _np_dtype(tdtype):
+    t = torch()
+    return {t.float64: np.float64, t.uint8: np.uint8, t.complex128: np.complex128}[tdtype]
+
+
+def solid_on_device(indicator, device):
+    """Cached device copy of an (immutable) IndicatorField's uint8 values."""
+    cache = indicator._device_cache
+    key = device.index
+    if key not in cache:
+        cache[key] = to_device(indicator.values, device, torch().uint8)
+    return cache[key]
