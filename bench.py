@@ -143,6 +143,7 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm
 STAGES = ("S1_spectral", "Z2D_cufft", "S3_local", "finalize", "S4_form_r", "D2Z_cufft")
+FUSED_STAGES = ("PK_axis0_spectral", "MI_axis1_inverse", "RS_rows_local", "finalize", "MF_axis1_forward", "-")
 
 
 def stage_bytes(n_real, n_half, d=3):
@@ -155,6 +156,19 @@ def stage_bytes(n_real, n_half, d=3):
         "finalize": 0,
         "S4_form_r": n_real * w * (2 * d) + n_real * w * d,
         "D2Z_cufft": d * (n_real * w + n_half * 16),
+    }
+
+
+def stage_bytes_fused(n_real, n_half):
+    """Algorithmic bytes per launch of the fused pipeline's passes."""
+    hw = n_half * 16  # one half-spectrum component
+    return {
+        "PK_axis0_spectral": 10 * hw,          # Y(3) Q D in; Y(3) Q D out
+        "MI_axis1_inverse": 6 * hw,            # Y(3) in; X(3) out
+        "RS_rows_local": 9 * hw + 24 * 8 * n_real + n_real,  # X(3) in, X(6) out; 12+12 state words; H
+        "finalize": 0,
+        "MF_axis1_forward": 9 * hw,            # X(6) in; Y(3) out
+        "-": 0,
     }
 
 
@@ -215,6 +229,7 @@ def run_ours(args):
     # per-stage launch times on the same stream (CUDA events; no graph)
     stage_ms = (ctypes.c_double * 6)()
     N.check(N.load().pf_stokes_profile(solver.plan.handle, prof_iters, stage_ms))
+    pipeline = solver.pipeline
     res = solver.end()
     assert not res.converged and res.iterations == args.warmup + args.steps + prof_iters, (
         "bench cell converged inside the timed window; raise the grid size or lower eps")
@@ -228,13 +243,16 @@ def run_ours(args):
 
     peak, peak_src = peak_hbm()
     n_real, n_half = n ** 3, n * n * (n // 2 + 1)
-    sb = stage_bytes(n_real, n_half)
+    names = FUSED_STAGES if pipeline == "fused" else STAGES
+    sb = stage_bytes_fused(n_real, n_half) if pipeline == "fused" else stage_bytes(n_real, n_half)
     stages = {}
-    for k, name in enumerate(STAGES):
+    for k, name in enumerate(names):
+        if name == "-":
+            continue
         t_ms = float(stage_ms[k])
         stages[name] = {"ms": t_ms, "alg_bytes": sb[name],
                         "GB_s": (sb[name] / (t_ms * 1e-3) / 1e9) if t_ms > 0 and sb[name] else None}
-    ours = [s for s in STAGES if "cufft" not in s and s != "finalize"]
+    ours = [s for s in stages if "cufft" not in s and s != "finalize"]
     dom = max(ours, key=lambda s: stages[s]["ms"])
     traffic = None
     tfile = ROOT / "profiles" / "traffic_per_launch.json"
@@ -288,8 +306,10 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_iters,
                 "d2h_bytes_per_step": d2h / e2e_iters, "iterations": e2e_iters,
                 "api": "paper_2312_15554_b200.solve_stokes (numpy in/out)"},
-        "gpu_launches": 4 * args.steps,
-        "library_launches_note": "plus 2 cuFFT executions (batch 3) per iteration",
+        "pipeline": pipeline,
+        "gpu_launches": (5 if pipeline == "fused" else 4) * args.steps,
+        "library_launches_note": ("none: all transforms are in-kernel" if pipeline == "fused"
+                                  else "plus 2 cuFFT executions (batch 3) per iteration"),
         "clocks": clk,
         "cpu_baseline": cpu,
     }

@@ -56,6 +56,10 @@ int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode
                    void* stream);
 int pf_plan_destroy(pf_plan* plan);
 int pf_plan_set_stream(pf_plan* plan, void* stream);
+/* Enable (default) or disable the fused power-of-two Stokes pipeline
+ * (cubic grids N = 64, 128, 256); disabled or unsupported grids use the
+ * general cuFFT pipeline.  Both compute the same iteration. */
+int pf_plan_set_fused(pf_plan* plan, int enable);
 /* Replace the symbol tables of one logical axis (host arrays of dims[axis]
  * doubles: kappa_j and the 1D Laplacian term, spectral.py:78-86).  The
  * Python host layer passes numpy's own tables so the device sees the
@@ -111,6 +115,9 @@ int pf_stokes_end(pf_plan* plan, pf_stokes_result* result);
  * events between stages; stage_ms (host, 6 doubles) receives the mean time of
  * S1 spectral | Z2D | S3 local | finalize | S4 form-R | D2Z, in ms. */
 int pf_stokes_profile(pf_plan* plan, int64_t n_iter, double* stage_ms);
+/* Pipeline of the active / last Stokes solve: 0 = cuFFT (stages as above),
+ * 1 = fused (stages PK | MI | RS | finalize | MF | -). */
+int pf_stokes_pipeline(const pf_plan* plan);
 
 /* ------------------------------------------------------------------------
  * Transport — replaces poreflow.transport.solve_transport

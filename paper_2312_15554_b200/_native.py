@@ -82,6 +82,7 @@ SIGNATURES = {
     "pf_plan_create": [ctypes.POINTER(_P), ctypes.c_int, _I64P, ctypes.c_int, ctypes.c_int, _P],
     "pf_plan_destroy": [_P],
     "pf_plan_set_stream": [_P, _P],
+    "pf_plan_set_fused": [_P, ctypes.c_int],
     "pf_plan_set_symbol_tables": [_P, ctypes.c_int, _P, _P],
     "pf_plan_device_bytes": [_P, ctypes.POINTER(ctypes.c_size_t)],
     "pf_stokes_solve": [_P, ctypes.POINTER(StokesParams), _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(StokesResult)],
@@ -89,6 +90,7 @@ SIGNATURES = {
     "pf_stokes_iterate": [_P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(StokesResult)],
     "pf_stokes_end": [_P, ctypes.POINTER(StokesResult)],
     "pf_stokes_profile": [_P, ctypes.c_int64, _DP],
+    "pf_stokes_pipeline": [_P],
     "pf_transport_solve": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_begin": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_iterate": [_P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(TransportResult)],

@@ -1,0 +1,766 @@
+// Fused Stokes ADMM pipeline for cubic power-of-two grids (N = 64, 128, 256).
+//
+// Every 3D transform of the loop is split along its axes and fused with the
+// pointwise / spectral work that consumes it, so each iteration streams the
+// fields through HBM in four passes instead of cuFFT's multi-pass transforms
+// plus separate pointwise kernels:
+//
+//   PK  (axis-0 pencils, tile = (k1, CP columns of k2), all k0):
+//         FFT_0 of R~ = FFT_{2,1}(b u~ - a) -> R^ ; Green's operator (pure.py:26-56),
+//         D^ = i k.U^, Q^' = Q^ - beta D^ (stokes.py:381, 408-409), Parseval sums;
+//         IFFT_0 of U^/n.                                   reads 5 words, writes 5
+//   MI  (axis-1 pencils, tile = (i0, CM columns)): IFFT_1 of U^.   reads 3, writes 3
+//   RS  (rows along axis 2, tile = NG rows): C2R of u' (two rows per complex FFT),
+//         the local projection and multiplier updates + six squared norms
+//         (pure.py:59-68, stokes.py:254-277), R2C of u~' and a' (one complex FFT
+//         per row).                                         reads 15 words, writes 18
+//   F   k_stokes_finalize (shared with the cuFFT pipeline)
+//   MF  (axis-1 pencils): R = b' u~' - a' formed on load (post-adaptation b',
+//         stokes.py:405-407), FFT_1.                         reads 6, writes 3
+//
+// Spectra are stored as [rows][N/2] complex plus a separate Nyquist column
+// [rows] so rows stay 2 KiB aligned.  All FFTs are hand-written radix-8/16
+// Stockham-style passes in registers with one padded shared-memory transpose
+// (fft_seq); a thread group of 8 or 16 lanes transforms one sequence.
+#include <cmath>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+namespace fz {
+
+template <int N>
+struct Cfg {
+  static constexpr int A = (N == 64) ? 8 : 16;  // radix of pass 1 (and stride of pass-1 stores)
+  static constexpr int B = N / A;               // radix of pass 2
+  static constexpr int G = A > B ? A : B;       // lanes per FFT group
+  static constexpr int NG = 256 / G;            // groups per 256-thread block
+  static constexpr int SS = N + N / A + 1;      // padded smem sequence stride (complex)
+  static constexpr int H = N / 2;               // stored half-spectrum columns (k2 < N/2)
+  static constexpr int RSR = NG;                // rows per RS tile
+  static constexpr int CM = NG;                 // k2 columns per MF / MI tile
+  static constexpr int CP = NG / 2;             // k2 columns per PK tile
+  static constexpr int NCHM = H / CM;           // column chunks per i0 (M kernels)
+  static constexpr int NCHP = H / CP;           // column chunks per k1 (PK)
+  static constexpr int M_TILES = N * NCHM + N / CM;
+  static constexpr int PK_TILES = N * NCHP + N / CP;
+  static constexpr int RS_TILES = N * N / RSR;
+  static __device__ __forceinline__ int pad(int e) { return e + e / A; }
+};
+
+// cos(2 pi m / 16)
+__device__ __forceinline__ double c16(int m) {
+  switch (m & 15) {
+    case 0: return 1.0;
+    case 1: case 15: return 0.92387953251128675613;
+    case 2: case 14: return 0.70710678118654752440;
+    case 3: case 13: return 0.38268343236508977173;
+    case 4: case 12: return 0.0;
+    case 5: case 11: return -0.38268343236508977173;
+    case 6: case 10: return -0.70710678118654752440;
+    case 7: case 9: return -0.92387953251128675613;
+    default: return -1.0;
+  }
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(__fma_rn(a.x, b.x, -(a.y * b.y)), __fma_rn(a.x, b.y, a.y * b.x));
+}
+
+
+// ---- TMA bulk copies (cp.async.bulk -> UBLKCP) completed on an mbarrier
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(m)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}" ::"r"(
+          su32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// x * exp(-+ 2 pi i m / 16): forward uses the minus sign.
+template <bool INV>
+__device__ __forceinline__ double2 rot16(double2 x, int m) {
+  m &= 15;
+  if (m == 0) return x;
+  if (m == 8) return make_double2(-x.x, -x.y);
+  if (m == 4) return INV ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
+  if (m == 12) return INV ? make_double2(x.y, -x.x) : make_double2(-x.y, x.x);
+  const double c = c16(m), s0 = c16(m - 4);  // sin(2 pi m/16)
+  const double s = INV ? s0 : -s0;
+  return make_double2(__fma_rn(x.x, c, -(x.y * s)), __fma_rn(x.x, s, x.y * c));
+}
+
+template <int R, bool INV>
+struct Dft;
+
+template <bool INV>
+struct Dft<2, INV> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  }
+};
+
+template <bool INV>
+struct Dft<4, INV> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double2 s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
+    const double2 s13 = cadd(x[1], x[3]), d13 = csub(x[1], x[3]);
+    // forward: X1 = d02 - i d13, X3 = d02 + i d13
+    const double2 jd = INV ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
+    x[0] = cadd(s02, s13);
+    x[2] = csub(s02, s13);
+    x[1] = cadd(d02, jd);
+    x[3] = csub(d02, jd);
+  }
+};
+
+// R = P * Q four-step in registers: n = Q n1 + n2, k = k1 + P k2.
+template <int P, int Q, bool INV>
+__device__ __forceinline__ void dft_pq(double2* x) {
+  constexpr int R = P * Q;
+  double2 y[R];
+#pragma unroll
+  for (int n2 = 0; n2 < Q; ++n2) {
+    double2 t[P];
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) t[n1] = x[Q * n1 + n2];
+    Dft<P, INV>::run(t);
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) y[n2 * P + k1] = rot16<INV>(t[k1], (n2 * k1) * (16 / R));
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) {
+    double2 t[Q];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) t[n2] = y[n2 * P + k1];
+    Dft<Q, INV>::run(t);
+#pragma unroll
+    for (int k2 = 0; k2 < Q; ++k2) x[k1 + P * k2] = t[k2];
+  }
+}
+
+template <bool INV>
+struct Dft<8, INV> {
+  static __device__ __forceinline__ void run(double2* x) { dft_pq<4, 2, INV>(x); }
+};
+template <bool INV>
+struct Dft<16, INV> {
+  static __device__ __forceinline__ void run(double2* x) { dft_pq<4, 4, INV>(x); }
+};
+
+// One N-point complex FFT (unnormalised) of the padded smem sequence s by the
+// G lanes of a group (lane l).  Pass 1: B sub-FFTs of size A over stride-B
+// elements + twiddles; pass 2: A sub-FFTs of size B.  Output in natural order.
+// Every lane of the warp must call this (it uses __syncwarp); `active` = false
+// makes a group participate without touching memory.
+template <int N, bool INV>
+__device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ tw, int l, bool active) {
+  using C = Cfg<N>;
+  constexpr int A = C::A, B = C::B;
+  double2 x[A > B ? A : B];
+  const bool p1 = active && l < B, p2 = active && l < A;
+  if (p1) {
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
+    Dft<A, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < A; ++k1) {
+      double2 w = tw[l * k1];
+      if (INV) w.y = -w.y;
+      x[k1] = cmul(x[k1], w);
+    }
+  }
+  __syncwarp();
+  if (p1) {
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) s[C::pad(k1 + A * l)] = x[k1];
+  }
+  __syncwarp();
+  if (p2) {
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) x[n2] = s[C::pad(l + A * n2)];
+    Dft<B, INV>::run(x);
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) s[C::pad(l + A * k2)] = x[k2];
+  }
+  __syncwarp();
+}
+
+struct Bufs {
+  double2 *XU, *XUn;  // X-space (after axis 2): u' in, u~' out   [3][N*N][H], [3][N*N]
+  double2 *XA, *XAn;  // X-space a'
+  double2 *Y, *Yn;    // Y-space (after axes 2,1): R~ in, U^ out  [3][N][N][H], [3][N][N]
+  double2 *Q, *Qn;    // full spectrum Q^   [N][N][H], [N][N]
+  double2 *D, *Dn;    // full spectrum D^_prev
+  double2* tw;        // N forward twiddles
+  double *part_rs, *part_pk;
+};
+
+struct State {
+  double *u, *ut, *a, *lam;
+  const uint8_t* H;
+};
+
+template <int N>
+__device__ __forceinline__ void load_tw(double2* tw, const double2* __restrict__ g) {
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tw[j] = g[j];
+}
+
+// ------------------------------------------------------------------ RS
+// Persistent: grid = 3 blocks per SM; each block walks tiles of R2 rows of one
+// velocity component.  Per tile, one thread issues TMA bulk copies of the
+// state rows (u, u~, a, lam), the X-space u' rows and the indicator into
+// shared memory (one mbarrier); the next tile's copies are issued as soon as
+// the current tile's staged inputs are consumed, so they overlap the forward
+// FFT and the output stores.  State outputs go straight to HBM.
+template <int N>
+struct RS2 {
+  using C = Cfg<N>;
+  static constexpr int R = 1024 / N;            // rows per tile (1024 voxels)
+  static constexpr int T = R * C::G;            // threads per block: one FFT group per row
+  static constexpr int V = R * N;               // voxels per tile
+  static constexpr int VPT = V / T;             // voxels per thread
+  static constexpr int NP = R / 2;              // inverse sequences (two rows each)
+  // shared-memory carve (bytes)
+  static constexpr size_t TW = sizeof(double2) * N;
+  static constexpr size_t INV = sizeof(double2) * NP * C::SS;
+  static constexpr size_t FWD = sizeof(double2) * R * C::SS;
+  static constexpr size_t ST = sizeof(double) * 4 * V;     // u, u~, a, lam rows
+  static constexpr size_t XM = sizeof(double2) * R * C::H; // X-space u' rows (main)
+  static constexpr size_t XN = sizeof(double2) * R;        // nyq column
+  static constexpr size_t HB = V;                          // indicator bytes
+  static constexpr size_t BYTES = TW + INV + FWD + ST + XM + XN + HB;
+  static constexpr uint32_t TX = (uint32_t)(ST + XM + XN + HB);
+};
+
+template <int N>
+__device__ __forceinline__ void rs_issue(int tile, const Bufs& B, const State& st, double* sst, double2* sx,
+                                         double2* sxn, uint8_t* sh, uint64_t* mbar) {
+  using K = RS2<N>;
+  using C = Cfg<N>;
+  constexpr int TPC = N * N / K::R;  // tiles per component
+  const int c = tile / TPC;
+  const int64_t row0 = (int64_t)(tile % TPC) * K::R;
+  const int64_t n = (int64_t)N * N * N;
+  const int64_t x0 = (int64_t)c * n + row0 * N;
+  const uint32_t vb = sizeof(double) * K::V;
+  fence_async_smem();
+  mbar_expect(mbar, K::TX);
+  bulk_load(sst + 0 * K::V, st.u + x0, vb, mbar);
+  bulk_load(sst + 1 * K::V, st.ut + x0, vb, mbar);
+  bulk_load(sst + 2 * K::V, st.a + x0, vb, mbar);
+  bulk_load(sst + 3 * K::V, st.lam + x0, vb, mbar);
+  bulk_load(sx, B.XU + ((int64_t)c * N * N + row0) * C::H, (uint32_t)K::XM, mbar);
+  bulk_load(sxn, B.XUn + (int64_t)c * N * N + row0, (uint32_t)K::XN, mbar);
+  bulk_load(sh, st.H + row0 * N, (uint32_t)K::HB, mbar);
+}
+
+template <int N>
+__global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = RS2<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
+  constexpr int TPC = N * N / R;
+  constexpr int NT = 3 * TPC;
+  if (ctrl->done) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  __shared__ uint64_t mbar;
+  double2* tw = (double2*)sraw;
+  double2* SI = (double2*)(sraw + K::TW);
+  double2* SF = (double2*)(sraw + K::TW + K::INV);
+  double* sst = (double*)(sraw + K::TW + K::INV + K::FWD);
+  double2* sx = (double2*)(sraw + K::TW + K::INV + K::FWD + K::ST);
+  double2* sxn = (double2*)(sraw + K::TW + K::INV + K::FWD + K::ST + K::XM);
+  uint8_t* sh = (uint8_t*)(sraw + K::TW + K::INV + K::FWD + K::ST + K::XM + K::XN);
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  const double alpha = ctrl->alpha, b = ctrl->b;
+  const int64_t n = (int64_t)N * N * N;
+  if (t == 0) {
+    mbar_init(&mbar);
+    if ((int)blockIdx.x < NT) rs_issue<N>(blockIdx.x, B, st, sst, sx, sxn, sh, &mbar);
+  }
+  __syncthreads();
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    double2* XU = B.XU + (size_t)c * N * N * H;
+    double2* XUn = B.XUn + (size_t)c * N * N;
+    double2* XA = B.XA + (size_t)c * N * N * H;
+    double2* XAn = B.XAn + (size_t)c * N * N;
+    mbar_wait(&mbar, phase);
+    // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      double2 xa = sx[(2 * p) * H + k], xb = sx[(2 * p + 1) * H + k];
+      if (k == 0) xa.y = xb.y = 0.0;  // C2R keeps the real part of self-conjugate modes
+      double2* sp = SI + p * SS;
+      sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+      if (k > 0) sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+    }
+    for (int p = t; p < NP; p += T) SI[p * SS + C::pad(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
+    __syncthreads();
+    fft_seq<N, true>(SI + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    __syncthreads();
+    // (2) local projection + multipliers (pure.py:59-68) and six squared norms
+#pragma unroll 4
+    for (int j = 0; j < K::VPT; ++j) {
+      const int v = t + T * j, row = v / N, col = v % N;
+      const double2 z = SI[(row >> 1) * SS + C::pad(col)];
+      const double u1 = (row & 1) ? z.y : z.x;
+      const double h = (double)sh[v];
+      const double u0 = sst[v], t0 = sst[V + v], a0 = sst[2 * V + v], l0 = sst[3 * V + v];
+      const double t1 = ((a0 + b * u1) - h * l0) / (b + alpha * h);
+      const double a1 = a0 + b * (u1 - t1);
+      const double l1 = l0 + alpha * (h * t1);
+      const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
+      acc[0] += s0 * s0;
+      acc[1] += s1 * s1;
+      acc[2] += l1 * l1;
+      acc[3] += s3 * s3;
+      acc[4] += s4 * s4;
+      acc[5] += a1 * a1;
+      const int64_t i = c * n + row0 * N + v;
+      st.u[i] = u1;
+      st.ut[i] = t1;
+      st.a[i] = a1;
+      st.lam[i] = l1;
+      SF[row * SS + C::pad(col)] = make_double2(t1, a1);  // z = u~' + i a'
+    }
+    __syncthreads();
+    // staged inputs consumed: prefetch the next tile while this one finishes
+    if (t == 0 && tile + (int)gridDim.x < NT) rs_issue<N>(tile + gridDim.x, B, st, sst, sx, sxn, sh, &mbar);
+    fft_seq<N, false>(SF + g * SS, tw, l, true);
+    __syncthreads();
+    // (3) separate the two real transforms, store X-space rows of u~' (in place of u') and a'
+    for (int idx = t; idx < R * H; idx += T) {
+      const int r = idx / H, k = idx % H;
+      const double2 zk = SF[r * SS + C::pad(k)], zm = SF[r * SS + C::pad((N - k) & (N - 1))];
+      XU[(row0 + r) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XA[(row0 + r) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+    for (int r = t; r < R; r += T) {
+      const double2 z = SF[r * SS + C::pad(H)];
+      XUn[row0 + r] = make_double2(z.x, 0.0);
+      XAn[row0 + r] = make_double2(z.y, 0.0);
+    }
+    __syncthreads();
+  }
+  block_sum<6>(acc);
+  if (t == 0)
+    for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// ------------------------------------------------------------------ MF / MI
+// Axis-1 pencils.  FWD: X-space (u~', a') -> Y-space R~ = FFT_1(b' u~' - a').
+//                  INV: Y-space U^ -> X-space u' (IFFT_1).
+template <int N, bool INV>
+__global__ void __launch_bounds__(256) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  constexpr int H = C::H, SS = C::SS, CM = C::CM, NCH = C::NCHM;
+  if (ctrl->done) return;
+  extern __shared__ double2 smem[];
+  double2* tw = smem;
+  double2* S = smem + N;
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  load_tw<N>(tw, B.tw);
+  const double b = ctrl->b;
+  const int tile = blockIdx.x;
+  const bool nyq = tile >= N * NCH;
+  const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
+  const int i0b = nyq ? (tile - N * NCH) * CM : 0;
+  __syncthreads();
+  for (int c = 0; c < 3; ++c) {
+    for (int idx = t; idx < N * CM; idx += 256) {
+      int e, q;  // element along axis 1, sequence
+      size_t off;
+      if (!nyq) {
+        q = idx % CM;
+        e = idx / CM;
+        off = ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
+      } else {
+        q = idx / N;
+        e = idx % N;
+        off = (size_t)(c * N + i0b + q) * N + e;
+      }
+      double2 v;
+      if (!INV) {
+        const double2 vu = nyq ? B.XUn[off] : B.XU[off];
+        const double2 va = nyq ? B.XAn[off] : B.XA[off];
+        v = make_double2(b * vu.x - va.x, b * vu.y - va.y);
+      } else {
+        v = nyq ? B.Yn[off] : B.Y[off];
+      }
+      S[q * SS + C::pad(e)] = v;
+    }
+    __syncthreads();
+    fft_seq<N, INV>(S + g * SS, tw, l, true);
+    __syncthreads();
+    for (int idx = t; idx < N * CM; idx += 256) {
+      int e, q;
+      size_t off;
+      if (!nyq) {
+        q = idx % CM;
+        e = idx / CM;
+        off = ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
+      } else {
+        q = idx / N;
+        e = idx % N;
+        off = (size_t)(c * N + i0b + q) * N + e;
+      }
+      const double2 v = S[q * SS + C::pad(e)];
+      if (!INV) {
+        if (nyq) B.Yn[off] = v; else B.Y[off] = v;
+      } else {
+        if (nyq) B.XUn[off] = v; else B.XU[off] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ PK
+struct SpecArgs {
+  const double* kap[3];
+  const double* ell[3];
+  double nu, g[3], inv_n, dn;
+};
+
+template <int N>
+__global__ void __launch_bounds__(256) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  constexpr int H = C::H, SS = C::SS, CP = C::CP, NCH = C::NCHP, NSEQ = 3 * CP;
+  if (ctrl->done) return;
+  extern __shared__ double2 smem[];
+  double2* tw = smem;
+  double2* S = smem + N;
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  load_tw<N>(tw, B.tw);
+  const double beta = ctrl->beta, b = ctrl->b;
+  const int tile = blockIdx.x;
+  const bool nyq = tile >= N * NCH;
+  const int k1 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
+  const int k1b = nyq ? (tile - N * NCH) * CP : 0;
+  auto yoff = [&](int c, int i0, int q) -> size_t {
+    return nyq ? (size_t)(c * N + i0) * N + k1b + q : ((size_t)(c * N + i0) * N + k1) * H + ch * CP + q;
+  };
+  for (int idx = t; idx < 3 * N * CP; idx += 256) {
+    const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+    const size_t off = yoff(c, i0, q);
+    S[(c * CP + q) * SS + C::pad(i0)] = nyq ? B.Yn[off] : B.Y[off];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < (NSEQ + C::NG - 1) / C::NG; ++r) {
+    const int sq = g + r * C::NG;
+    fft_seq<N, false>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
+  }
+  __syncthreads();
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int idx = t; idx < N * CP; idx += 256) {
+    const int q = idx % CP, k0 = idx / CP;
+    const int kk1 = nyq ? k1b + q : k1, k2 = nyq ? H : ch * CP + q;
+    const int idx3[3] = {k0, kk1, k2};
+    double kc[3];
+    double L = 0.0, ksq = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      kc[c] = __ldg(P.kap[c] + idx3[c]);
+      L = L + __ldg(P.ell[c] + idx3[c]);
+      ksq = ksq + kc[c] * kc[c];
+    }
+    const size_t qo = nyq ? (size_t)k0 * N + kk1 : ((size_t)k0 * N + kk1) * H + k2;
+    const double2 qv = nyq ? B.Qn[qo] : B.Q[qo];
+    const bool zero = (k0 | kk1 | k2) == 0;
+    double2 r[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double2 rc = S[(c * CP + q) * SS + C::pad(k0)];
+      r[c] = make_double2(kc[c] * qv.y + rc.x, -(kc[c] * qv.x) + rc.y);
+      if (zero) r[c].x = r[c].x + P.dn * P.g[c];
+    }
+    const double A = P.nu * L + b;
+    double2 kr = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) kr = cadd(kr, cscale(kc[c], r[c]));
+    const double f = beta / (A + beta * ksq);
+    const double2 corr = cscale(f, kr);
+    const double invA = 1.0 / A;
+    double2 dv = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double2 u = csub(r[c], cscale(kc[c], corr));
+      u = make_double2(u.x * invA, u.y * invA);
+      dv = cadd(dv, cik(kc[c], u));
+      S[(c * CP + q) * SS + C::pad(k0)] = make_double2(u.x * P.inv_n, u.y * P.inv_n);
+    }
+    double2 qn = csub(qv, cscale(beta, dv));
+    if (zero) qn = make_double2(0.0, 0.0);
+    const double2 dprev = nyq ? B.Dn[qo] : B.D[qo];
+    const double w = (k2 == 0 || k2 == H) ? 1.0 : 2.0;
+    acc[0] += w * cabs2(dv);
+    acc[1] += w * cabs2(csub(dv, dprev));
+    acc[2] += w * cabs2(qn);
+    if (nyq) {
+      B.Qn[qo] = qn;
+      B.Dn[qo] = dv;
+    } else {
+      B.Q[qo] = qn;
+      B.D[qo] = dv;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < (NSEQ + C::NG - 1) / C::NG; ++r) {
+    const int sq = g + r * C::NG;
+    fft_seq<N, true>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
+  }
+  __syncthreads();
+  for (int idx = t; idx < 3 * N * CP; idx += 256) {
+    const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+    const size_t off = yoff(c, i0, q);
+    const double2 v = S[(c * CP + q) * SS + C::pad(i0)];
+    if (nyq) B.Yn[off] = v; else B.Y[off] = v;
+  }
+  block_sum<3>(acc);
+  if (t == 0)
+    for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// ------------------------------------------------------------------ layout conversion (setup / teardown)
+// natural [rows][N/2+1] <-> fused [rows][N/2] + nyq [rows]
+__global__ void k_split(int64_t rows, int N, const double2* __restrict__ src, double2* __restrict__ main,
+                        double2* __restrict__ nyqv) {
+  const int H = N / 2, W = H + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * W; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / W;
+    const int k = (int)(i % W);
+    if (k < H) main[r * H + k] = src[i]; else nyqv[r] = src[i];
+  }
+}
+
+__global__ void k_merge(int64_t rows, int N, const double2* __restrict__ main, const double2* __restrict__ nyqv,
+                        double2* __restrict__ dst, double scale) {
+  const int H = N / 2, W = H + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * W; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / W;
+    const int k = (int)(i % W);
+    const double2 v = k < H ? main[r * H + k] : nyqv[r];
+    dst[i] = make_double2(v.x * scale, v.y * scale);
+  }
+}
+
+}  // namespace fz
+
+// ------------------------------------------------------------------ host
+struct FusedPlan {
+  int N = 0;
+  fz::Bufs b{};
+  void* mem = nullptr;
+  cufftHandle plan2d = 0;
+  size_t bytes = 0;
+};
+
+static FusedPlan* fp_of(pf_plan* p) { return reinterpret_cast<FusedPlan*>(p->fused); }
+
+bool fused_supported(const pf_plan* p) {
+  if (p->g.d != 3) return false;
+  const int N = p->g.n[0];
+  if (p->g.n[1] != N || p->g.n[2] != N) return false;
+  return N == 64 || N == 128 || N == 256;
+}
+
+template <int N>
+static size_t smem_m() { return sizeof(double2) * (N + fz::Cfg<N>::NG * fz::Cfg<N>::SS); }
+template <int N>
+static size_t smem_rs() { return fz::RS2<N>::BYTES; }
+constexpr int kRsBlocks = kSMs * 3;  // persistent RS grid: 3 blocks per SM
+template <int N>
+static size_t smem_pk() { return sizeof(double2) * (N + 3 * fz::Cfg<N>::CP * fz::Cfg<N>::SS); }
+
+template <int N>
+static int set_attrs() {
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
+  return PF_OK;
+}
+
+int fused_ensure(pf_plan* p) {
+  if (p->fused) return PF_OK;
+  const int N = p->g.n[0];
+  FusedPlan* f = new FusedPlan();
+  f->N = N;
+  const size_t H = N / 2, NN = (size_t)N * N;
+  const size_t main1 = NN * H, nyq1 = NN;  // one component, complex elements
+  // X: 6 comps (XU 3, XA 3); Y: 3; Q, D: 1 each
+  const size_t elems = 11 * (main1 + nyq1) + N;
+  const int nb_rs = kRsBlocks;
+  const int nb_pk = (N == 64) ? (N * 2 + N / 16) : (N * (N / 16) + N / 8);
+  const size_t part = 6 * (size_t)nb_rs + 3 * (size_t)nb_pk;
+  f->bytes = elems * sizeof(double2) + part * sizeof(double);
+  PF_CK_CUDA(cudaMalloc(&f->mem, f->bytes));
+  double2* m = (double2*)f->mem;
+  auto take = [&](size_t n) {
+    double2* r = m;
+    m += n;
+    return r;
+  };
+  f->b.XU = take(3 * main1);
+  f->b.XA = take(3 * main1);
+  f->b.Y = take(3 * main1);
+  f->b.Q = take(main1);
+  f->b.D = take(main1);
+  f->b.XUn = take(3 * nyq1);
+  f->b.XAn = take(3 * nyq1);
+  f->b.Yn = take(3 * nyq1);
+  f->b.Qn = take(nyq1);
+  f->b.Dn = take(nyq1);
+  f->b.tw = take(N);
+  f->b.part_rs = (double*)m;
+  f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
+  std::vector<double2> tw(N);
+  for (int j = 0; j < N; ++j) {
+    const double a = 2.0 * M_PI * (double)j / (double)N;
+    tw[j] = make_double2(std::cos(a), -std::sin(a));
+  }
+  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+  // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
+  // right-hand side at setup time.
+  size_t ws = 0;
+  long long dims2[2] = {N, N};
+  PF_CK_FFT(cufftCreate(&f->plan2d));
+  PF_CK_FFT(cufftSetAutoAllocation(f->plan2d, 0));
+  PF_CK_FFT(cufftMakePlanMany64(f->plan2d, 2, dims2, nullptr, 1, (long long)NN, nullptr, 1,
+                                (long long)N * (H + 1), CUFFT_D2Z, 3LL * N, &ws));
+  if (ws > p->fft_work_bytes) {
+    PF_CK_CUDA(cudaStreamSynchronize(p->work));
+    if (p->fft_work) PF_CK_CUDA(cudaFree(p->fft_work));
+    PF_CK_CUDA(cudaMalloc(&p->fft_work, ws));
+    p->fft_work_bytes = ws;
+    for (int k = 0; k < 4; ++k) {
+      if (p->fwd[k]) PF_CK_FFT(cufftSetWorkArea(p->fwd[k], p->fft_work));
+      if (p->inv[k]) PF_CK_FFT(cufftSetWorkArea(p->inv[k], p->fft_work));
+    }
+    p->graph.reset();
+  }
+  PF_CK_FFT(cufftSetWorkArea(f->plan2d, p->fft_work));
+  PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
+  switch (N) {
+    case 64: PF_CK(set_attrs<64>()); break;
+    case 128: PF_CK(set_attrs<128>()); break;
+    default: PF_CK(set_attrs<256>()); break;
+  }
+  p->fused = f;
+  p->scratch_bytes += f->bytes;
+  return PF_OK;
+}
+
+void fused_free(pf_plan* p) {
+  FusedPlan* f = fp_of(p);
+  if (!f) return;
+  if (f->plan2d) cufftDestroy(f->plan2d);
+  cudaFree(f->mem);
+  delete f;
+  p->fused = nullptr;
+}
+
+// Setup: Q^, D^_prev and the Y-space right-hand side from the real state.
+int fused_setup(pf_plan* p) {
+  FusedPlan* f = fp_of(p);
+  const int N = f->N;
+  const int64_t n = p->g.nr, nh = p->g.nh, NN = (int64_t)N * N;
+  const int grid = blocks_for(nh * 3);
+  // Q^ = FFT(q), gauge Q^(0) = 0
+  PF_CK(plan_fft(p, true, 1, p->s_q, p->specB));
+  fz::k_split<<<grid, kThreads, 0, p->work>>>(NN, N, p->specB, f->b.Q, f->b.Qn);
+  PF_CK_CUDA(cudaMemsetAsync(f->b.Q, 0, sizeof(double2), p->work));
+  // D^_prev = i k . FFT(u)
+  PF_CK(stokes_div_spectrum(p, p->s_u, p->specB, p->spec2));
+  fz::k_split<<<grid, kThreads, 0, p->work>>>(NN, N, p->spec2, f->b.D, f->b.Dn);
+  // Y-space R~ = FFT_{2,1}(b u~ - a)
+  PF_CK(stokes_form_r(p, p->realB));
+  PF_CK_FFT(cufftExecD2Z(f->plan2d, (cufftDoubleReal*)p->realB, (cufftDoubleComplex*)p->specA));
+  fz::k_split<<<grid, kThreads, 0, p->work>>>(3 * NN, N, p->specA, f->b.Y, f->b.Yn);
+  PF_CK_CUDA(cudaGetLastError());
+  (void)n;
+  return PF_OK;
+}
+
+// q = Re ifft(Q^) into the user's q.
+int fused_finish(pf_plan* p) {
+  FusedPlan* f = fp_of(p);
+  const int N = f->N;
+  const int64_t NN = (int64_t)N * N;
+  fz::k_merge<<<blocks_for(p->g.nh), kThreads, 0, p->work>>>(NN, N, f->b.Q, f->b.Qn, p->specB, p->g.inv_n);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
+  return PF_OK;
+}
+
+template <int N>
+static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
+  using C = fz::Cfg<N>;
+  FusedPlan* f = fp_of(p);
+  fz::State st{p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid};
+  fz::SpecArgs sa;
+  for (int i = 0; i < 3; ++i) {
+    sa.kap[i] = p->kap[i];
+    sa.ell[i] = p->ell[i];
+    sa.g[i] = p->sc.g[i];
+  }
+  sa.nu = p->sc.nu;
+  sa.inv_n = p->g.inv_n;
+  sa.dn = p->g.dn;
+  auto mark = [&](int i) -> int {
+    if (ev) PF_CK_CUDA(cudaEventRecord(ev[i], p->work));
+    return PF_OK;
+  };
+  PF_CK(mark(0));
+  fz::k_pk<N><<<C::PK_TILES, 256, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(1));
+  fz::k_maxis<N, true><<<C::M_TILES, 256, smem_m<N>(), p->work>>>(f->b, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(2));
+  fz::k_rs<N><<<kRsBlocks, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(3));
+  k_stokes_finalize_launch(p, f->b.part_rs, kRsBlocks, f->b.part_pk, C::PK_TILES);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(4));
+  fz::k_maxis<N, false><<<C::M_TILES, 256, smem_m<N>(), p->work>>>(f->b, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(5));
+  PF_CK(mark(6));
+  return PF_OK;
+}
+
+int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {
+  switch (fp_of(p)->N) {
+    case 64: return enqueue_fused_t<64>(p, ev);
+    case 128: return enqueue_fused_t<128>(p, ev);
+    default: return enqueue_fused_t<256>(p, ev);
+  }
+}
+
+}  // namespace pf

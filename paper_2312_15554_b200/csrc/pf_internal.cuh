@@ -142,6 +142,10 @@ struct pf_plan {
   pf::Ctrl* h_ctrl;   // pinned host, 2 slots for double-buffered polling
   double* h_small;    // pinned host scratch (64 doubles)
   size_t scratch_bytes;
+  // fused power-of-two pipeline (pf_fused.cu)
+  void* fused;       // FusedPlan*
+  int fused_enable;  // 1 = use the fused pipeline when the grid supports it
+  int pipeline;      // pipeline of the active Stokes solve: 0 cuFFT, 1 fused
   // active solve state
   int active;  // 0 none, 1 stokes, 2 transport
   pf::Graph graph;
@@ -164,6 +168,18 @@ int enter(pf_plan* p);  // order plan->work after user stream
 int leave(pf_plan* p);  // order user stream after plan->work
 int run_chunks(pf_plan* p, int64_t n_iter, int poll, int (*enqueue)(pf_plan*), Ctrl* out_ctrl);
 int symbol_tables_for(int mode, int n, std::vector<double>& kap, std::vector<double>& ell);
+
+// fused pipeline (pf_fused.cu)
+bool fused_supported(const pf_plan* p);
+int fused_ensure(pf_plan* p);
+void fused_free(pf_plan* p);
+int fused_setup(pf_plan* p);
+int fused_finish(pf_plan* p);
+int enqueue_fused(pf_plan* p, cudaEvent_t* ev);
+// Stokes helpers shared with the fused pipeline (pf_stokes.cu)
+int stokes_div_spectrum(pf_plan* p, const double* u, double2* tmp, double2* out);
+int stokes_form_r(pf_plan* p, double* R);
+void k_stokes_finalize_launch(pf_plan* p, const double* part3, int nb3, const double* part1, int nb1);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }

@@ -251,6 +251,7 @@ int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode
   p->mode = symbol_mode;
   p->device = device;
   p->user_stream = (cudaStream_t)stream;
+  p->fused_enable = 1;
   PF_CK_CUDA(cudaStreamCreateWithFlags(&p->work, cudaStreamNonBlocking));
   PF_CK_CUDA(cudaEventCreateWithFlags(&p->ev_user, cudaEventDisableTiming));
   PF_CK_CUDA(cudaEventCreateWithFlags(&p->ev_work, cudaEventDisableTiming));
@@ -291,6 +292,16 @@ int pf_plan_set_symbol_tables(pf_plan* p, int axis, const double* kappa_host, co
   return PF_OK;
 }
 
+int pf_plan_set_fused(pf_plan* p, int enable) {
+  PF_ARG(p, "null plan");
+  if (p->active) {
+    set_error("pf_plan_set_fused while a solve is active");
+    return PF_ERR_STATE;
+  }
+  p->fused_enable = enable ? 1 : 0;
+  return PF_OK;
+}
+
 int pf_plan_set_stream(pf_plan* p, void* stream) {
   PF_ARG(p, "null plan");
   p->user_stream = (cudaStream_t)stream;
@@ -308,6 +319,7 @@ int pf_plan_destroy(pf_plan* p) {
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->work);
   p->graph.reset();
+  fused_free(p);
   for (int k = 0; k < 4; ++k) {
     if (p->fwd[k]) cufftDestroy(p->fwd[k]);
     if (p->inv[k]) cufftDestroy(p->inv[k]);

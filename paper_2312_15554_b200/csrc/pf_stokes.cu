@@ -301,6 +301,7 @@ static int enqueue_stokes_t(pf_plan* p, cudaEvent_t* ev = nullptr) {
 }
 
 static int enqueue_stokes(pf_plan* p) {
+  if (p->pipeline == 1) return enqueue_fused(p, nullptr);
   switch (p->g.d) {
     case 1: return enqueue_stokes_t<1>(p);
     case 2: return enqueue_stokes_t<2>(p);
@@ -309,11 +310,41 @@ static int enqueue_stokes(pf_plan* p) {
 }
 
 static int enqueue_stokes_ev(pf_plan* p, cudaEvent_t* ev) {
+  if (p->pipeline == 1) return enqueue_fused(p, ev);
   switch (p->g.d) {
     case 1: return enqueue_stokes_t<1>(p, ev);
     case 2: return enqueue_stokes_t<2>(p, ev);
     default: return enqueue_stokes_t<3>(p, ev);
   }
+}
+
+int stokes_div_spectrum(pf_plan* p, const double* u, double2* tmp, double2* out) {
+  const int d = p->g.d;
+  PF_CK(plan_fft(p, true, d, (void*)u, tmp));
+  const int nb = blocks_for(p->g.nh);
+  switch (d) {
+    case 1: k_div_spectrum<1><<<nb, kThreads, 0, p->work>>>(p->g, tables_of(p), tmp, out); break;
+    case 2: k_div_spectrum<2><<<nb, kThreads, 0, p->work>>>(p->g, tables_of(p), tmp, out); break;
+    default: k_div_spectrum<3><<<nb, kThreads, 0, p->work>>>(p->g, tables_of(p), tmp, out); break;
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+int stokes_form_r(pf_plan* p, double* R) {
+  const int64_t n = p->g.nr;
+  switch (p->g.d) {
+    case 1: k_form_r<1><<<blocks_for(n), kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 0); break;
+    case 2: k_form_r<2><<<blocks_for(n), kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 0); break;
+    default: k_form_r<3><<<blocks_for(n), kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 0); break;
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+void k_stokes_finalize_launch(pf_plan* p, const double* part3, int nb3, const double* part1, int nb1) {
+  k_stokes_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, part3, nb3, part1, nb1, p->s_hist, p->sc,
+                                                          p->g.inv_n);
 }
 
 template <int D>
@@ -375,6 +406,12 @@ int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid,
   p->graph.reset();
   k_ctrl_init<<<1, 1, 0, p->work>>>(p->ctrl, P->alpha, P->beta, P->b);
   PF_CK_CUDA(cudaGetLastError());
+  p->pipeline = (p->fused_enable && fused_supported(p)) ? 1 : 0;
+  if (p->pipeline == 1) {
+    PF_CK(fused_ensure(p));
+    PF_CK(fused_setup(p));
+    return PF_OK;
+  }
   switch (d) {
     case 1: PF_CK(stokes_setup_t<1>(p, P->b)); break;
     case 2: PF_CK(stokes_setup_t<2>(p, P->b)); break;
@@ -412,9 +449,13 @@ int pf_stokes_end(pf_plan* p, pf_stokes_result* res) {
   }
   // q = Re ifft(Q^): copy (Z2D overwrites its input), fold 1/n, transform.
   const int64_t nh = p->g.nh;
-  k_scale_copy<<<blocks_for(nh), kThreads, 0, p->work>>>(nh, p->spec1, p->specB, p->g.inv_n);
-  PF_CK_CUDA(cudaGetLastError());
-  PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
+  if (p->pipeline == 1) {
+    PF_CK(fused_finish(p));
+  } else {
+    k_scale_copy<<<blocks_for(nh), kThreads, 0, p->work>>>(nh, p->spec1, p->specB, p->g.inv_n);
+    PF_CK_CUDA(cudaGetLastError());
+    PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
+  }
   PF_CK_CUDA(cudaMemcpyAsync(&p->h_ctrl[0], p->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, p->work));
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
   const Ctrl c = p->h_ctrl[0];
@@ -461,6 +502,8 @@ int pf_stokes_profile(pf_plan* p, int64_t n_iter, double* stage_ms) {
   for (int k = 0; k < 6; ++k) stage_ms[k] = acc[k] / (double)n_iter;
   return leave(p);
 }
+
+int pf_stokes_pipeline(const pf_plan* p) { return p ? p->pipeline : -1; }
 
 int pf_stokes_solve(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
                     double* a, double* lam, double* history, pf_stokes_result* res) {

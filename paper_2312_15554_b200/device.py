@@ -114,6 +114,8 @@ def to_device(arr, device, dtype=None):
         x = arr.to(device=device, dtype=dtype or arr.dtype)
         return x.contiguous()
     a = np.ascontiguousarray(arr, dtype=dtype and _np_dtype(dtype))
+    if not a.flags.writeable:
+        a = a.copy()
     return t.from_numpy(a).to(device=device, non_blocking=False)
 
 

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -211,7 +212,8 @@ class StokesSolver:
     """
 
     def __init__(self, indicator: IndicatorField, cfg: StokesConfig, penalties: PenaltyParams,
-                 state: DeviceAdmmState, device=None, history_rows: int | None = None):
+                 state: DeviceAdmmState, device=None, history_rows: int | None = None,
+                 pipeline: str | None = None):
         self.device = require_cuda(device)
         self.indicator, self.cfg, self.penalties, self.state = indicator, cfg, penalties, state
         grid = indicator.grid
@@ -223,15 +225,26 @@ class StokesSolver:
         self.result = N.StokesResult()
         self._params = _params(cfg, penalties, min(cfg.max_iter, self.rows))
         self._begun = False
+        self.pipeline_request = pipeline or os.environ.get("POREFLOW_B200_PIPELINE", "auto")
+        if self.pipeline_request not in ("auto", "fused", "cufft"):
+            raise ValueError("pipeline must be 'auto', 'fused' or 'cufft'")
+
+    @property
+    def pipeline(self) -> str:
+        """Pipeline the device chose for this solve: 'fused' (N^3, N in 64/128/256) or 'cufft'."""
+        return {0: "cufft", 1: "fused"}.get(N.load().pf_stokes_pipeline(self.plan.handle), "none")
 
     def begin(self):
         lib = N.load()
         s = self.state
         h = self.plan.bind_stream()
+        N.check(lib.pf_plan_set_fused(h, 0 if self.pipeline_request == "cufft" else 1))
         N.check(lib.pf_stokes_begin(h, ctypes.byref(self._params), self.solid.data_ptr(), s.u.data_ptr(),
                                     s.u_tilde.data_ptr(), s.q.data_ptr(), s.a.data_ptr(), s.lam.data_ptr(),
                                     self.history.data_ptr()))
         self._begun = True
+        if self.pipeline_request == "fused" and self.pipeline != "fused":
+            raise ValueError(f"fused pipeline unsupported for grid {self.indicator.grid.dims}")
         return self
 
     def iterate(self, n_iter: int, poll: bool = True):
@@ -254,11 +267,12 @@ class StokesSolver:
             REPORT_COLUMNS, hist, converged=bool(self.result.converged), iterations=it,
             meta={"symbol_mode": self.cfg.symbol_mode, "eps_abs": self.cfg.eps_abs,
                   "eps_rel": self.cfg.eps_rel, "nu": self.cfg.nu, "pressure_gradient": g_p,
-                  "final_penalties": fp})
+                  "final_penalties": fp, "pipeline": self.pipeline})
 
 
 def solve_stokes_device(indicator: IndicatorField, cfg: StokesConfig | None = None,
-                        penalties: PenaltyParams | None = None, init=None, device=None):
+                        penalties: PenaltyParams | None = None, init=None, device=None,
+                        pipeline: str | None = None):
     """Device-resident ``solve_stokes``: returns (DeviceAdmmState, ConvergenceReport)."""
     cfg = cfg or StokesConfig()
     penalties = penalties or PenaltyParams()
@@ -280,7 +294,7 @@ def solve_stokes_device(indicator: IndicatorField, cfg: StokesConfig | None = No
             state = DeviceAdmmState.from_host(init, dev)
     else:
         state = DeviceAdmmState.zeros(grid, dev)
-    solver = StokesSolver(indicator, cfg, penalties, state, dev)
+    solver = StokesSolver(indicator, cfg, penalties, state, dev, pipeline=pipeline)
     solver.begin()
     solver.iterate(cfg.max_iter, poll=True)
     solver.end()

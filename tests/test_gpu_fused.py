@@ -1,0 +1,118 @@
+"""Fused power-of-two pipeline (pf_fused.cu: hand-written axis-split FFTs fused
+with the pointwise and spectral steps) against the CPU oracle, the cuFFT
+pipeline and the live-reference cfg-1 golden.  Same parity bar: identical
+iteration counts, fields within 1e-10 relative L2."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_15554_b200 as pf
+
+    return pf
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def _hist_close(mine, ref, rtol=1e-5):
+    scale = np.abs(ref).max(axis=0, keepdims=True)
+    err = np.abs(mine - ref) / np.maximum(np.abs(ref), 1e-9 * scale + 1e-300)
+    assert err.max() <= rtol, (err.max(), np.unravel_index(err.argmax(), err.shape))
+
+
+@pytest.mark.parametrize("n,iters,geom", [(64, 30, "packing"), (64, 12, "sphere"), (128, 4, "packing")])
+def test_fused_truncated_vs_oracle(pf, n, iters, geom):
+    from oracle import poreflow_oracle as O
+
+    ind = (pf.random_packing_geometry(n, seed=3) if geom == "packing"
+           else pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25))
+    g = (0.3, 1.0, -0.5)
+    cfg = pf.StokesConfig.with_tolerance(1e-7, pressure_gradient=g, max_iter=iters)
+    st, rep = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    assert rep.meta["pipeline"] == "fused"
+    ost, ohist, _, oit, ofp = O.solve_stokes(ind.values, g, 1e-7, 1e-7, max_iter=iters)
+    assert rep.iterations == oit == iters
+    h = st.to_host()
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(getattr(h, k), ost[k]) <= FIELD_TOL, (k, rel_l2(getattr(h, k), ost[k]))
+    _hist_close(rep.history, ohist)
+    np.testing.assert_allclose(rep.meta["final_penalties"], ofp, rtol=1e-12)
+
+
+def test_fused_matches_cufft_pipeline_full_solve(pf):
+    """Converged 64^3 solve (stiff, eps 1e-5): both device pipelines agree."""
+    ind = pf.make_model_geometry(pf.UnitCellGrid((64, 64, 64)), radius=0.3)
+    pen = pf.PenaltyParams(alpha=1000.0, beta=1000.0, b=1000.0, adaptive=False)
+    cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(0.0, 0.0, 1.0))
+    a, ra = pf.solve_stokes_device(ind, cfg, pen, pipeline="fused")
+    b, rb = pf.solve_stokes_device(ind, cfg, pen, pipeline="cufft")
+    assert ra.meta["pipeline"] == "fused" and rb.meta["pipeline"] == "cufft"
+    assert ra.converged and rb.converged and ra.iterations == rb.iterations
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        x, y = getattr(a, k).cpu().numpy(), getattr(b, k).cpu().numpy()
+        assert rel_l2(x, y) <= FIELD_TOL, k
+    _hist_close(ra.history, rb.history)
+
+
+def test_fused_warm_start_and_gauge(pf):
+    from oracle import poreflow_oracle as O
+
+    n = 64
+    ind = pf.random_packing_geometry(n, seed=5)
+    rng = np.random.default_rng(1)
+    init = pf.AdmmState(*(0.01 * rng.standard_normal(s) for s in [(3, n, n, n), (3, n, n, n), (n, n, n),
+                                                                   (3, n, n, n), (3, n, n, n)]))
+    g = (1.0, 0.0, 0.0)
+    cfg = pf.StokesConfig.with_tolerance(1e-6, pressure_gradient=g, max_iter=10)
+    st, rep = pf.solve_stokes(ind, cfg, None, init)
+    ost, ohist, _, oit, _ = O.solve_stokes(ind.values, g, 1e-6, 1e-6, max_iter=10,
+                                           init=dict(u=init.u, u_tilde=init.u_tilde, q=init.q, a=init.a,
+                                                     lam=init.lam))
+    assert rep.meta["pipeline"] == "fused" and rep.iterations == oit
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(getattr(st, k), ost[k]) <= FIELD_TOL, k
+    assert abs(st.q.mean()) <= 1e-12 * np.abs(st.q).max()
+    _hist_close(rep.history, ohist)
+
+
+def test_fused_cfg1_sphere64_matches_reference_golden(pf, golden):
+    """BASELINE cfg 1 (64^3 sphere array, r = 0.25, stiff, eps 1e-5), 3 load cases:
+    iteration counts, history, sampled velocity and the permeability tensor K
+    (Stokes symbols) against the live reference."""
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "stokes_sphere64_cfg1.npz")
+    if not os.path.exists(path):
+        pytest.skip("cfg-1 golden not generated")
+    z = golden("stokes_sphere64_cfg1")
+    n = int(z["dims"][0])
+    solid = np.unpackbits(z["solid_packed"])[: n ** 3].reshape(n, n, n)
+    ind = pf.IndicatorField(pf.UnitCellGrid((n, n, n)), solid)
+    pen = pf.PenaltyParams(alpha=1000.0, beta=1000.0, b=1000.0, adaptive=False)
+    us = []
+    for ax in range(3):
+        g = [0.0] * 3
+        g[ax] = 1.0
+        st, rep = pf.solve_stokes(ind, pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=tuple(g)), pen)
+        assert rep.meta["pipeline"] == "fused"
+        assert rep.iterations == int(z["iterations"][ax])
+        ref_h = z["history"][ax][: rep.iterations]
+        _hist_close(rep.history, ref_h)
+        us_s = st.u.ravel()[z["sample"]]
+        assert np.abs(us_s - z["u_sample"][ax]).max() <= 1e-10 * z["u_max"][ax]
+        assert abs(np.linalg.norm(st.u) - z["u_norm"][ax]) <= 1e-10 * z["u_norm"][ax]
+        us.append(st.u)
+    K = pf.permeability(us, ind, pf.make_symbols(ind.grid, "central"))
+    assert np.abs(K - z["K"]).max() <= 1e-9 * np.abs(z["K"]).max()
