@@ -143,7 +143,8 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm
 STAGES = ("S1_spectral", "Z2D_cufft", "S3_local", "finalize", "S4_form_r", "D2Z_cufft")
-FUSED_STAGES = ("PK_axis0_spectral", "MI_axis1_inverse", "RS_rows_local", "finalize", "MF_axis1_forward", "-")
+FUSED_STAGES = ("PK_axis0_spectral", "MI_axis1_inverse", "RS_rows_local", "finalize", "RSF_rows_fix",
+                "MF_axis1_forward")
 
 
 def stage_bytes(n_real, n_half, d=3):
@@ -165,10 +166,10 @@ def stage_bytes_fused(n_real, n_half):
     return {
         "PK_axis0_spectral": 10 * hw,          # Y(3) Q D in; Y(3) Q D out
         "MI_axis1_inverse": 6 * hw,            # Y(3) in; X(3) out
-        "RS_rows_local": 9 * hw + 24 * 8 * n_real + n_real,  # X(3) in, X(6) out; 12+12 state words; H
+        "RS_rows_local": 6 * hw + 24 * 8 * n_real + n_real,  # X(3) in, X(3) out; 12+12 state words; H
         "finalize": 0,
-        "MF_axis1_forward": 9 * hw,            # X(6) in; Y(3) out
-        "-": 0,
+        "RSF_rows_fix": 0,                     # no-op unless residual balancing changed b
+        "MF_axis1_forward": 6 * hw,            # X(3) in; Y(3) out
     }
 
 
@@ -252,7 +253,7 @@ def run_ours(args):
         t_ms = float(stage_ms[k])
         stages[name] = {"ms": t_ms, "alg_bytes": sb[name],
                         "GB_s": (sb[name] / (t_ms * 1e-3) / 1e9) if t_ms > 0 and sb[name] else None}
-    ours = [s for s in stages if "cufft" not in s and s != "finalize"]
+    ours = [s for s in stages if "cufft" not in s and s not in ("finalize", "RSF_rows_fix")]
     dom = max(ours, key=lambda s: stages[s]["ms"])
     traffic = None
     tfile = ROOT / "profiles" / "traffic_per_launch.json"
@@ -307,7 +308,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h / e2e_iters, "iterations": e2e_iters,
                 "api": "paper_2312_15554_b200.solve_stokes (numpy in/out)"},
         "pipeline": pipeline,
-        "gpu_launches": (5 if pipeline == "fused" else 4) * args.steps,
+        "gpu_launches": (6 if pipeline == "fused" else 4) * args.steps,
         "library_launches_note": ("none: all transforms are in-kernel" if pipeline == "fused"
                                   else "plus 2 cuFFT executions (batch 3) per iteration"),
         "clocks": clk,

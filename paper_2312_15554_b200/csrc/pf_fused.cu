@@ -10,13 +10,14 @@
 //         D^ = i k.U^, Q^' = Q^ - beta D^ (stokes.py:381, 408-409), Parseval sums;
 //         IFFT_0 of U^/n.                                   reads 5 words, writes 5
 //   MI  (axis-1 pencils, tile = (i0, CM columns)): IFFT_1 of U^.   reads 3, writes 3
-//   RS  (rows along axis 2, tile = NG rows): C2R of u' (two rows per complex FFT),
-//         the local projection and multiplier updates + six squared norms
-//         (pure.py:59-68, stokes.py:254-277), R2C of u~' and a' (one complex FFT
-//         per row).                                         reads 15 words, writes 18
+//   RS  (rows along axis 2, tile = 1024 voxels of one component): C2R of u'
+//         (two rows per complex FFT), the local projection and multiplier
+//         updates + six squared norms (pure.py:59-68, stokes.py:254-277), and
+//         R2C of R = b u~' - a' (two rows per complex FFT).  reads 15 words, writes 15
 //   F   k_stokes_finalize (shared with the cuFFT pipeline)
-//   MF  (axis-1 pencils): R = b' u~' - a' formed on load (post-adaptation b',
-//         stokes.py:405-407), FFT_1.                         reads 6, writes 3
+//   RSF (only when residual balancing changed b): X-space of u~'.
+//   MF  (axis-1 pencils): FFT_1 of R + (b' - b) X(u~') = X(b' u~' - a')
+//         (post-adaptation b', stokes.py:405-407).           reads 3, writes 3
 //
 // Spectra are stored as [rows][N/2] complex plus a separate Nyquist column
 // [rows] so rows stay 2 KiB aligned.  All FFTs are hand-written radix-8/16
@@ -90,6 +91,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 16-byte LDGSTS into an arbitrary (16-B aligned) shared address, L1 bypass.
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit_wait_all() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
 
 // x * exp(-+ 2 pi i m / 16): forward uses the minus sign.
 template <bool INV>
@@ -203,11 +212,11 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
 }
 
 struct Bufs {
-  double2 *XU, *XUn;  // X-space (after axis 2): u' in, u~' out   [3][N*N][H], [3][N*N]
-  double2 *XA, *XAn;  // X-space a'
+  double2 *XU, *XUn;  // X-space (after axis 2): u' (MI -> RS); X(u~') when b changed (RS-fix -> MF)
+  double2 *XR, *XRn;  // X-space R = b u~' - a' (RS -> MF)   [3][N*N][H], [3][N*N]
   double2 *Y, *Yn;    // Y-space (after axes 2,1): R~ in, U^ out  [3][N][N][H], [3][N][N]
-  double2 *Q, *Qn;    // full spectrum Q^   [N][N][H], [N][N]
-  double2 *D, *Dn;    // full spectrum D^_prev
+  double2* Q;         // full spectrum Q^, PK tile-major [tile][q][k0] (nh modes)
+  double2* D;         // full spectrum D^_prev, same layout
   double2* tw;        // N forward twiddles
   double *part_rs, *part_pk;
 };
@@ -240,7 +249,7 @@ struct RS2 {
   // shared-memory carve (bytes)
   static constexpr size_t TW = sizeof(double2) * N;
   static constexpr size_t INV = sizeof(double2) * NP * C::SS;
-  static constexpr size_t FWD = sizeof(double2) * R * C::SS;
+  static constexpr size_t FWD = sizeof(double2) * NP * C::SS;
   static constexpr size_t ST = sizeof(double) * 4 * V;     // u, u~, a, lam rows
   static constexpr size_t XM = sizeof(double2) * R * C::H; // X-space u' rows (main)
   static constexpr size_t XN = sizeof(double2) * R;        // nyq column
@@ -302,10 +311,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
     const int64_t row0 = (int64_t)(tile % TPC) * R;
-    double2* XU = B.XU + (size_t)c * N * N * H;
-    double2* XUn = B.XUn + (size_t)c * N * N;
-    double2* XA = B.XA + (size_t)c * N * N * H;
-    double2* XAn = B.XAn + (size_t)c * N * N;
+    double2* XR = B.XR + (size_t)c * N * N * H;
+    double2* XRn = B.XRn + (size_t)c * N * N;
     mbar_wait(&mbar, phase);
     // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
     for (int idx = t; idx < NP * H; idx += T) {
@@ -343,24 +350,25 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
       st.ut[i] = t1;
       st.a[i] = a1;
       st.lam[i] = l1;
-      SF[row * SS + C::pad(col)] = make_double2(t1, a1);  // z = u~' + i a'
+      // R = b u~' - a' with the pre-adaptation b (stokes.py:405-407); rows 2p, 2p+1 -> Re, Im
+      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::pad(col))[row & 1] = b * t1 - a1;
     }
     __syncthreads();
     // staged inputs consumed: prefetch the next tile while this one finishes
     if (t == 0 && tile + (int)gridDim.x < NT) rs_issue<N>(tile + gridDim.x, B, st, sst, sx, sxn, sh, &mbar);
-    fft_seq<N, false>(SF + g * SS, tw, l, true);
+    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
     __syncthreads();
-    // (3) separate the two real transforms, store X-space rows of u~' (in place of u') and a'
-    for (int idx = t; idx < R * H; idx += T) {
-      const int r = idx / H, k = idx % H;
-      const double2 zk = SF[r * SS + C::pad(k)], zm = SF[r * SS + C::pad((N - k) & (N - 1))];
-      XU[(row0 + r) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-      XA[(row0 + r) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    // (3) separate the two real transforms of each row pair, store X-space rows of R
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      XR[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XR[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
-    for (int r = t; r < R; r += T) {
-      const double2 z = SF[r * SS + C::pad(H)];
-      XUn[row0 + r] = make_double2(z.x, 0.0);
-      XAn[row0 + r] = make_double2(z.y, 0.0);
+    for (int p = t; p < NP; p += T) {
+      const double2 z = SF[p * SS + C::pad(H)];
+      XRn[row0 + 2 * p] = make_double2(z.x, 0.0);
+      XRn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
     __syncthreads();
   }
@@ -369,71 +377,141 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
 }
 
-// ------------------------------------------------------------------ MF / MI
-// Axis-1 pencils.  FWD: X-space (u~', a') -> Y-space R~ = FFT_1(b' u~' - a').
-//                  INV: Y-space U^ -> X-space u' (IFFT_1).
-template <int N, bool INV>
-__global__ void __launch_bounds__(256) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
+// RS-fix: X-space of u~' (row FFTs of the state), needed by MF only in the
+// iterations where residual balancing changed b (ctrl->db != 0); a no-op
+// otherwise.  Persistent, TMA bulk loads, same tiling as RS.
+template <int N>
+__global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __restrict__ ut, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
-  constexpr int H = C::H, SS = C::SS, CM = C::CM, NCH = C::NCHM;
+  using K = RS2<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
+  constexpr int TPC = N * N / R;
+  constexpr int NT = 3 * TPC;
+  if (ctrl->done || ctrl->db == 0.0) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  __shared__ uint64_t mbar;
+  double2* tw = (double2*)sraw;
+  double2* SF = (double2*)(sraw + K::TW);
+  double* sst = (double*)(sraw + K::TW + K::INV);
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  const int64_t n = (int64_t)N * N * N;
+  auto issue = [&](int tile) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    fence_async_smem();
+    mbar_expect(&mbar, sizeof(double) * V);
+    bulk_load(sst, ut + (int64_t)c * n + row0 * N, sizeof(double) * V, &mbar);
+  };
+  if (t == 0) {
+    mbar_init(&mbar);
+    if ((int)blockIdx.x < NT) issue(blockIdx.x);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    double2* XU = B.XU + (size_t)c * N * N * H;
+    double2* XUn = B.XUn + (size_t)c * N * N;
+    mbar_wait(&mbar, phase);
+    for (int v = t; v < V; v += T) {
+      const int row = v / N, col = v % N;
+      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::pad(col))[row & 1] = sst[v];
+    }
+    __syncthreads();
+    if (t == 0 && tile + (int)gridDim.x < NT) issue(tile + gridDim.x);
+    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    __syncthreads();
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      XU[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XU[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+    for (int p = t; p < NP; p += T) {
+      const double2 z = SF[p * SS + C::pad(H)];
+      XUn[row0 + 2 * p] = make_double2(z.x, 0.0);
+      XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ MF / MI
+// Axis-1 pencils, one component per block (tile = (c, i0, 8 columns of k2) or a
+// Nyquist tile of 8 rows i0).  All staged loads are 16-byte LDGSTS issued up
+// front straight into the padded FFT sequences, so a block has its whole tile
+// in flight at once; several blocks per SM overlap load and compute phases.
+//   FWD: X-space R = b u~' - a' (+ (b' - b) u~' when residual balancing changed b)
+//        -> Y-space R~ = FFT_1(b' u~' - a')
+//   INV: Y-space U^ -> X-space u'                                 (IFFT_1)
+template <int N>
+struct M2 {
+  using C = Cfg<N>;
+  static constexpr int T = 128;
+  static constexpr int NGM = T / C::G;        // groups = sequences per tile
+  static constexpr int CM = NGM;              // columns per tile
+  static constexpr int NCH = C::H / CM;
+  static constexpr int TPC = N * NCH + N / CM;  // tiles per component
+  static constexpr int TILES = 3 * TPC;
+  static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
+  static constexpr size_t BYTES_INV = sizeof(double2) * N + SEQ;
+  static constexpr size_t BYTES_FWD = sizeof(double2) * N + SEQ;
+};
+
+template <int N, bool INV>
+__global__ void __launch_bounds__(128) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = M2<N>;
+  constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
   if (ctrl->done) return;
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
   double2* S = smem + N;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  load_tw<N>(tw, B.tw);
-  const double b = ctrl->b;
-  const int tile = blockIdx.x;
+  const int c = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
   const bool nyq = tile >= N * NCH;
   const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
   const int i0b = nyq ? (tile - N * NCH) * CM : 0;
+  auto off_of = [&](int e, int q) -> size_t {
+    return nyq ? (size_t)(c * N + i0b + q) * N + e : ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
+  };
+  // element mapping: main tiles walk (e, q) with q fastest (contiguous columns);
+  // Nyquist tiles walk (q, e) with e fastest (contiguous rows).
+  for (int idx = t; idx < N * CM; idx += T) {
+    const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+    const size_t o = off_of(e, q);
+    if (INV) cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
+    else cp16(S + q * SS + C::pad(e), nyq ? B.XRn + o : B.XR + o);
+  }
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  cp_commit_wait_all();
   __syncthreads();
-  for (int c = 0; c < 3; ++c) {
-    for (int idx = t; idx < N * CM; idx += 256) {
-      int e, q;  // element along axis 1, sequence
-      size_t off;
-      if (!nyq) {
-        q = idx % CM;
-        e = idx / CM;
-        off = ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
-      } else {
-        q = idx / N;
-        e = idx % N;
-        off = (size_t)(c * N + i0b + q) * N + e;
+  if (!INV) {
+    const double db = ctrl->db;
+    if (db != 0.0) {  // rare: b changed this iteration; XU holds X(u~') (k_rsfix)
+      for (int idx = t; idx < N * CM; idx += T) {
+        const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+        const size_t o = off_of(e, q);
+        const double2 vu = nyq ? B.XUn[o] : B.XU[o];
+        double2* p = S + q * SS + C::pad(e);
+        *p = make_double2(p->x + db * vu.x, p->y + db * vu.y);
       }
-      double2 v;
-      if (!INV) {
-        const double2 vu = nyq ? B.XUn[off] : B.XU[off];
-        const double2 va = nyq ? B.XAn[off] : B.XA[off];
-        v = make_double2(b * vu.x - va.x, b * vu.y - va.y);
-      } else {
-        v = nyq ? B.Yn[off] : B.Y[off];
-      }
-      S[q * SS + C::pad(e)] = v;
+      __syncthreads();
     }
-    __syncthreads();
-    fft_seq<N, INV>(S + g * SS, tw, l, true);
-    __syncthreads();
-    for (int idx = t; idx < N * CM; idx += 256) {
-      int e, q;
-      size_t off;
-      if (!nyq) {
-        q = idx % CM;
-        e = idx / CM;
-        off = ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
-      } else {
-        q = idx / N;
-        e = idx % N;
-        off = (size_t)(c * N + i0b + q) * N + e;
-      }
-      const double2 v = S[q * SS + C::pad(e)];
-      if (!INV) {
-        if (nyq) B.Yn[off] = v; else B.Y[off] = v;
-      } else {
-        if (nyq) B.XUn[off] = v; else B.XU[off] = v;
-      }
+  }
+  fft_seq<N, INV>(S + g * SS, tw, l, true);
+  __syncthreads();
+  for (int idx = t; idx < N * CM; idx += T) {
+    const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+    const size_t o = off_of(e, q);
+    const double2 v = S[q * SS + C::pad(e)];
+    if (!INV) {
+      if (nyq) B.Yn[o] = v; else B.Y[o] = v;
+    } else {
+      if (nyq) B.XUn[o] = v; else B.XU[o] = v;
     }
-    __syncthreads();
   }
 }
 
@@ -444,16 +522,34 @@ struct SpecArgs {
   double nu, g[3], inv_n, dn;
 };
 
+// Axis-0 pencils: tile = (k1, CP columns of k2) or a Nyquist tile of CP values
+// of k1, all k0, three components.  Y-space loads are LDGSTS straight into the
+// padded sequences; Q^ and D^ live in tile-major order ([tile][q][k0]) so the
+// spectral step reads and writes them fully coalesced, prefetched into
+// registers before the forward FFTs.
 template <int N>
-__global__ void __launch_bounds__(256) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
+struct PK2 {
   using C = Cfg<N>;
-  constexpr int H = C::H, SS = C::SS, CP = C::CP, NCH = C::NCHP, NSEQ = 3 * CP;
+  static constexpr int T = 128;
+  static constexpr int NGP = T / C::G;
+  static constexpr int CP = NGP / 2;
+  static constexpr int NSEQ = 3 * CP;
+  static constexpr int NCH = C::H / CP;
+  static constexpr int TILES = N * NCH + N / CP;
+  static constexpr int MPT = CP * N / T;  // modes per thread
+  static constexpr size_t BYTES = sizeof(double2) * (N + NSEQ * C::SS);
+};
+
+template <int N>
+__global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = PK2<N>;
+  constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
   if (ctrl->done) return;
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
   double2* S = smem + N;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  load_tw<N>(tw, B.tw);
   const double beta = ctrl->beta, b = ctrl->b;
   const int tile = blockIdx.x;
   const bool nyq = tile >= N * NCH;
@@ -462,21 +558,32 @@ __global__ void __launch_bounds__(256) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
   auto yoff = [&](int c, int i0, int q) -> size_t {
     return nyq ? (size_t)(c * N + i0) * N + k1b + q : ((size_t)(c * N + i0) * N + k1) * H + ch * CP + q;
   };
-  for (int idx = t; idx < 3 * N * CP; idx += 256) {
+  for (int idx = t; idx < 3 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
-    const size_t off = yoff(c, i0, q);
-    S[(c * CP + q) * SS + C::pad(i0)] = nyq ? B.Yn[off] : B.Y[off];
+    const size_t o = yoff(c, i0, q);
+    cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const size_t tbase = (size_t)tile * CP * N;  // tile-major Q^, D^
+  double2 qv[K::MPT], dp[K::MPT];
+#pragma unroll
+  for (int j = 0; j < K::MPT; ++j) {
+    qv[j] = B.Q[tbase + t + T * j];
+    dp[j] = B.D[tbase + t + T * j];
+  }
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < (NSEQ + C::NG - 1) / C::NG; ++r) {
-    const int sq = g + r * C::NG;
+  for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
+    const int sq = g + r * K::NGP;
     fft_seq<N, false>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
   }
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int idx = t; idx < N * CP; idx += 256) {
-    const int q = idx % CP, k0 = idx / CP;
+#pragma unroll
+  for (int j = 0; j < K::MPT; ++j) {
+    const int m = t + T * j, q = m / N, k0 = m % N;
     const int kk1 = nyq ? k1b + q : k1, k2 = nyq ? H : ch * CP + q;
     const int idx3[3] = {k0, kk1, k2};
     double kc[3];
@@ -487,15 +594,14 @@ __global__ void __launch_bounds__(256) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
       L = L + __ldg(P.ell[c] + idx3[c]);
       ksq = ksq + kc[c] * kc[c];
     }
-    const size_t qo = nyq ? (size_t)k0 * N + kk1 : ((size_t)k0 * N + kk1) * H + k2;
-    const double2 qv = nyq ? B.Qn[qo] : B.Q[qo];
+    const double2 qq = qv[j];
     const bool zero = (k0 | kk1 | k2) == 0;
     double2 r[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double2 rc = S[(c * CP + q) * SS + C::pad(k0)];
-      r[c] = make_double2(kc[c] * qv.y + rc.x, -(kc[c] * qv.x) + rc.y);
-      if (zero) r[c].x = r[c].x + P.dn * P.g[c];
+      r[c] = make_double2(kc[c] * qq.y + rc.x, -(kc[c] * qq.x) + rc.y);  // -i k q + R^
+      if (zero) r[c].x = r[c].x + P.dn * P.g[c];                          // n g_p at k = 0
     }
     const double A = P.nu * L + b;
     double2 kr = make_double2(0.0, 0.0);
@@ -512,37 +618,54 @@ __global__ void __launch_bounds__(256) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
       dv = cadd(dv, cik(kc[c], u));
       S[(c * CP + q) * SS + C::pad(k0)] = make_double2(u.x * P.inv_n, u.y * P.inv_n);
     }
-    double2 qn = csub(qv, cscale(beta, dv));
+    double2 qn = csub(qq, cscale(beta, dv));
     if (zero) qn = make_double2(0.0, 0.0);
-    const double2 dprev = nyq ? B.Dn[qo] : B.D[qo];
     const double w = (k2 == 0 || k2 == H) ? 1.0 : 2.0;
     acc[0] += w * cabs2(dv);
-    acc[1] += w * cabs2(csub(dv, dprev));
+    acc[1] += w * cabs2(csub(dv, dp[j]));
     acc[2] += w * cabs2(qn);
-    if (nyq) {
-      B.Qn[qo] = qn;
-      B.Dn[qo] = dv;
-    } else {
-      B.Q[qo] = qn;
-      B.D[qo] = dv;
-    }
+    B.Q[tbase + m] = qn;
+    B.D[tbase + m] = dv;
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < (NSEQ + C::NG - 1) / C::NG; ++r) {
-    const int sq = g + r * C::NG;
+  for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
+    const int sq = g + r * K::NGP;
     fft_seq<N, true>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
   }
   __syncthreads();
-  for (int idx = t; idx < 3 * N * CP; idx += 256) {
+  for (int idx = t; idx < 3 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
-    const size_t off = yoff(c, i0, q);
+    const size_t o = yoff(c, i0, q);
     const double2 v = S[(c * CP + q) * SS + C::pad(i0)];
-    if (nyq) B.Yn[off] = v; else B.Y[off] = v;
+    if (nyq) B.Yn[o] = v; else B.Y[o] = v;
   }
   block_sum<3>(acc);
   if (t == 0)
     for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// natural full spectrum [k0][k1][N/2+1] <-> PK tile-major [tile][q][k0]
+template <int N>
+__global__ void k_tilemajor(const double2* __restrict__ nat, double2* __restrict__ tm, double scale, int to_tm) {
+  using K = PK2<N>;
+  constexpr int H = N / 2, W = H + 1, CP = K::CP;
+  const int64_t total = (int64_t)K::TILES * CP * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(i / (CP * N));
+    const int q = (int)((i / N) % CP), k0 = (int)(i % N);
+    int k1, k2;
+    if (tile < N * K::NCH) {
+      k1 = tile / K::NCH;
+      k2 = (tile % K::NCH) * CP + q;
+    } else {
+      k1 = (tile - N * K::NCH) * CP + q;
+      k2 = H;
+    }
+    const int64_t o = ((int64_t)k0 * N + k1) * W + k2;
+    if (to_tm) tm[i] = make_double2(nat[o].x * scale, nat[o].y * scale);
+    else tm[o] = make_double2(nat[i].x * scale, nat[i].y * scale);  // here nat = tile-major src, tm = natural dst
+  }
 }
 
 // ------------------------------------------------------------------ layout conversion (setup / teardown)
@@ -589,18 +712,23 @@ bool fused_supported(const pf_plan* p) {
 }
 
 template <int N>
-static size_t smem_m() { return sizeof(double2) * (N + fz::Cfg<N>::NG * fz::Cfg<N>::SS); }
+static size_t smem_mi() { return fz::M2<N>::BYTES_INV; }
+template <int N>
+static size_t smem_mf() { return fz::M2<N>::BYTES_FWD; }
 template <int N>
 static size_t smem_rs() { return fz::RS2<N>::BYTES; }
+template <int N>
+static size_t smem_rsfix() { return fz::RS2<N>::TW + fz::RS2<N>::INV + fz::RS2<N>::ST / 4; }
 constexpr int kRsBlocks = kSMs * 3;  // persistent RS grid: 3 blocks per SM
 template <int N>
-static size_t smem_pk() { return sizeof(double2) * (N + 3 * fz::Cfg<N>::CP * fz::Cfg<N>::SS); }
+static size_t smem_pk() { return fz::PK2<N>::BYTES; }
 
 template <int N>
 static int set_attrs() {
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
   return PF_OK;
 }
@@ -612,10 +740,10 @@ int fused_ensure(pf_plan* p) {
   f->N = N;
   const size_t H = N / 2, NN = (size_t)N * N;
   const size_t main1 = NN * H, nyq1 = NN;  // one component, complex elements
-  // X: 6 comps (XU 3, XA 3); Y: 3; Q, D: 1 each
+  // X: 6 comps (XU 3, XR 3); Y: 3; Q, D: 1 each
   const size_t elems = 11 * (main1 + nyq1) + N;
   const int nb_rs = kRsBlocks;
-  const int nb_pk = (N == 64) ? (N * 2 + N / 16) : (N * (N / 16) + N / 8);
+  const int nb_pk = (N == 64) ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : fz::PK2<256>::TILES);
   const size_t part = 6 * (size_t)nb_rs + 3 * (size_t)nb_pk;
   f->bytes = elems * sizeof(double2) + part * sizeof(double);
   PF_CK_CUDA(cudaMalloc(&f->mem, f->bytes));
@@ -626,15 +754,13 @@ int fused_ensure(pf_plan* p) {
     return r;
   };
   f->b.XU = take(3 * main1);
-  f->b.XA = take(3 * main1);
+  f->b.XR = take(3 * main1);
   f->b.Y = take(3 * main1);
-  f->b.Q = take(main1);
-  f->b.D = take(main1);
+  f->b.Q = take(main1 + nyq1);
+  f->b.D = take(main1 + nyq1);
   f->b.XUn = take(3 * nyq1);
-  f->b.XAn = take(3 * nyq1);
+  f->b.XRn = take(3 * nyq1);
   f->b.Yn = take(3 * nyq1);
-  f->b.Qn = take(nyq1);
-  f->b.Dn = take(nyq1);
   f->b.tw = take(N);
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
@@ -684,6 +810,18 @@ void fused_free(pf_plan* p) {
   p->fused = nullptr;
 }
 
+static int to_tilemajor(int N, const double2* src, double2* dst, double scale, bool to_tm, cudaStream_t s) {
+  const int64_t total = (int64_t)N * N * (N / 2 + 1);
+  const int nb = blocks_for(total);
+  switch (N) {
+    case 64: fz::k_tilemajor<64><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
+    case 128: fz::k_tilemajor<128><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
+    default: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
 // Setup: Q^, D^_prev and the Y-space right-hand side from the real state.
 int fused_setup(pf_plan* p) {
   FusedPlan* f = fp_of(p);
@@ -692,11 +830,11 @@ int fused_setup(pf_plan* p) {
   const int grid = blocks_for(nh * 3);
   // Q^ = FFT(q), gauge Q^(0) = 0
   PF_CK(plan_fft(p, true, 1, p->s_q, p->specB));
-  fz::k_split<<<grid, kThreads, 0, p->work>>>(NN, N, p->specB, f->b.Q, f->b.Qn);
-  PF_CK_CUDA(cudaMemsetAsync(f->b.Q, 0, sizeof(double2), p->work));
+  PF_CK(to_tilemajor(N, p->specB, f->b.Q, 1.0, true, p->work));
+  PF_CK_CUDA(cudaMemsetAsync(f->b.Q, 0, sizeof(double2), p->work));  // tile 0, q 0, k0 0 = mode (0,0,0)
   // D^_prev = i k . FFT(u)
   PF_CK(stokes_div_spectrum(p, p->s_u, p->specB, p->spec2));
-  fz::k_split<<<grid, kThreads, 0, p->work>>>(NN, N, p->spec2, f->b.D, f->b.Dn);
+  PF_CK(to_tilemajor(N, p->spec2, f->b.D, 1.0, true, p->work));
   // Y-space R~ = FFT_{2,1}(b u~ - a)
   PF_CK(stokes_form_r(p, p->realB));
   PF_CK_FFT(cufftExecD2Z(f->plan2d, (cufftDoubleReal*)p->realB, (cufftDoubleComplex*)p->specA));
@@ -711,8 +849,8 @@ int fused_finish(pf_plan* p) {
   FusedPlan* f = fp_of(p);
   const int N = f->N;
   const int64_t NN = (int64_t)N * N;
-  fz::k_merge<<<blocks_for(p->g.nh), kThreads, 0, p->work>>>(NN, N, f->b.Q, f->b.Qn, p->specB, p->g.inv_n);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(to_tilemajor(N, f->b.Q, p->specB, p->g.inv_n, false, p->work));
+  (void)NN;
   PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
   return PF_OK;
 }
@@ -736,21 +874,23 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
     return PF_OK;
   };
   PF_CK(mark(0));
-  fz::k_pk<N><<<C::PK_TILES, 256, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
+  fz::k_pk<N><<<fz::PK2<N>::TILES, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(1));
-  fz::k_maxis<N, true><<<C::M_TILES, 256, smem_m<N>(), p->work>>>(f->b, p->ctrl);
+  fz::k_maxis<N, true><<<fz::M2<N>::TILES, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
   fz::k_rs<N><<<kRsBlocks, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
-  k_stokes_finalize_launch(p, f->b.part_rs, kRsBlocks, f->b.part_pk, C::PK_TILES);
+  k_stokes_finalize_launch(p, f->b.part_rs, kRsBlocks, f->b.part_pk, fz::PK2<N>::TILES);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  fz::k_maxis<N, false><<<C::M_TILES, 256, smem_m<N>(), p->work>>>(f->b, p->ctrl);
+  fz::k_rsfix<N><<<kRsBlocks, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(5));
+  fz::k_maxis<N, false><<<fz::M2<N>::TILES, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(6));
   return PF_OK;
 }

@@ -78,6 +78,7 @@ struct Geom {
 struct Ctrl {
   double alpha, beta, b;  // current penalties (Stokes)
   double best;            // running minimum of r1+r2 (transport)
+  double db;              // b' - b of the last adaptation (fused pipeline's right-hand-side correction)
   int64_t iter;           // completed iterations
   int32_t done, converged, diverged, reason;
 };

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
   tp[2] = C.tol_vec + er * pymax(rp[2], an);
   td[2] = C.tol_vec + er * an;
   const int64_t it = ctrl->iter + 1;
+  ctrl->db = 0.0;
   double* row = hist + (it - 1) * PF_STOKES_COLUMNS;
   for (int k = 0; k < 3; ++k) {
     row[4 * k + 0] = rp[k];
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
     ctrl->alpha = v[0];
     ctrl->beta = v[1];
     ctrl->b = v[2];
+    ctrl->db = v[2] - b;
   }
   if (it >= C.max_iter) ctrl->done = 1;
 }
@@ -252,6 +254,7 @@ __global__ void k_ctrl_init(Ctrl* c, double alpha, double beta, double b) {
   c->alpha = alpha;
   c->beta = beta;
   c->b = b;
+  c->db = 0.0;
   c->best = INFINITY;
   c->iter = 0;
   c->done = c->converged = c->diverged = c->reason = 0;

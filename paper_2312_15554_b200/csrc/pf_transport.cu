@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_reduce_rows(const double* 
 }
 
 __global__ void k_ctrl_init_t(Ctrl* c) {
-  c->alpha = c->beta = c->b = 0.0;
+  c->alpha = c->beta = c->b = c->db = 0.0;
   c->best = INFINITY;
   c->iter = 0;
   c->done = c->converged = c->diverged = c->reason = 0;
