@@ -231,15 +231,29 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
   __syncthreads();
 }
 
-// Deterministic block partials -> totals: partials laid out [q][nblk].
+// Deterministic block partials -> totals: partials laid out [q][nblk].  Each
+// thread keeps four independent running sums per quantity (loads in flight),
+// combined in a fixed order, then a fixed-shape block tree.
 template <int NQ>
 __device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nblk, double (&tot)[NQ]) {
+  double s4[NQ][4];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x) s += part[(int64_t)q * nblk + i];
-    tot[q] = s;
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s4[q][u] = 0.0;
+  const int stride = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + 3 * stride < nblk; i += 4 * stride) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s4[q][u] += part[(int64_t)q * nblk + i + u * stride];
   }
+  for (; i < nblk; i += stride)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) s4[q][0] += part[(int64_t)q * nblk + i];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) tot[q] = (s4[q][0] + s4[q][1]) + (s4[q][2] + s4[q][3]);
   block_sum<NQ>(tot);
 }
 
