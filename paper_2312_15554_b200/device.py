@@ -125,8 +125,12 @@ def _np_dtype(tdtype):
 
 
 def solid_on_device(indicator, device):
-    """Cached device copy of an (immutable) IndicatorField's uint8 values."""
-    cache = indicator._device_cache
+    """Device copy of an (immutable) indicator's uint8 values, cached on this
+    package's IndicatorField; duck-typed indicators (e.g. the reference's own
+    ``poreflow.IndicatorField``) are copied per call."""
+    cache = getattr(indicator, "_device_cache", None)
+    if cache is None:
+        return to_device(np.asarray(indicator.values, dtype=np.uint8), device, torch().uint8)
     key = device.index
     if key not in cache:
         cache[key] = to_device(indicator.values, device, torch().uint8)
