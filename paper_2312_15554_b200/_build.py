@@ -30,9 +30,15 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _flags():
-    return ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                   "-I", str(ROOT / "include"), "-Xptxas", "-v"] + (["-DNDEBUG"])
+# The kernel plugin and the cuFFT pipeline evaluate the reference's formulas in
+# its order without FMA contraction (bit-exact pointwise kernels); the fused
+# pipeline's transforms differ from pocketfft anyway, so it lets nvcc contract.
+FMAD = {"pf_fused.cu": "true"}
+
+
+def _flags(src: str = ""):
+    return ARCH + ["-O3", "-lineinfo", f"--fmad={FMAD.get(src, 'false')}", "-std=c++17", "-Xcompiler",
+                   "-fPIC,-O3", "-I", str(ROOT / "include"), "-Xptxas", "-v"] + (["-DNDEBUG"])
 
 
 def sources():
@@ -43,7 +49,8 @@ def needs_build() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
+    deps = (list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
+            + [Path(__file__)])
     return any(p.stat().st_mtime > t for p in deps)
 
 
@@ -56,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path):
         obj = objdir / (src.stem + ".o")
-        cmd = [cc, "-c", str(src), "-o", str(obj)] + _flags()
+        cmd = [cc, "-c", str(src), "-o", str(obj)] + _flags(src.name)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")

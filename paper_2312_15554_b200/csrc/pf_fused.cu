@@ -607,9 +607,12 @@ __global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
     double2 kr = make_double2(0.0, 0.0);
 #pragma unroll
     for (int c = 0; c < 3; ++c) kr = cadd(kr, cscale(kc[c], r[c]));
-    const double f = beta / (A + beta * ksq);
+    // one division: f = beta/(A + beta ksq) and 1/A from 1/(A (A + beta ksq))
+    const double Dn = A + beta * ksq;
+    const double rAD = 1.0 / (A * Dn);
+    const double f = beta * A * rAD;
     const double2 corr = cscale(f, kr);
-    const double invA = 1.0 / A;
+    const double invA = Dn * rAD;
     double2 dv = make_double2(0.0, 0.0);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
