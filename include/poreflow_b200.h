@@ -149,6 +149,8 @@ int pf_transport_begin(pf_plan* plan, const pf_transport_params* params, const u
                        pf_transport_result* result);
 int pf_transport_iterate(pf_plan* plan, int64_t n_iter, int poll, pf_transport_result* result);
 int pf_transport_end(pf_plan* plan, pf_transport_result* result);
+/* Pipeline of the active / last transport solve: 0 = cuFFT, 1 = fused. */
+int pf_transport_pipeline(const pf_plan* plan);
 
 /* ------------------------------------------------------------------------
  * Effective properties — effective.py:32-108, grid.py:108-110.

@@ -19,7 +19,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libporeflow_b200.so"
-SOURCES = ["pf_plan.cu", "pf_stokes.cu", "pf_transport.cu", "pf_effective.cu", "pf_kernels.cu", "pf_fused.cu"]
+SOURCES = ["pf_plan.cu", "pf_stokes.cu", "pf_transport.cu", "pf_effective.cu", "pf_kernels.cu", "pf_fused.cu",
+           "pf_fused_transport.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -33,7 +34,7 @@ def nvcc() -> str:
 # The kernel plugin and the cuFFT pipeline evaluate the reference's formulas in
 # its order without FMA contraction (bit-exact pointwise kernels); the fused
 # pipeline's transforms differ from pocketfft anyway, so it lets nvcc contract.
-FMAD = {"pf_fused.cu": "true"}
+FMAD = {"pf_fused.cu": "true", "pf_fused_transport.cu": "true"}
 
 
 def _flags(src: str = ""):

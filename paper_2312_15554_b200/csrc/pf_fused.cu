@@ -27,189 +27,10 @@
 
 #include "pf_internal.cuh"
 
+#include "pf_fft.cuh"
+
 namespace pf {
 namespace fz {
-
-template <int N>
-struct Cfg {
-  static constexpr int A = (N == 64) ? 8 : 16;  // radix of pass 1 (and stride of pass-1 stores)
-  static constexpr int B = N / A;               // radix of pass 2
-  static constexpr int G = A > B ? A : B;       // lanes per FFT group
-  static constexpr int NG = 256 / G;            // groups per 256-thread block
-  static constexpr int SS = N + N / A + 1;      // padded smem sequence stride (complex)
-  static constexpr int H = N / 2;               // stored half-spectrum columns (k2 < N/2)
-  static constexpr int RSR = NG;                // rows per RS tile
-  static constexpr int CM = NG;                 // k2 columns per MF / MI tile
-  static constexpr int CP = NG / 2;             // k2 columns per PK tile
-  static constexpr int NCHM = H / CM;           // column chunks per i0 (M kernels)
-  static constexpr int NCHP = H / CP;           // column chunks per k1 (PK)
-  static constexpr int M_TILES = N * NCHM + N / CM;
-  static constexpr int PK_TILES = N * NCHP + N / CP;
-  static constexpr int RS_TILES = N * N / RSR;
-  static __device__ __forceinline__ int pad(int e) { return e + e / A; }
-};
-
-// cos(2 pi m / 16)
-__device__ __forceinline__ double c16(int m) {
-  switch (m & 15) {
-    case 0: return 1.0;
-    case 1: case 15: return 0.92387953251128675613;
-    case 2: case 14: return 0.70710678118654752440;
-    case 3: case 13: return 0.38268343236508977173;
-    case 4: case 12: return 0.0;
-    case 5: case 11: return -0.38268343236508977173;
-    case 6: case 10: return -0.70710678118654752440;
-    case 7: case 9: return -0.92387953251128675613;
-    default: return -1.0;
-  }
-}
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(__fma_rn(a.x, b.x, -(a.y * b.y)), __fma_rn(a.x, b.y, a.y * b.x));
-}
-
-
-// ---- TMA bulk copies (cp.async.bulk -> UBLKCP) completed on an mbarrier
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* m) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(m)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* m, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(m))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}" ::"r"(
-          su32(m)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-// 16-byte LDGSTS into an arbitrary (16-B aligned) shared address, L1 bypass.
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit_wait_all() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
-// x * exp(-+ 2 pi i m / 16): forward uses the minus sign.
-template <bool INV>
-__device__ __forceinline__ double2 rot16(double2 x, int m) {
-  m &= 15;
-  if (m == 0) return x;
-  if (m == 8) return make_double2(-x.x, -x.y);
-  if (m == 4) return INV ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
-  if (m == 12) return INV ? make_double2(x.y, -x.x) : make_double2(-x.y, x.x);
-  const double c = c16(m), s0 = c16(m - 4);  // sin(2 pi m/16)
-  const double s = INV ? s0 : -s0;
-  return make_double2(__fma_rn(x.x, c, -(x.y * s)), __fma_rn(x.x, s, x.y * c));
-}
-
-template <int R, bool INV>
-struct Dft;
-
-template <bool INV>
-struct Dft<2, INV> {
-  static __device__ __forceinline__ void run(double2* x) {
-    const double2 a = x[0], b = x[1];
-    x[0] = cadd(a, b);
-    x[1] = csub(a, b);
-  }
-};
-
-template <bool INV>
-struct Dft<4, INV> {
-  static __device__ __forceinline__ void run(double2* x) {
-    const double2 s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
-    const double2 s13 = cadd(x[1], x[3]), d13 = csub(x[1], x[3]);
-    // forward: X1 = d02 - i d13, X3 = d02 + i d13
-    const double2 jd = INV ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
-    x[0] = cadd(s02, s13);
-    x[2] = csub(s02, s13);
-    x[1] = cadd(d02, jd);
-    x[3] = csub(d02, jd);
-  }
-};
-
-// R = P * Q four-step in registers: n = Q n1 + n2, k = k1 + P k2.
-template <int P, int Q, bool INV>
-__device__ __forceinline__ void dft_pq(double2* x) {
-  constexpr int R = P * Q;
-  double2 y[R];
-#pragma unroll
-  for (int n2 = 0; n2 < Q; ++n2) {
-    double2 t[P];
-#pragma unroll
-    for (int n1 = 0; n1 < P; ++n1) t[n1] = x[Q * n1 + n2];
-    Dft<P, INV>::run(t);
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) y[n2 * P + k1] = rot16<INV>(t[k1], (n2 * k1) * (16 / R));
-  }
-#pragma unroll
-  for (int k1 = 0; k1 < P; ++k1) {
-    double2 t[Q];
-#pragma unroll
-    for (int n2 = 0; n2 < Q; ++n2) t[n2] = y[n2 * P + k1];
-    Dft<Q, INV>::run(t);
-#pragma unroll
-    for (int k2 = 0; k2 < Q; ++k2) x[k1 + P * k2] = t[k2];
-  }
-}
-
-template <bool INV>
-struct Dft<8, INV> {
-  static __device__ __forceinline__ void run(double2* x) { dft_pq<4, 2, INV>(x); }
-};
-template <bool INV>
-struct Dft<16, INV> {
-  static __device__ __forceinline__ void run(double2* x) { dft_pq<4, 4, INV>(x); }
-};
-
-// One N-point complex FFT (unnormalised) of the padded smem sequence s by the
-// G lanes of a group (lane l).  Pass 1: B sub-FFTs of size A over stride-B
-// elements + twiddles; pass 2: A sub-FFTs of size B.  Output in natural order.
-// Every lane of the warp must call this (it uses __syncwarp); `active` = false
-// makes a group participate without touching memory.
-template <int N, bool INV>
-__device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ tw, int l, bool active) {
-  using C = Cfg<N>;
-  constexpr int A = C::A, B = C::B;
-  double2 x[A > B ? A : B];
-  const bool p1 = active && l < B, p2 = active && l < A;
-  if (p1) {
-#pragma unroll
-    for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
-    Dft<A, INV>::run(x);
-#pragma unroll
-    for (int k1 = 1; k1 < A; ++k1) {
-      double2 w = tw[l * k1];
-      if (INV) w.y = -w.y;
-      x[k1] = cmul(x[k1], w);
-    }
-  }
-  __syncwarp();
-  if (p1) {
-#pragma unroll
-    for (int k1 = 0; k1 < A; ++k1) s[C::pad(k1 + A * l)] = x[k1];
-  }
-  __syncwarp();
-  if (p2) {
-#pragma unroll
-    for (int n2 = 0; n2 < B; ++n2) x[n2] = s[C::pad(l + A * n2)];
-    Dft<B, INV>::run(x);
-#pragma unroll
-    for (int k2 = 0; k2 < B; ++k2) s[C::pad(l + A * k2)] = x[k2];
-  }
-  __syncwarp();
-}
 
 struct Bufs {
   double2 *XU, *XUn;  // X-space (after axis 2): u' (MI -> RS); X(u~') when b changed (RS-fix -> MF)

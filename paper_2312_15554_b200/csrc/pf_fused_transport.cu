@@ -1,0 +1,632 @@
+// Fused comparison-medium transport pipeline for cubic power-of-two grids
+// (N = 64, 128, 256) — reference pkg/src/poreflow/transport.py:225-258 and
+// backends/pure.py:71-115.
+//
+// One iteration streams 25 words + 1 byte per voxel through HBM (the
+// canonical cuFFT accounting of SURVEY §8d is 34 words + 4 B):
+//
+//   PK_T (axis-0 pencils, 2 components): FFT_0 of Y_b and Y_w0; F^ = Y_b +
+//         i k0 W0^ (the i k2 / i k1 parts were folded in the X / Y passes);
+//         chi^ = F^ / (i b0.k + a0 L), chi^(0) = 0 (pure.py:106-110); Parseval
+//         residuals r1^2 = sum w |d chi^|^2 / n and r2^2 = sum w |k|^2 |d chi^|^2 / n
+//         (|grad^ chi' - grad^ chi|^2 = |k|^2 |d chi^|^2 since grad^ = i k chi^);
+//         chi^ kept (tile-major); IFFT_0 of chi^/n and i k0 chi^/n.
+//                                                  reads Y 2 + chi^ 1, writes Y 2 + chi^ 1
+//   MI_T (axis-1 pencils, 3 outputs): X(chi), X(d0 chi), X(d1 chi) = IFFT_1 of
+//         Y(chi), Y(d0 chi), i k1 Y(chi).          reads 3 (Y(chi) twice), writes 3
+//   RS_T (rows): C2R of d0, d1 chi (one complex FFT per row) and d2 chi = i k2 X(chi)
+//         (two rows per FFT); polarization w, s from grad chi', u, H (pure.py:71-87
+//         with the coefficients of build_coefficients, transport.py:112-121); R2C of
+//         (w0 + i w1) and (s + i w2); X_a = X(s) + i k2 X(w2).
+//                                                  reads X 3 + u 3 + H, writes X 3
+//   F    k_transport_finalize (history row, non-finite / growth guards, convergence)
+//   MF_T (axis-1 pencils, 2 outputs): Y_b = FFT_1(X_a) + i k1 FFT_1(X(w1)),
+//         Y_w0 = FFT_1(X(w0)).                     reads 3, writes 2
+//
+// The real fields chi and grad chi are materialised only at the end (cuFFT
+// from chi^), exactly as Re ifftn of the spectra the reference inverts.
+#include <cmath>
+#include <cstring>
+
+#include "pf_fft.cuh"
+
+namespace pf {
+namespace ft {
+
+using fz::Cfg;
+using fz::cmul;
+using fz::cp16;
+using fz::fft_seq;
+
+struct TBufs {
+  double2 *X, *Xn;  // X-space [3][N*N][H] + nyq [3][N*N]
+  double2 *Y, *Yn;  // Y-space [2][N][N][H] + nyq [2][N][N]
+  double2* CH;      // chi^ (PK tile-major, nh)
+  double2* G0;      // FFT(initial grad chi), 3 comps tile-major (warm start only) or null
+  double2* tw;
+  double* part;     // PK_T partials [2][blocks]
+};
+
+struct TP {
+  const double* kap[3];
+  const double* ell[3];
+  double pe, eta, a0, ubg, inv_n;
+  double g[3], b0v[3];
+};
+
+// ------------------------------------------------------------------ PK_T
+template <int N>
+struct TPK {
+  using C = Cfg<N>;
+  static constexpr int T = 128;
+  static constexpr int NGP = T / C::G;
+  static constexpr int CP = NGP / 2;
+  static constexpr int NSEQ = 2 * CP;
+  static constexpr int NCH = C::H / CP;
+  static constexpr int TILES = N * NCH + N / CP;
+  static constexpr int MPT = CP * N / T;
+  static constexpr size_t BYTES = sizeof(double2) * (N + NSEQ * C::SS);
+};
+
+template <int N>
+__global__ void __launch_bounds__(128) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = TPK<N>;
+  constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) double2 smem[];
+  double2* tw = smem;
+  double2* S = smem + N;
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  const int tile = blockIdx.x;
+  const bool nyq = tile >= N * NCH;
+  const int k1 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
+  const int k1b = nyq ? (tile - N * NCH) * CP : 0;
+  auto yoff = [&](int c, int i0, int q) -> size_t {
+    return nyq ? (size_t)(c * N + i0) * N + k1b + q : ((size_t)(c * N + i0) * N + k1) * H + ch * CP + q;
+  };
+  for (int idx = t; idx < 2 * N * CP; idx += T) {
+    const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+    const size_t o = yoff(c, i0, q);
+    cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  const bool first = (B.G0 != nullptr) && ctrl->iter == 0;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  fft_seq<N, false>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
+  __syncthreads();
+  const size_t tbase = (size_t)tile * CP * N;
+  const size_t nh = (size_t)K::TILES * CP * N;
+  double acc[2] = {0.0, 0.0};
+#pragma unroll 2
+  for (int j = 0; j < K::MPT; ++j) {
+    const int m = t + T * j, q = m / N, k0 = m % N;
+    const int kk1 = nyq ? k1b + q : k1, k2 = nyq ? H : ch * CP + q;
+    const int idx3[3] = {k0, kk1, k2};
+    double kc[3];
+    double L = 0.0, bk = 0.0, ksq = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      kc[c] = __ldg(P.kap[c] + idx3[c]);
+      L = L + __ldg(P.ell[c] + idx3[c]);
+      bk = bk + P.b0v[c] * kc[c];
+      ksq = ksq + kc[c] * kc[c];
+    }
+    const double2 fb = S[q * SS + C::pad(k0)], fw0 = S[(CP + q) * SS + C::pad(k0)];
+    const double2 f = cadd(fb, cik(kc[0], fw0));  // F^ = S^ + i k.W^   (pure.py:104-105)
+    const bool zero = (k0 | kk1 | k2) == 0;
+    const double2 chi = zero ? make_double2(0.0, 0.0) : cdiv_np(f, make_double2(P.a0 * L, bk));
+    const double2 prev = B.CH[tbase + m];
+    const double2 dch = csub(chi, prev);
+    const double w = (k2 == 0 || k2 == H) ? 1.0 : 2.0;
+    acc[0] += w * cabs2(dch);
+    if (!first) {
+      acc[1] += w * ksq * cabs2(dch);
+    } else {  // iteration 1 of a warm start: the given grad chi need not equal i k chi^
+      double s2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s2 += cabs2(csub(cik(kc[c], chi), B.G0[c * nh + tbase + m]));
+      acc[1] += w * s2;
+    }
+    B.CH[tbase + m] = chi;
+    S[q * SS + C::pad(k0)] = make_double2(chi.x * P.inv_n, chi.y * P.inv_n);
+    const double2 g0 = cik(kc[0], chi);
+    S[(CP + q) * SS + C::pad(k0)] = make_double2(g0.x * P.inv_n, g0.y * P.inv_n);
+  }
+  __syncthreads();
+  fft_seq<N, true>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
+  __syncthreads();
+  for (int idx = t; idx < 2 * N * CP; idx += T) {
+    const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+    const size_t o = yoff(c, i0, q);
+    const double2 v = S[(c * CP + q) * SS + C::pad(i0)];
+    if (nyq) B.Yn[o] = v; else B.Y[o] = v;
+  }
+  block_sum<2>(acc);
+  if (t == 0) {
+    B.part[blockIdx.x] = acc[0];
+    B.part[gridDim.x + blockIdx.x] = acc[1];
+  }
+}
+
+// ------------------------------------------------------------------ MI_T / MF_T
+template <int N>
+struct TM {
+  using C = Cfg<N>;
+  static constexpr int T = 128;
+  static constexpr int NGM = T / C::G;
+  static constexpr int CM = NGM;
+  static constexpr int NCH = C::H / CM;
+  static constexpr int TPC = N * NCH + N / CM;  // tiles per output component
+  static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
+  static constexpr size_t BYTES = sizeof(double2) * N + 2 * SEQ;
+};
+
+// INV (MI_T): outputs oc = 0 X(chi) <- Y0; 1 X(d0 chi) <- Y1; 2 X(d1 chi) <- i k1 Y0.
+// FWD (MF_T): outputs oc = 0 Y_b <- FFT(X0) + i k1 FFT(X2); 1 Y_w0 <- FFT(X1).
+template <int N, bool INV>
+__global__ void __launch_bounds__(128) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = TM<N>;
+  constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) double2 smem[];
+  double2* tw = smem;
+  double2* S = smem + N;
+  double2* S2 = S + K::NGM * SS;
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  const int oc = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
+  const bool nyq = tile >= N * NCH;
+  const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
+  const int i0b = nyq ? (tile - N * NCH) * CM : 0;
+  // X-space plane stride (per component) and Y-space component stride are both N*N*H (+N*N nyq)
+  auto off_of = [&](int c, int e, int q) -> size_t {
+    return nyq ? (size_t)(c * N + i0b + q) * N + e : ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
+  };
+  const int cin = INV ? (oc == 1 ? 1 : 0) : (oc == 1 ? 1 : 0);
+  const bool two = !INV && oc == 0;  // Y_b needs X0 and X2
+  for (int idx = t; idx < N * CM; idx += T) {
+    const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+    const size_t o = off_of(cin, e, q);
+    if (INV) {
+      cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
+    } else {
+      cp16(S + q * SS + C::pad(e), nyq ? B.Xn + o : B.X + o);
+      if (two) {
+        const size_t o2 = off_of(2, e, q);
+        cp16(S2 + q * SS + C::pad(e), nyq ? B.Xn + o2 : B.X + o2);
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (INV && oc == 2) {  // i k1 Y(chi) before the inverse axis-1 transform
+    for (int idx = t; idx < N * CM; idx += T) {
+      const int q = idx / N, e = idx % N;
+      double2* p = S + q * SS + C::pad(e);
+      *p = cik(__ldg(kap1 + e), *p);
+    }
+    __syncthreads();
+  }
+  fft_seq<N, INV>(S + g * SS, tw, l, true);
+  if (two) fft_seq<N, false>(S2 + g * SS, tw, l, true);
+  __syncthreads();
+  for (int idx = t; idx < N * CM; idx += T) {
+    const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+    double2 v = S[q * SS + C::pad(e)];
+    if (two) v = cadd(v, cik(__ldg(kap1 + e), S2[q * SS + C::pad(e)]));
+    const size_t o = off_of(oc, e, q);
+    if (INV) {
+      if (nyq) B.Xn[o] = v; else B.X[o] = v;
+    } else {
+      if (nyq) B.Yn[o] = v; else B.Y[o] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ RS_T
+template <int N>
+struct TRS {
+  using C = Cfg<N>;
+  static constexpr int R = 512 / N;          // rows per tile
+  static constexpr int NSF = 2 * R;          // forward sequences: (w0 + i w1), (s + i w2) per row
+  static constexpr int NSI = R + R / 2;      // inverse: (d0 + i d1) per row, (d2, d2) per row pair
+  static constexpr int T = NSF * C::G;       // one group per forward sequence
+  static constexpr int V = R * N;
+  static constexpr int VPT = V / T;
+  static constexpr size_t TW = sizeof(double2) * N;
+  static constexpr size_t SI = sizeof(double2) * NSI * C::SS;
+  static constexpr size_t SF = sizeof(double2) * NSF * C::SS;
+  static constexpr size_t XM = sizeof(double2) * 3 * R * C::H;   // X comps 0..2, R rows each
+  static constexpr size_t XN = sizeof(double2) * 3 * R;
+  static constexpr size_t UB = sizeof(double) * 3 * V;
+  static constexpr size_t HB = V;
+  static constexpr size_t BYTES = TW + SI + SF + XM + XN + UB + HB;
+  static constexpr uint32_t TX = (uint32_t)(XM + XN + UB + HB);
+};
+
+template <int N>
+__device__ __forceinline__ void trs_issue(int tile, const TBufs& B, const double* u, const uint8_t* Hs, double2* sx,
+                                          double2* sxn, double* su, uint8_t* sh, uint64_t* mbar) {
+  using K = TRS<N>;
+  using C = Cfg<N>;
+  constexpr int R = K::R, H = C::H;
+  const int64_t row0 = (int64_t)tile * R;
+  const int64_t n = (int64_t)N * N * N, NN = (int64_t)N * N;
+  fz::fence_async_smem();
+  fz::mbar_expect(mbar, K::TX);
+  for (int c = 0; c < 3; ++c) {
+    fz::bulk_load(sx + c * R * H, B.X + (c * NN + row0) * H, sizeof(double2) * R * H, mbar);
+    fz::bulk_load(sxn + c * R, B.Xn + c * NN + row0, sizeof(double2) * R, mbar);
+    fz::bulk_load(su + c * K::V, u + c * n + row0 * N, sizeof(double) * K::V, mbar);
+  }
+  fz::bulk_load(sh, Hs + row0 * N, (uint32_t)K::HB, mbar);
+}
+
+template <int N>
+__global__ void __launch_bounds__(TRS<N>::T) k_trs(TBufs B, TP P, const double* __restrict__ u,
+                                                   const uint8_t* __restrict__ Hs, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = TRS<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V;
+  constexpr int NT = N * N / R;
+  if (ctrl->done) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  __shared__ uint64_t mbar;
+  double2* tw = (double2*)sraw;
+  double2* SIq = (double2*)(sraw + K::TW);
+  double2* SFq = (double2*)(sraw + K::TW + K::SI);
+  double2* sx = (double2*)(sraw + K::TW + K::SI + K::SF);
+  double2* sxn = (double2*)(sraw + K::TW + K::SI + K::SF + K::XM);
+  double* su = (double*)(sraw + K::TW + K::SI + K::SF + K::XM + K::XN);
+  uint8_t* sh = (uint8_t*)(sraw + K::TW + K::SI + K::SF + K::XM + K::XN + K::UB);
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  const double* kap2 = P.kap[2];
+  if (t == 0) {
+    fz::mbar_init(&mbar);
+    if ((int)blockIdx.x < NT) trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar);
+  }
+  __syncthreads();
+  const double pe = P.pe, eta = P.eta, a0 = P.a0, ubg = P.ubg;
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
+    const int64_t row0 = (int64_t)tile * R;
+    fz::mbar_wait(&mbar, phase);
+    // (1) inverse sequences: per row r  Z = X(d0) + i X(d1);  per pair p  Z = X(d2)_{2p} + i X(d2)_{2p+1}
+    for (int idx = t; idx < (R + R / 2) * (H + 1); idx += T) {
+      const int sq = idx / (H + 1), k = idx % (H + 1);
+      double2 xa, xb;
+      if (sq < R) {
+        xa = k < H ? sx[(1 * R + sq) * H + k] : sxn[1 * R + sq];
+        xb = k < H ? sx[(2 * R + sq) * H + k] : sxn[2 * R + sq];
+      } else {
+        const int p = sq - R;
+        const double kk = __ldg(kap2 + k);  // X(d2 chi) = i k2 X(chi); Nyquist k2 -> 0
+        xa = cik(kk, k < H ? sx[(2 * p) * H + k] : sxn[2 * p]);
+        xb = cik(kk, k < H ? sx[(2 * p + 1) * H + k] : sxn[2 * p + 1]);
+      }
+      double2* sp = SIq + sq * SS;
+      if (k == 0 || k == H) {
+        sp[C::pad(k)] = make_double2(xa.x, xb.x);  // C2R keeps the real part of self-conjugate modes
+      } else {
+        sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+        sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+      }
+    }
+    __syncthreads();
+    fft_seq<N, true>(SIq + (g < K::NSI ? g : 0) * SS, tw, l, g < K::NSI);
+    __syncthreads();
+    // (2) polarization (pure.py:71-87) with A, B, F from H and u (transport.py:112-121)
+    for (int j = 0; j < K::VPT; ++j) {
+      const int v = t + T * j, row = v / N, col = v % N;
+      const double2 z01 = SIq[row * SS + C::pad(col)];
+      const double2 z2 = SIq[(R + (row >> 1)) * SS + C::pad(col)];
+      const double gr[3] = {z01.x, z01.y, (row & 1) ? z2.y : z2.x};
+      const double h = (double)sh[v];
+      const double pore = 1.0 - h;
+      const double contrast = (pore + eta * h) - a0;
+      const double pep = pe * pore;
+      double s = pep * ubg;
+      double w[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double tg = gr[c] + P.g[c];
+        w[c] = contrast * tg;
+        s = s - (pep * su[c * V + v] - P.b0v[c]) * tg;
+      }
+      SFq[(2 * row) * SS + C::pad(col)] = make_double2(w[0], w[1]);
+      SFq[(2 * row + 1) * SS + C::pad(col)] = make_double2(s, w[2]);
+    }
+    __syncthreads();
+    if (t == 0 && tile + (int)gridDim.x < NT) trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbar);
+    fft_seq<N, false>(SFq + g * SS, tw, l, true);
+    __syncthreads();
+    // (3) separate; X_a = X(s) + i k2 X(w2); store X comps 0 (X_a), 1 (X(w0)), 2 (X(w1))
+    const int64_t NN = (int64_t)N * N;
+    for (int idx = t; idx < R * (H + 1); idx += T) {
+      const int r = idx / (H + 1), k = idx % (H + 1);
+      const double2* s1 = SFq + (2 * r) * SS;
+      const double2* s2 = SFq + (2 * r + 1) * SS;
+      const double2 a1 = s1[C::pad(k)], m1 = s1[C::pad((N - k) & (N - 1))];
+      const double2 a2 = s2[C::pad(k)], m2 = s2[C::pad((N - k) & (N - 1))];
+      const double2 xw0 = make_double2(0.5 * (a1.x + m1.x), 0.5 * (a1.y - m1.y));
+      const double2 xw1 = make_double2(0.5 * (a1.y + m1.y), -0.5 * (a1.x - m1.x));
+      const double2 xs = make_double2(0.5 * (a2.x + m2.x), 0.5 * (a2.y - m2.y));
+      const double2 xw2 = make_double2(0.5 * (a2.y + m2.y), -0.5 * (a2.x - m2.x));
+      const double2 xa = cadd(xs, cik(__ldg(kap2 + k), xw2));
+      if (k < H) {
+        B.X[(0 * NN + row0 + r) * H + k] = xa;
+        B.X[(1 * NN + row0 + r) * H + k] = xw0;
+        B.X[(2 * NN + row0 + r) * H + k] = xw1;
+      } else {
+        B.Xn[0 * NN + row0 + r] = xa;
+        B.Xn[1 * NN + row0 + r] = xw0;
+        B.Xn[2 * NN + row0 + r] = xw1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ setup / teardown helpers
+// natural [4][N][N][N/2+1] 2D-transformed (w0, w1, w2, s) -> Y_b = S + i k2 W2 + i k1 W1, Y_w0 = W0
+template <int N>
+__global__ void k_tinit_y(const double2* __restrict__ nat, TBufs B, const double* __restrict__ kap1,
+                          const double* __restrict__ kap2) {
+  constexpr int H = N / 2, W = H + 1;
+  const int64_t rows = (int64_t)N * N, per = rows * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / W;
+    const int k2 = (int)(i % W), kk1 = (int)(r % N);
+    const double2 w0 = nat[i], w1 = nat[per + i], w2 = nat[2 * per + i], s = nat[3 * per + i];
+    const double2 yb = cadd(cadd(s, cik(kap2[k2], w2)), cik(kap1[kk1], w1));
+    if (k2 < H) {
+      B.Y[r * H + k2] = yb;
+      B.Y[(rows + r) * H + k2] = w0;
+    } else {
+      B.Yn[r] = yb;
+      B.Yn[rows + r] = w0;
+    }
+  }
+}
+
+// tile-major chi^ -> natural [ncomp][N][N][N/2+1] of chi^/n (comp 0) and i k_c chi^/n (comps 1..3)
+template <int N>
+__global__ void k_tout(const double2* __restrict__ CH, double2* __restrict__ nat, TP P, int with_grad) {
+  using K = TPK<N>;
+  constexpr int H = N / 2, W = H + 1, CP = K::CP;
+  const int64_t per = (int64_t)N * N * W;
+  const int64_t total = (int64_t)K::TILES * CP * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(i / (CP * N));
+    const int q = (int)((i / N) % CP), k0 = (int)(i % N);
+    int k1, k2;
+    if (tile < N * K::NCH) {
+      k1 = tile / K::NCH;
+      k2 = (tile % K::NCH) * CP + q;
+    } else {
+      k1 = (tile - N * K::NCH) * CP + q;
+      k2 = H;
+    }
+    const int64_t o = ((int64_t)k0 * N + k1) * W + k2;
+    const double2 c = make_double2(CH[i].x * P.inv_n, CH[i].y * P.inv_n);
+    nat[o] = c;
+    if (with_grad) {
+      const int idx3[3] = {k0, k1, k2};
+      for (int a = 0; a < 3; ++a) nat[(a + 1) * per + o] = cik(P.kap[a][idx3[a]], c);
+    }
+  }
+}
+
+template <int N>
+__global__ void k_to_tm(const double2* __restrict__ nat, double2* __restrict__ tm, int ncomp) {
+  using K = TPK<N>;
+  constexpr int H = N / 2, W = H + 1, CP = K::CP;
+  const int64_t per = (int64_t)N * N * W;
+  const int64_t total = (int64_t)K::TILES * CP * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(i / (CP * N));
+    const int q = (int)((i / N) % CP), k0 = (int)(i % N);
+    int k1, k2;
+    if (tile < N * K::NCH) {
+      k1 = tile / K::NCH;
+      k2 = (tile % K::NCH) * CP + q;
+    } else {
+      k1 = (tile - N * K::NCH) * CP + q;
+      k2 = H;
+    }
+    const int64_t o = ((int64_t)k0 * N + k1) * W + k2;
+    for (int c = 0; c < ncomp; ++c) tm[c * total + i] = nat[c * per + o];
+  }
+}
+
+}  // namespace ft
+
+// ------------------------------------------------------------------ host
+struct FusedTPlan {
+  int N = 0;
+  ft::TBufs b{};
+  void* mem = nullptr;
+  double2* g0mem = nullptr;
+  cufftHandle plan2d = 0;
+};
+
+constexpr int kTrsBlocks = kSMs * 3;
+
+static FusedTPlan* ftp(pf_plan* p) { return reinterpret_cast<FusedTPlan*>(p->tfused); }
+
+template <int N>
+static int tset_attrs() {
+  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_tpk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TPK<N>::BYTES));
+  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_taxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TM<N>::BYTES));
+  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_taxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TM<N>::BYTES));
+  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_trs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TRS<N>::BYTES));
+  return PF_OK;
+}
+
+static int tfused_ensure(pf_plan* p) {
+  if (p->tfused) return PF_OK;
+  const int N = p->g.n[0];
+  FusedTPlan* f = new FusedTPlan();
+  f->N = N;
+  const size_t H = N / 2, NN = (size_t)N * N, nh = NN * (H + 1);
+  const int nb_pk = (N == 64) ? ft::TPK<64>::TILES : (N == 128 ? ft::TPK<128>::TILES : ft::TPK<256>::TILES);
+  const size_t elems = 3 * NN * H + 3 * NN + 2 * NN * H + 2 * NN + nh + N;
+  const size_t bytes = elems * sizeof(double2) + 2 * (size_t)nb_pk * sizeof(double);
+  PF_CK_CUDA(cudaMalloc(&f->mem, bytes));
+  double2* m = (double2*)f->mem;
+  auto take = [&](size_t k) {
+    double2* r = m;
+    m += k;
+    return r;
+  };
+  f->b.X = take(3 * NN * H);
+  f->b.Y = take(2 * NN * H);
+  f->b.CH = take(nh);
+  f->b.Xn = take(3 * NN);
+  f->b.Yn = take(2 * NN);
+  f->b.tw = take(N);
+  f->b.part = (double*)m;
+  std::vector<double2> tw(N);
+  for (int j = 0; j < N; ++j) {
+    const double a = 2.0 * M_PI * (double)j / (double)N;
+    tw[j] = make_double2(std::cos(a), -std::sin(a));
+  }
+  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+  size_t ws = 0;
+  long long dims2[2] = {N, N};
+  PF_CK_FFT(cufftCreate(&f->plan2d));
+  PF_CK_FFT(cufftSetAutoAllocation(f->plan2d, 0));
+  PF_CK_FFT(cufftMakePlanMany64(f->plan2d, 2, dims2, nullptr, 1, (long long)NN, nullptr, 1, (long long)N * (H + 1),
+                                CUFFT_D2Z, 4LL * N, &ws));
+  if (ws > p->fft_work_bytes) {
+    PF_CK_CUDA(cudaStreamSynchronize(p->work));
+    if (p->fft_work) PF_CK_CUDA(cudaFree(p->fft_work));
+    PF_CK_CUDA(cudaMalloc(&p->fft_work, ws));
+    p->fft_work_bytes = ws;
+    PF_CK(plan_reset_work_areas(p));
+  }
+  PF_CK_FFT(cufftSetWorkArea(f->plan2d, p->fft_work));
+  PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
+  switch (N) {
+    case 64: PF_CK(tset_attrs<64>()); break;
+    case 128: PF_CK(tset_attrs<128>()); break;
+    default: PF_CK(tset_attrs<256>()); break;
+  }
+  p->tfused = f;
+  p->scratch_bytes += bytes;
+  return PF_OK;
+}
+
+void tfused_free(pf_plan* p) {
+  FusedTPlan* f = ftp(p);
+  if (!f) return;
+  if (f->plan2d) cufftDestroy(f->plan2d);
+  cudaFree(f->mem);
+  cudaFree(f->g0mem);
+  delete f;
+  p->tfused = nullptr;
+}
+
+static ft::TP tparams(pf_plan* p) {
+  ft::TP P;
+  for (int i = 0; i < 3; ++i) {
+    P.kap[i] = p->kap[i];
+    P.ell[i] = p->ell[i];
+    P.g[i] = p->tc.g[i];
+    P.b0v[i] = p->tc.b0v[i];
+  }
+  P.pe = p->tc.pe;
+  P.eta = p->tc.eta;
+  P.a0 = p->tc.a0;
+  P.ubg = p->tc.ubar_dot_g;
+  P.inv_n = p->g.inv_n;
+  return P;
+}
+
+template <int N>
+static int tsetup_t(pf_plan* p, bool warm) {
+  FusedTPlan* f = ftp(p);
+  const int64_t nh = p->g.nh;
+  const int nb = blocks_for(nh);
+  // chi^ of the initial chi (r1 of iteration 1); zero start -> zeros
+  if (warm) {
+    PF_CK(plan_fft(p, true, 1, p->t_chi, p->specB));
+    ft::k_to_tm<N><<<nb, kThreads, 0, p->work>>>(p->specB, f->b.CH, 1);
+    // FFT of the given grad chi (r2 of iteration 1)
+    if (!f->g0mem) PF_CK_CUDA(cudaMalloc(&f->g0mem, sizeof(double2) * 3 * nh));
+    PF_CK(plan_fft(p, true, 3, p->t_grad, p->specB));
+    ft::k_to_tm<N><<<nb, kThreads, 0, p->work>>>(p->specB, f->g0mem, 3);
+    f->b.G0 = f->g0mem;
+  } else {
+    PF_CK_CUDA(cudaMemsetAsync(f->b.CH, 0, sizeof(double2) * nh, p->work));
+    f->b.G0 = nullptr;
+  }
+  // first polarization from the given grad chi, transformed over axes (1, 2)
+  PF_CK(transport_polarize(p, p->t_grad, p->realB));
+  PF_CK_FFT(cufftExecD2Z(f->plan2d, (cufftDoubleReal*)p->realB, (cufftDoubleComplex*)p->specA));
+  ft::k_tinit_y<N><<<nb, kThreads, 0, p->work>>>(p->specA, f->b, p->kap[1], p->kap[2]);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+template <int N>
+static int tfinish_t(pf_plan* p) {
+  FusedTPlan* f = ftp(p);
+  const int nb = blocks_for(p->g.nh);
+  ft::k_tout<N><<<nb, kThreads, 0, p->work>>>(f->b.CH, p->specB, tparams(p), 1);
+  PF_CK_CUDA(cudaGetLastError());
+  // chi and grad chi as one batch-4 inverse into (chi, grad) — they are separate user buffers
+  PF_CK(plan_fft(p, false, 1, p->specB, p->t_chi));
+  PF_CK(plan_fft(p, false, 3, p->specB + p->g.nh, p->t_grad));
+  return PF_OK;
+}
+
+template <int N>
+static int tenqueue_t(pf_plan* p) {
+  FusedTPlan* f = ftp(p);
+  const ft::TP P = tparams(p);
+  ft::k_tpk<N><<<ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work>>>(f->b, P, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  ft::k_trs<N><<<kTrsBlocks, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work>>>(f->b, P, p->t_u, p->s_solid, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  transport_finalize_launch(p, f->b.part, ft::TPK<N>::TILES, p->g.inv_n);
+  PF_CK_CUDA(cudaGetLastError());
+  ft::k_taxis<N, false><<<2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+int tfused_setup(pf_plan* p, bool warm) {
+  PF_CK(tfused_ensure(p));
+  switch (ftp(p)->N) {
+    case 64: return tsetup_t<64>(p, warm);
+    case 128: return tsetup_t<128>(p, warm);
+    default: return tsetup_t<256>(p, warm);
+  }
+}
+
+int tfused_finish(pf_plan* p) {
+  switch (ftp(p)->N) {
+    case 64: return tfinish_t<64>(p);
+    case 128: return tfinish_t<128>(p);
+    default: return tfinish_t<256>(p);
+  }
+}
+
+int tfused_enqueue(pf_plan* p) {
+  switch (ftp(p)->N) {
+    case 64: return tenqueue_t<64>(p);
+    case 128: return tenqueue_t<128>(p);
+    default: return tenqueue_t<256>(p);
+  }
+}
+
+}  // namespace pf

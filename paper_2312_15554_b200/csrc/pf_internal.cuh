@@ -147,6 +147,8 @@ struct pf_plan {
   void* fused;       // FusedPlan*
   int fused_enable;  // 1 = use the fused pipeline when the grid supports it
   int pipeline;      // pipeline of the active Stokes solve: 0 cuFFT, 1 fused
+  void* tfused;      // FusedTPlan* (pf_fused_transport.cu)
+  int t_pipeline;    // pipeline of the active transport solve: 0 cuFFT, 1 fused
   // active solve state
   int active;  // 0 none, 1 stokes, 2 transport
   pf::Graph graph;
@@ -177,6 +179,15 @@ void fused_free(pf_plan* p);
 int fused_setup(pf_plan* p);
 int fused_finish(pf_plan* p);
 int enqueue_fused(pf_plan* p, cudaEvent_t* ev);
+// fused transport pipeline (pf_fused_transport.cu)
+int tfused_setup(pf_plan* p, bool warm);
+int tfused_finish(pf_plan* p);
+int tfused_enqueue(pf_plan* p);
+void tfused_free(pf_plan* p);
+int plan_reset_work_areas(pf_plan* p);
+// transport helpers shared with the fused pipeline (pf_transport.cu)
+int transport_polarize(pf_plan* p, const double* grad, double* out);
+void transport_finalize_launch(pf_plan* p, const double* part, int nb, double scale);
 // Stokes helpers shared with the fused pipeline (pf_stokes.cu)
 int stokes_div_spectrum(pf_plan* p, const double* u, double2* tmp, double2* out);
 int stokes_form_r(pf_plan* p, double* R);

@@ -72,6 +72,15 @@ int leave(pf_plan* p) {
   return PF_OK;
 }
 
+int plan_reset_work_areas(pf_plan* p) {
+  for (int k = 0; k < 4; ++k) {
+    if (p->fwd[k]) PF_CK_FFT(cufftSetWorkArea(p->fwd[k], p->fft_work));
+    if (p->inv[k]) PF_CK_FFT(cufftSetWorkArea(p->inv[k], p->fft_work));
+  }
+  p->graph.reset();  // captured graphs reference the old work area
+  return PF_OK;
+}
+
 static int slot_of(pf_plan* p, int batch) {
   for (int i = 0; i < 4; ++i)
     if (p->batch_of[i] == batch) return i;
@@ -320,6 +329,7 @@ int pf_plan_destroy(pf_plan* p) {
   cudaStreamSynchronize(p->work);
   p->graph.reset();
   fused_free(p);
+  tfused_free(p);
   for (int k = 0; k < 4; ++k) {
     if (p->fwd[k]) cufftDestroy(p->fwd[k]);
     if (p->inv[k]) cufftDestroy(p->inv[k]);

@@ -130,15 +130,17 @@ __global__ void __launch_bounds__(kThreads) k_transport_local(const int64_t n, P
   }
 }
 
+// scale = 1 for real-space partials, 1/n for Parseval partials (fused pipeline)
 __global__ void __launch_bounds__(kFinalizeThreads) k_transport_finalize(Ctrl* __restrict__ ctrl,
                                                                          const double* __restrict__ part, int nb,
                                                                          double* __restrict__ hist, const double t1,
-                                                                         const double t2, const int64_t max_iter) {
+                                                                         const double t2, const int64_t max_iter,
+                                                                         const double scale) {
   if (ctrl->done) return;
   double S[2];
   reduce_partials<2>(part, nb, S);
   if (threadIdx.x != 0) return;
-  const double r1 = sqrt(S[0]), r2 = sqrt(S[1]);
+  const double r1 = sqrt(S[0] * scale), r2 = sqrt(S[1] * scale);
   const int64_t it = ctrl->iter + 1;
   double* row = hist + (it - 1) * PF_TRANSPORT_COLUMNS;
   row[0] = r1;
@@ -255,12 +257,30 @@ static int enqueue_transport_t(pf_plan* p) {
                                                      p->s_solid, p->realB, p->ctrl, p->partials);
   PF_CK_CUDA(cudaGetLastError());
   k_transport_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, p->partials, nb, p->t_hist, C.eps_tol1,
-                                                            C.eps_tol2, C.max_iter);
+                                                            C.eps_tol2, C.max_iter, 1.0);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
 
+int transport_polarize(pf_plan* p, const double* grad, double* out) {
+  const int64_t n = p->g.nr;
+  switch (p->g.d) {
+    case 1: k_polarize<1><<<blocks_for(n), kThreads, 0, p->work>>>(n, polar_of(p), grad, p->t_u, p->s_solid, out); break;
+    case 2: k_polarize<2><<<blocks_for(n), kThreads, 0, p->work>>>(n, polar_of(p), grad, p->t_u, p->s_solid, out); break;
+    default: k_polarize<3><<<blocks_for(n), kThreads, 0, p->work>>>(n, polar_of(p), grad, p->t_u, p->s_solid, out); break;
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+void transport_finalize_launch(pf_plan* p, const double* part, int nb, double scale) {
+  const TransportConst& C = p->tc;
+  k_transport_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, part, nb, p->t_hist, C.eps_tol1, C.eps_tol2,
+                                                            C.max_iter, scale);
+}
+
 static int enqueue_transport(pf_plan* p) {
+  if (p->t_pipeline == 1) return tfused_enqueue(p);
   switch (p->g.d) {
     case 1: return enqueue_transport_t<1>(p);
     case 2: return enqueue_transport_t<2>(p);
@@ -324,6 +344,8 @@ int pf_transport_begin(pf_plan* p, const pf_transport_params* P, const uint8_t* 
   if (res) *res = p->t_res;
   k_ctrl_init_t<<<1, 1, 0, p->work>>>(p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
+  p->t_pipeline = (p->fused_enable && fused_supported(p)) ? 1 : 0;
+  if (p->t_pipeline == 1) return tfused_setup(p, true);
   const int64_t n = p->g.nr;
   switch (d) {
     case 1: k_polarize<1><<<blocks_for(n), kThreads, 0, p->work>>>(n, polar_of(p), grad, u, solid, p->realB); break;
@@ -363,6 +385,7 @@ int pf_transport_end(pf_plan* p, pf_transport_result* res) {
     set_error("pf_transport_end without pf_transport_begin");
     return PF_ERR_STATE;
   }
+  if (p->t_pipeline == 1) PF_CK(tfused_finish(p));
   PF_CK_CUDA(cudaMemcpyAsync(&p->h_ctrl[0], p->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, p->work));
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
   fill_tres(p, p->h_ctrl[0], res);
@@ -370,6 +393,8 @@ int pf_transport_end(pf_plan* p, pf_transport_result* res) {
   PF_CK(leave(p));
   return PF_OK;
 }
+
+int pf_transport_pipeline(const pf_plan* p) { return p ? p->t_pipeline : -1; }
 
 int pf_transport_solve(pf_plan* p, const pf_transport_params* P, const uint8_t* solid, const double* u, double* chi,
                        double* grad, double* history, pf_transport_result* res) {

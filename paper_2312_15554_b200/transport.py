@@ -10,6 +10,7 @@ is still offered for API callers and is computed on device).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -138,7 +139,7 @@ class TransportSolver:
     """Device-resident comparison-medium driver (begin / iterate / end)."""
 
     def __init__(self, indicator, u_dev, cfg: TransportConfig, state: DeviceTransportState, device=None,
-                 history_rows: int | None = None):
+                 history_rows: int | None = None, pipeline: str | None = None):
         self.device = require_cuda(device)
         self.indicator, self.cfg, self.state, self.u = indicator, cfg, state, u_dev
         self.plan = get_plan(indicator.grid.dims, cfg.symbol_mode, self.device)
@@ -148,13 +149,23 @@ class TransportSolver:
         self.solid = solid_on_device(indicator, self.device)
         self.result = N.TransportResult()
         self._params = _params(cfg, min(cfg.max_iter, self.rows))
+        self.pipeline_request = pipeline or os.environ.get("POREFLOW_B200_PIPELINE", "auto")
+        if self.pipeline_request not in ("auto", "fused", "cufft"):
+            raise ValueError("pipeline must be 'auto', 'fused' or 'cufft'")
+
+    @property
+    def pipeline(self) -> str:
+        return {0: "cufft", 1: "fused"}.get(N.load().pf_transport_pipeline(self.plan.handle), "none")
 
     def begin(self):
         h = self.plan.bind_stream()
+        N.check(N.load().pf_plan_set_fused(h, 0 if self.pipeline_request == "cufft" else 1))
         s = self.state
         N.check(N.load().pf_transport_begin(h, ctypes.byref(self._params), self.solid.data_ptr(), self.u.data_ptr(),
                                             s.chi.data_ptr(), s.grad_chi.data_ptr(), self.history.data_ptr(),
                                             ctypes.byref(self.result)))
+        if self.pipeline_request == "fused" and self.pipeline != "fused":
+            raise ValueError(f"fused pipeline unsupported for grid {self.indicator.grid.dims}")
         return self
 
     def iterate(self, n_iter: int, poll: bool = True):
@@ -179,11 +190,11 @@ class TransportSolver:
             reason=_REASONS[int(r.reason)],
             meta={"symbol_mode": self.cfg.symbol_mode, "eps": self.cfg.eps, "pe": self.cfg.pe,
                   "eta": self.cfg.eta, "a0": self.cfg.a0, "b0": self.cfg.b0, "b0_vec": b0v,
-                  "composition_gradient": g})
+                  "composition_gradient": g, "pipeline": self.pipeline})
 
 
 def solve_transport_device(indicator: IndicatorField, u, cfg: TransportConfig | None = None, init=None,
-                           device=None):
+                           device=None, pipeline: str | None = None):
     """Device-resident ``solve_transport``: returns (DeviceTransportState, ConvergenceReport)."""
     cfg = cfg or TransportConfig()
     grid = indicator.grid
@@ -205,7 +216,7 @@ def solve_transport_device(indicator: IndicatorField, u, cfg: TransportConfig | 
         chi = t.zeros(grid.dims, dtype=t.float64, device=dev)
         gch = t.zeros((grid.dim, *grid.dims), dtype=t.float64, device=dev)
     state = DeviceTransportState(chi, gch)
-    solver = TransportSolver(indicator, ud, cfg, state, dev)
+    solver = TransportSolver(indicator, ud, cfg, state, dev, pipeline=pipeline)
     solver.begin()
     solver.iterate(cfg.max_iter, poll=True)
     solver.end()
