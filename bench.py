@@ -321,6 +321,118 @@ def run_ours(args):
     return 0
 
 
+def run_transport_workload(args):
+    """Secondary line (not the headline): transport voxel-iters/s, BASELINE cfg-2 cell
+    (n^3 sphere array, r = 0.25) under its unit flow; Pe = 10, a0 = 0.55 (cfg 2's
+    Pe = 50 trips the reference's divergence guard on this cell) and eps = 1e-12 so
+    the timed window never terminates early."""
+    import torch
+
+    import paper_2312_15554_b200 as pf
+
+    dev = torch.device("cuda", 0)
+    n = args.n
+    ind = pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25)
+    pen = pf.PenaltyParams(alpha=100.0, beta=100.0, b=100.0, adaptive=False)
+    st, _ = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-4, pressure_gradient=(1.0, 0.0, 0.0),
+                                                                       max_iter=200), pen)
+    cfg = pf.TransportConfig(pe=10.0, a0=0.55, eps=1e-12, composition_gradient=(1.0, 0.0, 0.0), max_iter=10**6)
+    z = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev)  # noqa: E731
+    state = pf.DeviceTransportState(z(n, n, n), z(3, n, n, n))
+    solver = pf.TransportSolver(ind, st.u, cfg, state, dev, history_rows=args.warmup + args.steps + 1)
+    solver.begin()
+    solver.iterate(args.warmup, poll=False)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    solver.iterate(args.steps, poll=False)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    res = solver.end()
+    assert res.iterations == args.warmup + args.steps and not res.diverged and not res.converged
+    peak, _ = peak_hbm()
+    value = n ** 3 * args.steps / (ms / 1e3)
+    print(json.dumps({"metric": "transport voxel-iters/s (secondary)", "value": value, "unit": UNIT,
+                      "ms_per_step": ms / args.steps, "steps": args.steps, "warmup": args.warmup,
+                      "pipeline": solver.pipeline, "dtype": "f64",
+                      "config": {"workload": f"transport_sphere_{n}^3", "pe": 10.0, "a0": 0.55},
+                      "roofline_201B": {"alg_bytes_per_voxel_iter": 201, "achieved_GB_s": 201 * value / 1e9,
+                                        "frac": 201 * value / 1e9 / peak}}), flush=True)
+    return 0
+
+
+def run_ensemble_workload(args):
+    """Secondary line: BASELINE cfg 4 — an ensemble of independent 128^3 random
+    packings (seeds rank*C .. rank*C + C-1), C cells resident per GPU, each on its
+    own plan / CUDA stream so their passes overlap; aggregate voxel-iters/s, max
+    over ranks under torchrun (weak scaling, no collective in the timed region)."""
+    import torch
+
+    import paper_2312_15554_b200 as pf
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    n, C = args.n, args.cells
+    solvers = []
+    for k in range(C):
+        ind = pf.random_packing_geometry(n, seed=rank * C + k)
+        cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(1.0, 0.0, 0.0), max_iter=10**7)
+        st = pf.DeviceAdmmState.zeros(ind.grid, dev)
+        s = pf.StokesSolver(ind, cfg, pf.PenaltyParams(), st, dev, history_rows=args.warmup + args.steps + 1,
+                            plan_slot=k)
+        s.begin()
+        solvers.append(s)
+    for s in solvers:
+        s.iterate(args.warmup, poll=False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    chunk = 8
+    done = 0
+    while done < args.steps:
+        k = min(chunk, args.steps - done)
+        for s in solvers:
+            s.iterate(k, poll=False)
+        done += k
+    for s in solvers:  # join every cell's stream into the timing stream
+        torch.cuda.current_stream().wait_stream(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    its = []
+    for s in solvers:
+        r = s.end()
+        its.append(int(r.iterations))
+    assert all(i == args.warmup + args.steps for i in its), its
+    value = world * C * n ** 3 * args.steps / (ms / 1e3)
+    peak, _ = peak_hbm()
+    if rank == 0:
+        print(json.dumps({"metric": "Stokes ALM voxel-iters/s, ensemble of 128^3 cells (secondary, cfg 4)",
+                          "value": value, "unit": UNIT, "n_gpus": world, "cells_per_gpu": C,
+                          "ms_per_step": ms / args.steps, "steps": args.steps, "warmup": args.warmup,
+                          "scaling": "weak", "dtype": "f64", "pipeline": solvers[0].pipeline,
+                          "config": {"workload": f"ensemble_random_packing_{n}^3", "cells": world * C},
+                          "iteration_roofline": {"alg_bytes_per_voxel_iter": B_ALG_ITER,
+                                                 "frac": B_ALG_ITER * value / world / 1e9 / peak}}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,7 +442,14 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="stokes", choices=("stokes", "transport", "ensemble"),
+                    help="stokes = the headline metric; transport / ensemble = secondary lines")
+    ap.add_argument("--cells", type=int, default=8, help="cells per GPU for --workload ensemble")
     args = ap.parse_args()
+    if args.workload == "transport":
+        return run_transport_workload(args)
+    if args.workload == "ensemble":
+        return run_ensemble_workload(args)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

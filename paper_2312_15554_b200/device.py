@@ -87,12 +87,16 @@ class Plan:
 _plans = threading.local()
 
 
-def get_plan(dims, mode: str, device=None) -> Plan:
+def get_plan(dims, mode: str, device=None, slot: int = 0) -> Plan:
+    """Cached plan for (grid, symbol mode, device, slot) on this host thread.
+
+    Concurrent solves (one CUDA stream each, e.g. an ensemble of cells on one
+    GPU) need distinct ``slot`` values: a plan owns its scratch and stream."""
     device = require_cuda(device)
     cache = getattr(_plans, "cache", None)
     if cache is None:
         cache = _plans.cache = {}
-    key = (tuple(int(n) for n in dims), mode, device.index)
+    key = (tuple(int(n) for n in dims), mode, device.index, int(slot))
     plan = cache.get(key)
     if plan is None:
         plan = cache[key] = Plan(dims, mode, device)
@@ -135,3 +139,47 @@ def solid_on_device(indicator, device):
     if key not in cache:
         cache[key] = to_device(indicator.values, device, torch().uint8)
     return cache[key]
+
+
+_STAGE_BYTES = 64 << 20
+_stage = threading.local()
+
+
+def _stage_buffers(device):
+    bufs = getattr(_stage, "bufs", None)
+    if bufs is None or bufs[0].device.type != "cpu":
+        t = torch()
+        bufs = _stage.bufs = [t.empty(_STAGE_BYTES, dtype=t.uint8, pin_memory=True) for _ in range(2)]
+        _stage.events = [t.cuda.Event() for _ in range(2)]
+    return _stage.bufs, _stage.events
+
+
+def to_host(x) -> np.ndarray:
+    """CUDA tensor -> new numpy array through two reusable pinned staging buffers
+    (device-to-host DMA of chunk i+1 overlaps the host copy of chunk i); several
+    times faster than a pageable ``.cpu()`` for multi-GB solver states."""
+    t = torch()
+    x = x.contiguous()
+    out = np.empty(tuple(x.shape), dtype={t.float64: np.float64, t.uint8: np.uint8,
+                                          t.complex128: np.complex128}[x.dtype])
+    nbytes = out.nbytes
+    if nbytes <= (1 << 20):
+        return x.cpu().numpy().copy()
+    src = x.view(-1).view(t.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    bufs, evs = _stage_buffers(x.device)
+    stream = t.cuda.current_stream(x.device)
+    chunks = [(o, min(_STAGE_BYTES, nbytes - o)) for o in range(0, nbytes, _STAGE_BYTES)]
+    for i, (o, k) in enumerate(chunks[:2]):
+        bufs[i][:k].copy_(src[o:o + k], non_blocking=True)
+        evs[i].record(stream)
+    for i, (o, k) in enumerate(chunks):
+        j = i & 1
+        evs[j].synchronize()
+        np.copyto(dst[o:o + k], bufs[j][:k].numpy())
+        nxt = i + 2
+        if nxt < len(chunks):
+            o2, k2 = chunks[nxt]
+            bufs[j][:k2].copy_(src[o2:o2 + k2], non_blocking=True)
+            evs[j].record(stream)
+    return out

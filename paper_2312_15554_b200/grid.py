@@ -72,7 +72,7 @@ class IndicatorField:
         values = np.asarray(self.values)
         if values.shape != self.grid.dims:
             raise ValueError(f"indicator shape {values.shape} does not match grid {self.grid.dims}")
-        if not np.isin(values, (0, 1)).all():
+        if not ((values == 0) | (values == 1)).all():
             raise ValueError("indicator values must be exactly 0 or 1")
         values = values.astype(np.uint8)
         values.setflags(write=False)

@@ -17,7 +17,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native as N
-from .device import get_plan, require_cuda, solid_on_device, to_device, torch
+from .device import get_plan, require_cuda, solid_on_device, to_device, to_host, torch
 from .grid import IndicatorField
 from .report import ConvergenceReport
 from .spectral import CENTRAL, SYMBOL_MODES
@@ -160,7 +160,7 @@ class DeviceAdmmState:
         return cls(f(st.u), f(st.u_tilde), f(st.q), f(st.a), f(st.lam), st.iterations)
 
     def to_host(self) -> AdmmState:
-        g = lambda x: x.detach().cpu().numpy()  # noqa: E731
+        g = lambda x: to_host(x.detach())  # noqa: E731
         return AdmmState(g(self.u), g(self.u_tilde), g(self.q), g(self.a), g(self.lam), self.iterations)
 
 
@@ -213,11 +213,11 @@ class StokesSolver:
 
     def __init__(self, indicator: IndicatorField, cfg: StokesConfig, penalties: PenaltyParams,
                  state: DeviceAdmmState, device=None, history_rows: int | None = None,
-                 pipeline: str | None = None):
+                 pipeline: str | None = None, plan_slot: int = 0):
         self.device = require_cuda(device)
         self.indicator, self.cfg, self.penalties, self.state = indicator, cfg, penalties, state
         grid = indicator.grid
-        self.plan = get_plan(grid.dims, cfg.symbol_mode, self.device)
+        self.plan = get_plan(grid.dims, cfg.symbol_mode, self.device, plan_slot)
         t = torch()
         self.rows = int(history_rows or cfg.max_iter)
         self.history = t.empty(self.rows * len(REPORT_COLUMNS), dtype=t.float64, device=self.device)
