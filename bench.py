@@ -25,6 +25,8 @@ import tempfile
 import time
 from pathlib import Path
 
+import numpy as np
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -433,6 +435,63 @@ def run_ensemble_workload(args):
     return 0
 
 
+def run_slab_workload(args):
+    """Secondary line: BASELINE cfg 5 — ONE random-packing cell slab-decomposed over
+    the ranks (x-slabs; two all_to_alls of 3 half-spectrum components and one
+    9-double all_reduce per iteration).  Strong scaling: total work fixed."""
+    import torch
+
+    import paper_2312_15554_b200 as pf
+    from paper_2312_15554_b200 import slab as S
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    ind = pf.random_packing_geometry(n, seed=0)
+    lo, hi = S.slab_range(n, world, rank)
+    cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(1.0, 0.0, 0.0),
+                                         max_iter=args.warmup + args.steps + 1)
+    be = S.DeviceSlabBackend((n, n, n), world, rank, "central", dev)
+    be.bind()
+    L = (hi - lo) * n * n
+    st = {k: torch.zeros(3 * L, dtype=torch.float64, device=dev) for k in ("u", "u_tilde", "a", "lam")}
+    st["q"] = torch.zeros(L, dtype=torch.float64, device=dev)
+    solid = torch.as_tensor(np.ascontiguousarray(ind.values[lo:hi])).reshape(-1).to(dev)
+    sol = S.SlabStokes(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st)
+    sol.begin()
+    sol.iterate(args.warmup, poll=False)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    a.record()
+    sol.iterate(args.steps, poll=False)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rep = sol.end()
+    assert rep.iterations == args.warmup + args.steps and not rep.converged
+    value = n ** 3 * args.steps / (ms / 1e3)
+    if rank == 0:
+        print(json.dumps({"metric": "Stokes ALM voxel-iters/s, one slab-decomposed cell (secondary, cfg 5)",
+                          "value": value, "unit": UNIT, "n_gpus": world, "ms_per_step": ms / args.steps,
+                          "steps": args.steps, "warmup": args.warmup, "scaling": "strong", "dtype": "f64",
+                          "pipeline": "slab (cuFFT local transforms + all_to_all)",
+                          "config": {"workload": f"slab_random_packing_{n}^3", "ranks": world}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -442,7 +501,7 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="stokes", choices=("stokes", "transport", "ensemble"),
+    ap.add_argument("--workload", default="stokes", choices=("stokes", "transport", "ensemble", "slab"),
                     help="stokes = the headline metric; transport / ensemble = secondary lines")
     ap.add_argument("--cells", type=int, default=8, help="cells per GPU for --workload ensemble")
     args = ap.parse_args()
@@ -450,6 +509,8 @@ def main():
         return run_transport_workload(args)
     if args.workload == "ensemble":
         return run_ensemble_workload(args)
+    if args.workload == "slab":
+        return run_slab_workload(args)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -120,6 +120,33 @@ int pf_stokes_profile(pf_plan* plan, int64_t n_iter, double* stage_ms);
 int pf_stokes_pipeline(const pf_plan* plan);
 
 /* ------------------------------------------------------------------------
+ * Slab decomposition of one Stokes cell over P ranks (BASELINE cfg 5).
+ * Rank `rank` owns real x-slab i0 in [rank*N0/P, (rank+1)*N0/P) ([c][N0/P][N1][N2])
+ * and spectral y-slab k1 in [rank*N1/P, ...) in "T layout" [c][N0][N1/P][N2/2+1].
+ * The host driver moves the exchange buffers between ranks (all_to_all with
+ * equal splits) between pf_slab_forward / _forward_finish and pf_slab_inverse /
+ * _inverse_finish, and all-reduces the 9 residual sums between pf_slab_local
+ * and pf_slab_finalize.  All buffers are device memory owned by the caller;
+ * complex buffers are passed as double* (interleaved).  Enqueue-only.
+ * ---------------------------------------------------------------------- */
+int pf_slab_plan_create(pf_plan** out, const int64_t* dims, int nranks, int rank, int symbol_mode, int device,
+                        void* stream);
+int pf_slab_sizes(pf_plan* plan, int64_t* exchange_per_comp, int64_t* tspec_per_comp, int64_t* real_per_comp);
+int pf_slab_forward(pf_plan* plan, const double* real, int ncomp, double* send);
+int pf_slab_forward_finish(pf_plan* plan, const double* recv, int ncomp, double* tspec);
+int pf_slab_inverse(pf_plan* plan, double* tspec, int ncomp, double* send);
+int pf_slab_inverse_finish(pf_plan* plan, const double* recv, int ncomp, double* real);
+int pf_slab_stokes_begin(pf_plan* plan, const pf_stokes_params* params, const uint8_t* solid, double* u,
+                         double* u_tilde, double* q, double* a, double* lam, double* history);
+int pf_slab_setup(pf_plan* plan, const double* q_tspec, const double* u_tspec, double* Q, double* D);
+int pf_slab_spectral(pf_plan* plan, const double* R, double* Q, double* D, double* U);
+int pf_slab_local(pf_plan* plan, const double* u_new, double* totals9);
+int pf_slab_finalize(pf_plan* plan, const double* totals9);
+int pf_slab_form_r(pf_plan* plan, double* R, int gated);
+int pf_slab_scale(pf_plan* plan, const double* src, double* dst, int64_t count, double scale);
+int pf_slab_read(pf_plan* plan, pf_stokes_result* result);
+
+/* ------------------------------------------------------------------------
  * Transport — replaces poreflow.transport.solve_transport
  * (transport.py:180-268) including build_coefficients (101-128).
  * ---------------------------------------------------------------------- */

@@ -91,6 +91,20 @@ SIGNATURES = {
     "pf_stokes_end": [_P, ctypes.POINTER(StokesResult)],
     "pf_stokes_profile": [_P, ctypes.c_int64, _DP],
     "pf_stokes_pipeline": [_P],
+    "pf_slab_plan_create": [ctypes.POINTER(_P), _I64P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P],
+    "pf_slab_sizes": [_P, _I64P, _I64P, _I64P],
+    "pf_slab_forward": [_P, _P, ctypes.c_int, _P],
+    "pf_slab_forward_finish": [_P, _P, ctypes.c_int, _P],
+    "pf_slab_inverse": [_P, _P, ctypes.c_int, _P],
+    "pf_slab_inverse_finish": [_P, _P, ctypes.c_int, _P],
+    "pf_slab_stokes_begin": [_P, ctypes.POINTER(StokesParams), _P, _P, _P, _P, _P, _P, _P],
+    "pf_slab_setup": [_P, _P, _P, _P, _P],
+    "pf_slab_spectral": [_P, _P, _P, _P, _P],
+    "pf_slab_local": [_P, _P, _P],
+    "pf_slab_finalize": [_P, _P],
+    "pf_slab_form_r": [_P, _P, ctypes.c_int],
+    "pf_slab_scale": [_P, _P, _P, ctypes.c_int64, ctypes.c_double],
+    "pf_slab_read": [_P, ctypes.POINTER(StokesResult)],
     "pf_transport_solve": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_begin": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_iterate": [_P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(TransportResult)],

@@ -72,6 +72,7 @@ struct Geom {
   int64_t nh;   // half-spectrum modes
   double inv_n; // 1/nr
   double dn;    // (double) nr
+  int k1off;    // global offset of local axis-1 modes (slab decomposition; 0 otherwise)
 };
 
 // Device-side solver control block (one per plan; lives in device memory).
@@ -149,6 +150,8 @@ struct pf_plan {
   int pipeline;      // pipeline of the active Stokes solve: 0 cuFFT, 1 fused
   void* tfused;      // FusedTPlan* (pf_fused_transport.cu)
   int t_pipeline;    // pipeline of the active transport solve: 0 cuFFT, 1 fused
+  void* slab;        // SlabPlan* (pf_slab.cu) for slab-decomposed plans
+  int slab_nb1;      // block count of the last slab spectral step (its partials)
   // active solve state
   int active;  // 0 none, 1 stokes, 2 transport
   pf::Graph graph;
@@ -188,6 +191,14 @@ int plan_reset_work_areas(pf_plan* p);
 // transport helpers shared with the fused pipeline (pf_transport.cu)
 int transport_polarize(pf_plan* p, const double* grad, double* out);
 void transport_finalize_launch(pf_plan* p, const double* part, int nb, double scale);
+void slab_free(pf_plan* p);
+// Stokes kernels shared with the slab pipeline (pf_stokes.cu)
+int stokes_spectral_launch(pf_plan* p, const Geom& gs, double2* Qh, const double2* Rh, double2* Dh, double2* Uh,
+                           double* part1, int* nb1);
+int stokes_local_launch(pf_plan* p, int64_t n, const double* un, double* part3, int* nb3);
+int stokes_div_launch(pf_plan* p, const Geom& gs, const double2* Uh, double2* Dh);
+int stokes_ctrl_init(pf_plan* p, double alpha, double beta, double b);
+int stokes_form_r_gated(pf_plan* p, double* R, int gated);
 // Stokes helpers shared with the fused pipeline (pf_stokes.cu)
 int stokes_div_spectrum(pf_plan* p, const double* u, double2* tmp, double2* out);
 int stokes_form_r(pf_plan* p, double* R);

@@ -330,6 +330,7 @@ int pf_plan_destroy(pf_plan* p) {
   p->graph.reset();
   fused_free(p);
   tfused_free(p);
+  slab_free(p);
   for (int k = 0; k < 4; ++k) {
     if (p->fwd[k]) cufftDestroy(p->fwd[k]);
     if (p->inv[k]) cufftDestroy(p->inv[k]);

@@ -60,9 +60,13 @@ __global__ void __launch_bounds__(kThreads) k_stokes_spectral(
   const double gp[3] = {gx, gy, gz};
   double acc[3] = {0.0, 0.0, 0.0};
   const uint32_t nh = (uint32_t)g.nh;
+  const bool owns_zero = g.k1off == 0;
   for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < nh; m += gridDim.x * blockDim.x) {
     int idx[3];
     mode_index(g, m, idx);
+    const int i2 = idx[2];
+    idx[1] += g.k1off;  // global axis-1 mode (slab decomposition)
+    const bool zero = owns_zero && m == 0;
     double kc[D];
     double L = 0.0, ksq = 0.0;
 #pragma unroll
@@ -78,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_stokes_spectral(
     for (int c = 0; c < D; ++c) {
       const double2 rc = Rh[(size_t)c * nh + m];
       r[c] = make_double2(kc[c] * q.y + rc.x, -(kc[c] * q.x) + rc.y);  // -i k q + R^
-      if (m == 0) r[c].x = r[c].x + g.dn * gp[c];                         // n g_p at k = 0
+      if (zero) r[c].x = r[c].x + g.dn * gp[c];                           // n g_p at k = 0
     }
     const double A = nu * L + b;
     double2 kr = make_double2(0.0, 0.0);
@@ -96,9 +100,9 @@ __global__ void __launch_bounds__(kThreads) k_stokes_spectral(
       Uh[(size_t)c * nh + m] = make_double2(u.x * g.inv_n, u.y * g.inv_n);
     }
     double2 qn = csub(q, cscale(beta, dv));
-    if (m == 0) qn = make_double2(0.0, 0.0);
+    if (zero) qn = make_double2(0.0, 0.0);
     const double2 dprev = Dh[m];
-    const double w = parseval_w(g, idx[2]);
+    const double w = parseval_w(g, i2);
     acc[0] += w * cabs2(dv);
     acc[1] += w * cabs2(csub(dv, dprev));
     acc[2] += w * cabs2(qn);
@@ -233,6 +237,7 @@ __global__ void k_div_spectrum(Geom g, Tables T, const double2* __restrict__ Uh,
   for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < nh; m += gridDim.x * blockDim.x) {
     int idx[3];
     mode_index(g, m, idx);
+    idx[1] += g.k1off;
     double2 dv = make_double2(0.0, 0.0);
 #pragma unroll
     for (int c = 0; c < D; ++c) {
@@ -319,6 +324,45 @@ static int enqueue_stokes_ev(pf_plan* p, cudaEvent_t* ev) {
     case 2: return enqueue_stokes_t<2>(p, ev);
     default: return enqueue_stokes_t<3>(p, ev);
   }
+}
+
+int stokes_spectral_launch(pf_plan* p, const Geom& gs, double2* Qh, const double2* Rh, double2* Dh, double2* Uh,
+                           double* part1, int* nb1) {
+  const int nb = blocks_for(gs.nh);
+  const StokesConst& C = p->sc;
+  k_stokes_spectral<3><<<nb, kThreads, 0, p->work>>>(gs, tables_of(p), C.nu, C.g[0], C.g[1], C.g[2], Qh, Rh, Dh, Uh,
+                                                     p->ctrl, part1);
+  PF_CK_CUDA(cudaGetLastError());
+  *nb1 = nb;
+  return PF_OK;
+}
+
+int stokes_local_launch(pf_plan* p, int64_t n, const double* un, double* part3, int* nb3) {
+  const int nb = blocks_for(n);
+  k_stokes_local<3><<<nb, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid, p->ctrl,
+                                                  part3);
+  PF_CK_CUDA(cudaGetLastError());
+  *nb3 = nb;
+  return PF_OK;
+}
+
+int stokes_ctrl_init(pf_plan* p, double alpha, double beta, double b) {
+  k_ctrl_init<<<1, 1, 0, p->work>>>(p->ctrl, alpha, beta, b);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+int stokes_form_r_gated(pf_plan* p, double* R, int gated) {
+  const int64_t n = p->g.nr;
+  k_form_r<3><<<blocks_for(n), kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, gated);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+int stokes_div_launch(pf_plan* p, const Geom& gs, const double2* Uh, double2* Dh) {
+  k_div_spectrum<3><<<blocks_for(gs.nh), kThreads, 0, p->work>>>(gs, tables_of(p), Uh, Dh);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
 }
 
 int stokes_div_spectrum(pf_plan* p, const double* u, double2* tmp, double2* out) {

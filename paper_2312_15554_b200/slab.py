@@ -1,0 +1,260 @@
+"""Slab-decomposed Stokes solve of ONE cell across ranks (BASELINE cfg 5).
+
+Rank r holds the x-slab i0 in [r N0/P, (r+1) N0/P) of every real field and the
+y-slab k1 in [r N1/P, ...) of every spectrum.  Per ADMM iteration the ranks
+exchange two half spectra (R^ forward, U^ back, 3 components each) with
+``all_to_all`` and all-reduce the 9 squared-norm partial sums; every decision
+(residuals, convergence, residual balancing — stokes.py:247-310) then runs on
+identical totals on every rank, so all ranks stop at the same iteration.
+
+The driver is backend-agnostic: ``DeviceSlabBackend`` runs the per-rank work on
+the GPU through ``pf_slab_*`` (include/poreflow_b200.h) and the collectives go
+through ``torch.distributed`` (NCCL on the GPU box); the CPU tests drive the
+same loop with a numpy test double over ``gloo``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .device import require_cuda, torch
+from .report import ConvergenceReport
+from .stokes import REPORT_COLUMNS, PenaltyParams, StokesConfig, _params
+
+
+def slab_range(n0: int, world: int, rank: int) -> tuple[int, int]:
+    """x-slab [lo, hi) of rank ``rank`` (N0 must be divisible by the world size)."""
+    if n0 % world:
+        raise ValueError(f"N0 = {n0} is not divisible by {world} ranks")
+    L0 = n0 // world
+    return rank * L0, (rank + 1) * L0
+
+
+class DeviceSlabBackend:
+    """Per-rank device work through the C ABI; buffers are CUDA tensors."""
+
+    def __init__(self, dims, world: int, rank: int, symbol_mode: str = "central", device=None):
+        from .device import _SYMBOL_CODES
+        from .spectral import symbol_tables
+
+        self.dev = require_cuda(device)
+        t = torch()
+        lib = N.load()
+        h = ctypes.c_void_p()
+        with t.cuda.device(self.dev):
+            stream = t.cuda.current_stream(self.dev).cuda_stream
+            N.check(lib.pf_slab_plan_create(ctypes.byref(h), N.i64_array(dims), world, rank,
+                                            _SYMBOL_CODES[symbol_mode], self.dev.index, ctypes.c_void_p(stream)))
+        self.h = h
+        for ax, (kap, lap1) in enumerate(symbol_tables(tuple(dims), symbol_mode)):
+            kap = np.ascontiguousarray(kap, dtype=np.float64)
+            lap1 = np.ascontiguousarray(lap1, dtype=np.float64)
+            N.check(lib.pf_plan_set_symbol_tables(h, ax, kap.ctypes.data, lap1.ctypes.data))
+        e, ts, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        N.check(lib.pf_slab_sizes(h, ctypes.byref(e), ctypes.byref(ts), ctypes.byref(r)))
+        self.exch, self.tspec, self.real = int(e.value), int(ts.value), int(r.value)
+        self.lib = lib
+
+    def _p(self, x):
+        return ctypes.c_void_p(x.data_ptr())
+
+    def bind(self):
+        t = torch()
+        N.check(self.lib.pf_plan_set_stream(self.h, ctypes.c_void_p(t.cuda.current_stream(self.dev).cuda_stream)))
+
+    # buffers: complex buffers are float64 tensors holding interleaved (re, im)
+    def alloc_complex(self, count):
+        t = torch()
+        return t.empty(2 * count, dtype=t.float64, device=self.dev)
+
+    def alloc_real(self, count):
+        t = torch()
+        return t.empty(count, dtype=t.float64, device=self.dev)
+
+    def forward(self, real, ncomp, send):
+        N.check(self.lib.pf_slab_forward(self.h, self._p(real), ncomp, self._p(send)))
+
+    def forward_finish(self, recv, ncomp, tspec):
+        N.check(self.lib.pf_slab_forward_finish(self.h, self._p(recv), ncomp, self._p(tspec)))
+
+    def inverse(self, tspec, ncomp, send):
+        N.check(self.lib.pf_slab_inverse(self.h, self._p(tspec), ncomp, self._p(send)))
+
+    def inverse_finish(self, recv, ncomp, real):
+        N.check(self.lib.pf_slab_inverse_finish(self.h, self._p(recv), ncomp, self._p(real)))
+
+    def begin(self, params, solid, u, ut, q, a, lam, hist):
+        N.check(self.lib.pf_slab_stokes_begin(self.h, ctypes.byref(params), self._p(solid), self._p(u), self._p(ut),
+                                              self._p(q), self._p(a), self._p(lam), self._p(hist)))
+
+    def setup(self, Tq, Tu, Q, D):
+        N.check(self.lib.pf_slab_setup(self.h, self._p(Tq), self._p(Tu), self._p(Q), self._p(D)))
+
+    def spectral(self, R, Q, D, U):
+        N.check(self.lib.pf_slab_spectral(self.h, self._p(R), self._p(Q), self._p(D), self._p(U)))
+
+    def local(self, unew, totals):
+        N.check(self.lib.pf_slab_local(self.h, self._p(unew), self._p(totals)))
+
+    def finalize(self, totals):
+        N.check(self.lib.pf_slab_finalize(self.h, self._p(totals)))
+
+    def form_r(self, R, gated):
+        N.check(self.lib.pf_slab_form_r(self.h, self._p(R), 1 if gated else 0))
+
+    def scale(self, src, dst, count, s):
+        N.check(self.lib.pf_slab_scale(self.h, self._p(src), self._p(dst), int(count), float(s)))
+
+    def read(self) -> dict:
+        r = N.StokesResult()
+        N.check(self.lib.pf_slab_read(self.h, ctypes.byref(r)))
+        return {"iterations": int(r.iterations), "converged": bool(r.converged), "done": bool(r.done),
+                "final_penalties": tuple(float(x) for x in r.final_penalties)}
+
+    def close(self):
+        if self.h:
+            self.lib.pf_plan_destroy(self.h)
+            self.h = None
+
+
+class SlabStokes:
+    """ADMM Stokes loop (stokes.py:313-427) over a slab-decomposed cell.
+
+    ``state`` = dict of the rank's local fields u, u_tilde, a, lam (3, L0, N1, N2)
+    and q (L0, N1, N2) as backend tensors (flattened), updated in place.
+    """
+
+    def __init__(self, backend, dims, cfg: StokesConfig, penalties: PenaltyParams | None, solid_local, state,
+                 group=None, poll_every: int = 8):
+        import torch.distributed as dist
+
+        self.b, self.dims, self.cfg = backend, tuple(int(x) for x in dims), cfg
+        self.pen = penalties or PenaltyParams()
+        self.solid, self.state, self.group, self.poll = solid_local, state, group, max(1, int(poll_every))
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        be = backend
+        self.send = be.alloc_complex(3 * be.exch)
+        self.recv = be.alloc_complex(3 * be.exch) if self.world > 1 else self.send
+        self.TR = be.alloc_complex(3 * be.tspec)
+        self.TU = be.alloc_complex(3 * be.tspec)
+        self.Q = be.alloc_complex(be.tspec)
+        self.D = be.alloc_complex(be.tspec)
+        self.R = be.alloc_real(3 * be.real)
+        self.unew = be.alloc_real(3 * be.real)
+        self.totals = be.alloc_real(9)
+        self.hist = be.alloc_real(cfg.max_iter * len(REPORT_COLUMNS))
+
+    def _exchange(self, ncomp):
+        if self.world == 1:
+            return
+        k = 2 * ncomp * self.b.exch
+        self.dist.all_to_all_single(self.recv[:k], self.send[:k], group=self.group)
+
+    def _to_spectrum(self, real, ncomp, tspec):
+        self.b.forward(real, ncomp, self.send)
+        self._exchange(ncomp)
+        self.b.forward_finish(self.recv, ncomp, tspec)
+
+    def _to_real(self, tspec, ncomp, real):
+        self.b.inverse(tspec, ncomp, self.send)
+        self._exchange(ncomp)
+        self.b.inverse_finish(self.recv, ncomp, real)
+
+    def begin(self):
+        """Bind the state and build the spectral copies of the initial state
+        (stokes.py:363-370; Q^(0) = 0 is the gauge)."""
+        cfg, st, be = self.cfg, self.state, self.b
+        params = _params(cfg, self.pen, cfg.max_iter)
+        be.begin(params, self.solid, st["u"], st["u_tilde"], st["q"], st["a"], st["lam"], self.hist)
+        self._to_spectrum(st["q"], 1, self.TU)
+        self._to_spectrum(st["u"], 3, self.TR)
+        be.setup(self.TU, self.TR, self.Q, self.D)
+        be.form_r(self.R, gated=False)
+        self._to_spectrum(self.R, 3, self.TR)
+        self.it = 0
+        return self
+
+    def iterate(self, n_iter: int, poll: bool = True) -> dict:
+        """Up to ``n_iter`` more ADMM iterations (stokes.py:375-417); with
+        ``poll`` the device control block is read every ``poll_every``
+        iterations and the loop stops once it is done (identically on all ranks)."""
+        be = self.b
+        info = {"done": False}
+        for _ in range(int(n_iter)):
+            be.spectral(self.TR, self.Q, self.D, self.TU)
+            self._to_real(self.TU, 3, self.unew)
+            be.local(self.unew, self.totals)
+            if self.world > 1:
+                self.dist.all_reduce(self.totals, group=self.group)
+            be.finalize(self.totals)
+            be.form_r(self.R, gated=True)
+            self.it += 1
+            if poll and (self.it % self.poll == 0 or self.it == self.cfg.max_iter):
+                info = be.read()
+                if info["done"]:
+                    return info
+            self._to_spectrum(self.R, 3, self.TR)
+        return info
+
+    def end(self) -> ConvergenceReport:
+        """q = Re ifft(Q^) into the state; the report (identical on all ranks)."""
+        cfg, st, be = self.cfg, self.state, self.b
+        info = be.read()
+        n = float(np.prod(self.dims))
+        be.scale(self.Q, self.TU, be.tspec, 1.0 / n)
+        self._to_real(self.TU, 1, st["q"])
+        its = info["iterations"]
+        hist = self.hist[: its * len(REPORT_COLUMNS)].reshape(its, len(REPORT_COLUMNS))
+        hist = hist.cpu().numpy() if hasattr(hist, "cpu") else np.asarray(hist)
+        return ConvergenceReport(REPORT_COLUMNS, hist, converged=info["converged"], iterations=its,
+                                 meta={"symbol_mode": cfg.symbol_mode, "eps_abs": cfg.eps_abs,
+                                       "eps_rel": cfg.eps_rel, "nu": cfg.nu,
+                                       "pressure_gradient": tuple(float(x) for x in cfg.pressure_gradient),
+                                       "final_penalties": info["final_penalties"], "ranks": self.world,
+                                       "pipeline": "slab"})
+
+    def solve(self) -> ConvergenceReport:
+        self.begin()
+        self.iterate(self.cfg.max_iter, poll=True)
+        return self.end()
+
+
+def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalties: PenaltyParams | None = None,
+                      init_local: dict | None = None, group=None, device=None):
+    """Device slab solve on this rank: ``solid_local`` is the rank's x-slab of the
+    indicator (uint8, (N0/P, N1, N2)); returns (local state dict of CUDA tensors,
+    ConvergenceReport — identical on every rank)."""
+    import torch.distributed as dist
+
+    t = torch()
+    cfg = cfg or StokesConfig(pressure_gradient=(1.0, 0.0, 0.0))
+    if len(cfg.pressure_gradient) != 3 or len(dims) != 3:
+        raise ValueError("slab decomposition is 3D")
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    lo, hi = slab_range(int(dims[0]), world, rank)
+    if tuple(np.shape(solid_local)) != (hi - lo, int(dims[1]), int(dims[2])):
+        raise ValueError("solid_local must be this rank's x-slab")
+    be = DeviceSlabBackend(dims, world, rank, cfg.symbol_mode, device)
+    be.bind()
+    dev = be.dev
+    L = (hi - lo) * int(dims[1]) * int(dims[2])
+    if init_local is None:
+        st = {k: t.zeros(3 * L, dtype=t.float64, device=dev) for k in ("u", "u_tilde", "a", "lam")}
+        st["q"] = t.zeros(L, dtype=t.float64, device=dev)
+    else:
+        st = {k: t.as_tensor(np.asarray(init_local[k], dtype=np.float64)).reshape(-1).to(dev).clone()
+              for k in ("u", "u_tilde", "q", "a", "lam")}
+    solid = t.as_tensor(np.ascontiguousarray(solid_local, dtype=np.uint8)).reshape(-1).to(dev)
+    solver = SlabStokes(be, dims, cfg, penalties, solid, st, group)
+    rep = solver.solve()
+    t.cuda.synchronize(dev)
+    shp3, shp1 = (3, hi - lo, int(dims[1]), int(dims[2])), (hi - lo, int(dims[1]), int(dims[2]))
+    out = {k: (v.reshape(shp1) if k == "q" else v.reshape(shp3)) for k, v in st.items()}
+    be.close()
+    return out, rep
+

@@ -1,0 +1,51 @@
+"""Device slab backend (pf_slab_*) on one GPU (P = 1: the exchange is the
+identity, every transform, packing and offset path still runs) against the
+live-reference fixtures and the single-GPU pipelines."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_15554_b200 as pf
+
+    return pf
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+@pytest.mark.parametrize("case", ["stokes_sphere16_stiff", "stokes_random_trunc", "stokes_sphere12_adaptive"])
+def test_device_slab_matches_reference(pf, golden, case):
+    from paper_2312_15554_b200.slab import solve_stokes_slab
+
+    z = golden(case)
+    pen = z["penalties"]
+    penalties = pf.PenaltyParams(alpha=float(pen[0]), beta=float(pen[1]), b=float(pen[2]), adaptive=bool(pen[3]))
+    cfg = pf.StokesConfig.with_tolerance(float(z["eps"]), pressure_gradient=tuple(z["g_p"]),
+                                         max_iter=int(z["max_iter"]))
+    st, rep = solve_stokes_slab(z["solid"], z["solid"].shape, cfg, penalties)
+    assert rep.iterations == int(z["iterations"]) and rep.converged == bool(z["converged"])
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(st[k].cpu().numpy(), z[k]) <= 1e-10, k
+
+
+def test_device_slab_matches_fused_at_64(pf):
+    from paper_2312_15554_b200.slab import solve_stokes_slab
+
+    ind = pf.random_packing_geometry(64, seed=7)
+    cfg = pf.StokesConfig.with_tolerance(1e-6, pressure_gradient=(0.0, 1.0, 0.0), max_iter=40)
+    st, rep = solve_stokes_slab(ind.values, ind.grid.dims, cfg)
+    ref, rref = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    assert rep.iterations == rref.iterations == 40
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(st[k].cpu().numpy(), getattr(ref, k).cpu().numpy()) <= 1e-10, k
+    np.testing.assert_allclose(rep.history, rref.history, rtol=1e-6, atol=1e-9 * np.abs(rref.history).max())
