@@ -29,6 +29,10 @@
 
 #include "pf_fft.cuh"
 
+#ifndef PF_PK_PREFETCH
+#define PF_PK_PREFETCH 1
+#endif
+
 namespace pf {
 namespace fz {
 
@@ -353,19 +357,22 @@ struct PK2 {
   using C = Cfg<N>;
   static constexpr int T = 128;
   static constexpr int NGP = T / C::G;
-  static constexpr int CP = NGP / 2;
+  static constexpr int CP = NGP / 2;  // 3 components x CP columns over NGP groups
   static constexpr int NSEQ = 3 * CP;
   static constexpr int NCH = C::H / CP;
   static constexpr int TILES = N * NCH + N / CP;
-  static constexpr int MPT = CP * N / T;  // modes per thread
-  static constexpr size_t BYTES = sizeof(double2) * (N + NSEQ * C::SS);
+  static constexpr int MPT = (CP * N + T - 1) / T;  // modes per thread (last one guarded)
+  // sequence stride with an 8-bank shift: the (q fastest, 4 columns) staging
+  // pattern of 8-lane phases is then conflict-free
+  static constexpr int SS = C::SS + 1;
+  static constexpr size_t BYTES = sizeof(double2) * (N + NSEQ * SS);
 };
 
 template <int N>
-__global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(PK2<N>::T) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = PK2<N>;
-  constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
+  constexpr int H = C::H, SS = K::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
@@ -386,12 +393,17 @@ __global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   const size_t tbase = (size_t)tile * CP * N;  // tile-major Q^, D^
+#if PF_PK_PREFETCH
   double2 qv[K::MPT], dp[K::MPT];
 #pragma unroll
   for (int j = 0; j < K::MPT; ++j) {
-    qv[j] = B.Q[tbase + t + T * j];
-    dp[j] = B.D[tbase + t + T * j];
+    const int m = t + T * j;
+    if (m < CP * N) {
+      qv[j] = B.Q[tbase + m];
+      dp[j] = B.D[tbase + m];
+    }
   }
+#endif
   for (int j = t; j < N; j += T) tw[j] = B.tw[j];
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -405,6 +417,7 @@ __global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
 #pragma unroll
   for (int j = 0; j < K::MPT; ++j) {
     const int m = t + T * j, q = m / N, k0 = m % N;
+    if (m >= CP * N) break;
     const int kk1 = nyq ? k1b + q : k1, k2 = nyq ? H : ch * CP + q;
     const int idx3[3] = {k0, kk1, k2};
     double kc[3];
@@ -415,7 +428,13 @@ __global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
       L = L + __ldg(P.ell[c] + idx3[c]);
       ksq = ksq + kc[c] * kc[c];
     }
+#if PF_PK_PREFETCH
     const double2 qq = qv[j];
+    const double2 dpj = dp[j];
+#else
+    const double2 qq = B.Q[tbase + m];
+    const double2 dpj = B.D[tbase + m];
+#endif
     const bool zero = (k0 | kk1 | k2) == 0;
     double2 r[3];
 #pragma unroll
@@ -446,7 +465,7 @@ __global__ void __launch_bounds__(128) k_pk(Bufs B, SpecArgs P, const Ctrl* __re
     if (zero) qn = make_double2(0.0, 0.0);
     const double w = (k2 == 0 || k2 == H) ? 1.0 : 2.0;
     acc[0] += w * cabs2(dv);
-    acc[1] += w * cabs2(csub(dv, dp[j]));
+    acc[1] += w * cabs2(csub(dv, dpj));
     acc[2] += w * cabs2(qn);
     B.Q[tbase + m] = qn;
     B.D[tbase + m] = dv;
