@@ -341,7 +341,7 @@ def run_transport_workload(args):
     cfg = pf.TransportConfig(pe=10.0, a0=0.55, eps=1e-12, composition_gradient=(1.0, 0.0, 0.0), max_iter=10**6)
     z = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev)  # noqa: E731
     state = pf.DeviceTransportState(z(n, n, n), z(3, n, n, n))
-    solver = pf.TransportSolver(ind, st.u, cfg, state, dev, history_rows=args.warmup + args.steps + 1)
+    solver = pf.TransportSolver(ind, st.u, cfg, state, dev, history_rows=args.warmup + args.steps + 4)
     solver.begin()
     solver.iterate(args.warmup, poll=False)
     torch.cuda.synchronize()
@@ -351,8 +351,14 @@ def run_transport_workload(args):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
+    import ctypes
+
+    from paper_2312_15554_b200 import _native as N
+
+    sm = (ctypes.c_double * 5)()
+    N.check(N.load().pf_transport_profile(solver.plan.handle, 3, sm))
     res = solver.end()
-    assert res.iterations == args.warmup + args.steps and not res.diverged and not res.converged
+    assert res.iterations == args.warmup + args.steps + 3 and not res.diverged and not res.converged
     peak, _ = peak_hbm()
     value = n ** 3 * args.steps / (ms / 1e3)
     print(json.dumps({"metric": "transport voxel-iters/s (secondary)", "value": value, "unit": UNIT,
@@ -360,7 +366,9 @@ def run_transport_workload(args):
                       "pipeline": solver.pipeline, "dtype": "f64",
                       "config": {"workload": f"transport_sphere_{n}^3", "pe": 10.0, "a0": 0.55},
                       "roofline_201B": {"alg_bytes_per_voxel_iter": 201, "achieved_GB_s": 201 * value / 1e9,
-                                        "frac": 201 * value / 1e9 / peak}}), flush=True)
+                                        "frac": 201 * value / 1e9 / peak},
+                      "stages_ms": dict(zip(("PK_T", "MI_T", "RS_T", "finalize", "MF_T"), list(sm)))}),
+          flush=True)
     return 0
 
 

@@ -178,6 +178,9 @@ int pf_transport_iterate(pf_plan* plan, int64_t n_iter, int poll, pf_transport_r
 int pf_transport_end(pf_plan* plan, pf_transport_result* result);
 /* Pipeline of the active / last transport solve: 0 = cuFFT, 1 = fused. */
 int pf_transport_pipeline(const pf_plan* plan);
+/* Measurement hook: n_iter fused-transport iterations with stage events;
+ * stage_ms (5 doubles): PK_T | MI_T | RS_T | finalize | MF_T. */
+int pf_transport_profile(pf_plan* plan, int64_t n_iter, double* stage_ms);
 
 /* ------------------------------------------------------------------------
  * Effective properties — effective.py:32-108, grid.py:108-110.

@@ -110,6 +110,7 @@ SIGNATURES = {
     "pf_transport_iterate": [_P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(TransportResult)],
     "pf_transport_end": [_P, ctypes.POINTER(TransportResult)],
     "pf_transport_pipeline": [_P],
+    "pf_transport_profile": [_P, ctypes.c_int64, _DP],
     "pf_pore_average": [_P, _P, _P, ctypes.c_int, _DP],
     "pf_solid_count": [_P, _P, _I64P],
     "pf_permeability": [_P, _P, ctypes.POINTER(_P), _DP],

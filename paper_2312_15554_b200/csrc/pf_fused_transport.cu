@@ -588,19 +588,29 @@ static int tfinish_t(pf_plan* p) {
 }
 
 template <int N>
-static int tenqueue_t(pf_plan* p) {
+static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   FusedTPlan* f = ftp(p);
   const ft::TP P = tparams(p);
+  auto mark = [&](int i) -> int {
+    if (ev) PF_CK_CUDA(cudaEventRecord(ev[i], p->work));
+    return PF_OK;
+  };
+  PF_CK(mark(0));
   ft::k_tpk<N><<<ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work>>>(f->b, P, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(1));
   ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(2));
   ft::k_trs<N><<<kTrsBlocks, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work>>>(f->b, P, p->t_u, p->s_solid, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(3));
   transport_finalize_launch(p, f->b.part, ft::TPK<N>::TILES, p->g.inv_n);
   PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(4));
   ft::k_taxis<N, false><<<2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
+  PF_CK(mark(5));
   return PF_OK;
 }
 
@@ -621,11 +631,11 @@ int tfused_finish(pf_plan* p) {
   }
 }
 
-int tfused_enqueue(pf_plan* p) {
+int tfused_enqueue(pf_plan* p, cudaEvent_t* ev) {
   switch (ftp(p)->N) {
-    case 64: return tenqueue_t<64>(p);
-    case 128: return tenqueue_t<128>(p);
-    default: return tenqueue_t<256>(p);
+    case 64: return tenqueue_t<64>(p, ev);
+    case 128: return tenqueue_t<128>(p, ev);
+    default: return tenqueue_t<256>(p, ev);
   }
 }
 

@@ -185,7 +185,7 @@ int enqueue_fused(pf_plan* p, cudaEvent_t* ev);
 // fused transport pipeline (pf_fused_transport.cu)
 int tfused_setup(pf_plan* p, bool warm);
 int tfused_finish(pf_plan* p);
-int tfused_enqueue(pf_plan* p);
+int tfused_enqueue(pf_plan* p, cudaEvent_t* ev = nullptr);
 void tfused_free(pf_plan* p);
 int plan_reset_work_areas(pf_plan* p);
 // transport helpers shared with the fused pipeline (pf_transport.cu)

@@ -396,6 +396,33 @@ int pf_transport_end(pf_plan* p, pf_transport_result* res) {
 
 int pf_transport_pipeline(const pf_plan* p) { return p ? p->t_pipeline : -1; }
 
+int pf_transport_profile(pf_plan* p, int64_t n_iter, double* stage_ms) {
+  PF_ARG(p && stage_ms && n_iter >= 1, "bad argument");
+  if (p->active != 2 || p->t_pipeline != 1) {
+    set_error("pf_transport_profile needs an active fused transport solve");
+    return PF_ERR_STATE;
+  }
+  PF_CK(enter(p));
+  cudaEvent_t ev[6];
+  for (int i = 0; i < 6; ++i) PF_CK_CUDA(cudaEventCreate(&ev[i]));
+  double acc[5] = {0, 0, 0, 0, 0};
+  int st = PF_OK;
+  for (int64_t it = 0; it < n_iter && st == PF_OK; ++it) {
+    st = tfused_enqueue(p, ev);
+    if (st != PF_OK) break;
+    cudaEventSynchronize(ev[5]);
+    for (int k = 0; k < 5; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      acc[k] += ms;
+    }
+  }
+  for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+  PF_CK(st);
+  for (int k = 0; k < 5; ++k) stage_ms[k] = acc[k] / (double)n_iter;
+  return leave(p);
+}
+
 int pf_transport_solve(pf_plan* p, const pf_transport_params* P, const uint8_t* solid, const double* u, double* chi,
                        double* grad, double* history, pf_transport_result* res) {
   PF_CK(pf_transport_begin(p, P, solid, u, chi, grad, history, res));

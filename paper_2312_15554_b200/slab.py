@@ -249,7 +249,7 @@ def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalt
     else:
         st = {k: t.as_tensor(np.asarray(init_local[k], dtype=np.float64)).reshape(-1).to(dev).clone()
               for k in ("u", "u_tilde", "q", "a", "lam")}
-    solid = t.as_tensor(np.ascontiguousarray(solid_local, dtype=np.uint8)).reshape(-1).to(dev)
+    solid = t.as_tensor(np.array(solid_local, dtype=np.uint8, copy=True)).reshape(-1).to(dev)
     solver = SlabStokes(be, dims, cfg, penalties, solid, st, group)
     rep = solver.solve()
     t.cuda.synchronize(dev)
