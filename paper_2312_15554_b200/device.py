@@ -141,45 +141,54 @@ def solid_on_device(indicator, device):
     return cache[key]
 
 
-_STAGE_BYTES = 64 << 20
+_STAGE_BYTES = 32 << 20
+_STAGES = 4
 _stage = threading.local()
 
 
-def _stage_buffers(device):
-    bufs = getattr(_stage, "bufs", None)
-    if bufs is None or bufs[0].device.type != "cpu":
+def _stage_buffers():
+    st = getattr(_stage, "bufs", None)
+    if st is None:
         t = torch()
-        bufs = _stage.bufs = [t.empty(_STAGE_BYTES, dtype=t.uint8, pin_memory=True) for _ in range(2)]
-        _stage.events = [t.cuda.Event() for _ in range(2)]
-    return _stage.bufs, _stage.events
+        _stage.bufs = [t.empty(_STAGE_BYTES, dtype=t.uint8, pin_memory=True) for _ in range(_STAGES)]
+        _stage.events = [t.cuda.Event() for _ in range(_STAGES)]
+        from concurrent.futures import ThreadPoolExecutor
+
+        _stage.pool = ThreadPoolExecutor(max_workers=_STAGES)
+    return _stage.bufs, _stage.events, _stage.pool
 
 
 def to_host(x) -> np.ndarray:
-    """CUDA tensor -> new numpy array through two reusable pinned staging buffers
-    (device-to-host DMA of chunk i+1 overlaps the host copy of chunk i); several
-    times faster than a pageable ``.cpu()`` for multi-GB solver states."""
+    """CUDA tensor -> new numpy array.  Device-to-host DMA into a ring of pinned
+    staging buffers (~55 GB/s) overlapped with parallel host copies out of them
+    (numpy releases the GIL), several times faster than a pageable ``.cpu()`` for
+    multi-GB solver states."""
     t = torch()
     x = x.contiguous()
     out = np.empty(tuple(x.shape), dtype={t.float64: np.float64, t.uint8: np.uint8,
                                           t.complex128: np.complex128}[x.dtype])
     nbytes = out.nbytes
-    if nbytes <= (1 << 20):
+    if nbytes <= (4 << 20):
         return x.cpu().numpy().copy()
     src = x.view(-1).view(t.uint8)
     dst = out.reshape(-1).view(np.uint8)
-    bufs, evs = _stage_buffers(x.device)
+    bufs, evs, pool = _stage_buffers()
     stream = t.cuda.current_stream(x.device)
     chunks = [(o, min(_STAGE_BYTES, nbytes - o)) for o in range(0, nbytes, _STAGE_BYTES)]
-    for i, (o, k) in enumerate(chunks[:2]):
-        bufs[i][:k].copy_(src[o:o + k], non_blocking=True)
-        evs[i].record(stream)
-    for i, (o, k) in enumerate(chunks):
-        j = i & 1
+    pending = [None] * _STAGES
+
+    def host_copy(j, o, k):
         evs[j].synchronize()
         np.copyto(dst[o:o + k], bufs[j][:k].numpy())
-        nxt = i + 2
-        if nxt < len(chunks):
-            o2, k2 = chunks[nxt]
-            bufs[j][:k2].copy_(src[o2:o2 + k2], non_blocking=True)
-            evs[j].record(stream)
+
+    for i, (o, k) in enumerate(chunks):
+        j = i % _STAGES
+        if pending[j] is not None:
+            pending[j].result()  # staging buffer j is free again
+        bufs[j][:k].copy_(src[o:o + k], non_blocking=True)
+        evs[j].record(stream)
+        pending[j] = pool.submit(host_copy, j, o, k)
+    for f in pending:
+        if f is not None:
+            f.result()
     return out
