@@ -32,6 +32,9 @@
 #ifndef PF_PK_PREFETCH
 #define PF_PK_PREFETCH 1
 #endif
+#ifndef PF_PK_THREADS
+#define PF_PK_THREADS 128
+#endif
 
 namespace pf {
 namespace fz {
@@ -355,7 +358,7 @@ struct SpecArgs {
 template <int N>
 struct PK2 {
   using C = Cfg<N>;
-  static constexpr int T = 128;
+  static constexpr int T = PF_PK_THREADS;
   static constexpr int NGP = T / C::G;
   static constexpr int CP = NGP / 2;  // 3 components x CP columns over NGP groups
   static constexpr int NSEQ = 3 * CP;
