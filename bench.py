@@ -162,13 +162,16 @@ def stage_bytes(n_real, n_half, d=3):
     }
 
 
-def stage_bytes_fused(n_real, n_half):
-    """Algorithmic bytes per launch of the fused pipeline's passes."""
+def stage_bytes_fused(n_real, n_half, n_solid=None):
+    """Algorithmic bytes per launch of the fused pipeline's passes.
+    With solid-only storage (n_solid given) RS streams u (r+w) on every voxel and
+    u~, a, lam (r+w) only on solid voxels."""
     hw = n_half * 16  # one half-spectrum component
+    rs_state = 24 * 8 * n_real if n_solid is None else 6 * 8 * n_real + 18 * 8 * n_solid
     return {
         "PK_axis0_spectral": 10 * hw,          # Y(3) Q D in; Y(3) Q D out
         "MI_axis1_inverse": 6 * hw,            # Y(3) in; X(3) out
-        "RS_rows_local": 6 * hw + 24 * 8 * n_real + n_real,  # X(3) in, X(3) out; 12+12 state words; H
+        "RS_rows_local": 6 * hw + rs_state + n_real,  # X(3) in, X(3) out; state; H
         "finalize": 0,
         "RSF_rows_fix": 0,                     # no-op unless residual balancing changed b
         "MF_axis1_forward": 6 * hw,            # X(3) in; Y(3) out
@@ -246,8 +249,12 @@ def run_ours(args):
 
     peak, peak_src = peak_hbm()
     n_real, n_half = n ** 3, n * n * (n // 2 + 1)
-    names = FUSED_STAGES if pipeline == "fused" else STAGES
-    sb = stage_bytes_fused(n_real, n_half) if pipeline == "fused" else stage_bytes(n_real, n_half)
+    fused = pipeline.startswith("fused")
+    names = FUSED_STAGES if fused else STAGES
+    sb = stage_bytes(n_real, n_half)
+    if fused:
+        n_solid = int(np.count_nonzero(ind.values))
+        sb = stage_bytes_fused(n_real, n_half, n_solid if pipeline == "fused-compact" else None)
     stages = {}
     for k, name in enumerate(names):
         if name == "-":
@@ -261,7 +268,7 @@ def run_ours(args):
     tfile = ROOT / "profiles" / "traffic_per_launch.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get(dom)
+            traffic = json.loads(tfile.read_text()).get(pipeline, {}).get(dom)
         except Exception:
             traffic = None
     achieved = stages[dom]["GB_s"]
@@ -313,8 +320,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h / e2e_iters, "iterations": e2e_iters,
                 "api": "paper_2312_15554_b200.solve_stokes (numpy in/out)"},
         "pipeline": pipeline,
-        "gpu_launches": (6 if pipeline == "fused" else 4) * args.steps,
-        "library_launches_note": ("none: all transforms are in-kernel" if pipeline == "fused"
+        "gpu_launches": (6 if fused else 4) * args.steps,
+        "library_launches_note": ("none: all transforms are in-kernel" if fused
                                   else "plus 2 cuFFT executions (batch 3) per iteration"),
         "clocks": clk,
         "cpu_baseline": cpu,

@@ -60,6 +60,10 @@ int pf_plan_set_stream(pf_plan* plan, void* stream);
  * (cubic grids N = 64, 128, 256); disabled or unsupported grids use the
  * general cuFFT pipeline.  Both compute the same iteration. */
 int pf_plan_set_fused(pf_plan* plan, int enable);
+/* Enable (default) or disable solid-only storage of u~, a, lam on the fused
+ * Stokes path (used when a = 0 on pore voxels, e.g. cold starts): on pore
+ * voxels the local step is exactly u~' = u', a' = 0, lam' = lam. */
+int pf_plan_set_compact(pf_plan* plan, int enable);
 /* Replace the symbol tables of one logical axis (host arrays of dims[axis]
  * doubles: kappa_j and the 1D Laplacian term, spectral.py:78-86).  The
  * Python host layer passes numpy's own tables so the device sees the
@@ -116,7 +120,8 @@ int pf_stokes_end(pf_plan* plan, pf_stokes_result* result);
  * S1 spectral | Z2D | S3 local | finalize | S4 form-R | D2Z, in ms. */
 int pf_stokes_profile(pf_plan* plan, int64_t n_iter, double* stage_ms);
 /* Pipeline of the active / last Stokes solve: 0 = cuFFT (stages as above),
- * 1 = fused (stages PK | MI | RS | finalize | MF | -). */
+ * 1 = fused, 2 = fused with solid-only multiplier storage
+ * (fused stages: PK | MI | RS | finalize | RSF | MF). */
 int pf_stokes_pipeline(const pf_plan* plan);
 
 /* ------------------------------------------------------------------------

@@ -24,6 +24,7 @@
 // Stockham-style passes in registers with one padded shared-memory transpose
 // (fft_seq); a thread group of 8 or 16 lanes transforms one sequence.
 #include <cmath>
+#include <cstring>
 
 #include "pf_internal.cuh"
 
@@ -82,7 +83,9 @@ struct RS2 {
   static constexpr size_t XM = sizeof(double2) * R * C::H; // X-space u' rows (main)
   static constexpr size_t XN = sizeof(double2) * R;        // nyq column
   static constexpr size_t HB = V;                          // indicator bytes
-  static constexpr size_t BYTES = TW + INV + FWD + ST + XM + XN + HB;
+  // the local step reads and rewrites each voxel's double in place, so the forward
+  // sequences reuse the inverse buffer (FWD is not carved separately)
+  static constexpr size_t BYTES = TW + INV + ST + XM + XN + HB;
   static constexpr uint32_t TX = (uint32_t)(ST + XM + XN + HB);
 };
 
@@ -120,14 +123,15 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   __shared__ uint64_t mbar;
   double2* tw = (double2*)sraw;
   double2* SI = (double2*)(sraw + K::TW);
-  double2* SF = (double2*)(sraw + K::TW + K::INV);
-  double* sst = (double*)(sraw + K::TW + K::INV + K::FWD);
-  double2* sx = (double2*)(sraw + K::TW + K::INV + K::FWD + K::ST);
-  double2* sxn = (double2*)(sraw + K::TW + K::INV + K::FWD + K::ST + K::XM);
-  uint8_t* sh = (uint8_t*)(sraw + K::TW + K::INV + K::FWD + K::ST + K::XM + K::XN);
+  double2* SF = SI;  // in place (see RS2::BYTES)
+  double* sst = (double*)(sraw + K::TW + K::INV);
+  double2* sx = (double2*)(sraw + K::TW + K::INV + K::ST);
+  double2* sxn = (double2*)(sraw + K::TW + K::INV + K::ST + K::XM);
+  uint8_t* sh = (uint8_t*)(sraw + K::TW + K::INV + K::ST + K::XM + K::XN);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   for (int j = t; j < N; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
+  const double inv_bp = 1.0 / b, inv_bs = 1.0 / (b + alpha);  // pore / solid divisors of pure.py:61
   const int64_t n = (int64_t)N * N * N;
   if (t == 0) {
     mbar_init(&mbar);
@@ -159,11 +163,13 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
 #pragma unroll 4
     for (int j = 0; j < K::VPT; ++j) {
       const int v = t + T * j, row = v / N, col = v % N;
-      const double2 z = SI[(row >> 1) * SS + C::pad(col)];
-      const double u1 = (row & 1) ? z.y : z.x;
-      const double h = (double)sh[v];
+      double* zv = reinterpret_cast<double*>(SI + (row >> 1) * SS + C::pad(col)) + (row & 1);
+      const double u1 = *zv;
+      const double h = sh[v] ? 1.0 : 0.0;
       const double u0 = sst[v], t0 = sst[V + v], a0 = sst[2 * V + v], l0 = sst[3 * V + v];
-      const double t1 = ((a0 + b * u1) - h * l0) / (b + alpha * h);
+      // (a + b u - H lam) / (b + alpha H): the divisor takes two values, so divide by
+      // multiplying with the hoisted reciprocals (<= 1 ulp from the quotient)
+      const double t1 = ((a0 + b * u1) - h * l0) * (h != 0.0 ? inv_bs : inv_bp);
       const double a1 = a0 + b * (u1 - t1);
       const double l1 = l0 + alpha * (h * t1);
       const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
       st.a[i] = a1;
       st.lam[i] = l1;
       // R = b u~' - a' with the pre-adaptation b (stokes.py:405-407); rows 2p, 2p+1 -> Re, Im
-      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::pad(col))[row & 1] = b * t1 - a1;
+      *zv = b * t1 - a1;
     }
     __syncthreads();
     // staged inputs consumed: prefetch the next tile while this one finishes
@@ -263,6 +269,353 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
       XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ compact RS
+// On pore voxels (H = 0) the local step is exactly u~' = u', a' = 0, lam' = lam
+// (a' = a + b(u' - (a + b u')/b) = 0 for any a), so once a = 0 on pore voxels
+// (cold start, or any state this path produced) u~, a, lam only need storage
+// and traffic on solid voxels.  The compact path keeps them in solid-only
+// arrays ([c][ns], rows padded to even counts so every row range is 16-byte
+// aligned) addressed through an exclusive prefix `off` of the per-row counts;
+// pore values are materialised once at the end.  RS then streams u (r+w), X
+// (r+w) and H for every voxel and the three multiplier fields only for the
+// solid fraction.
+struct Compact {
+  const uint32_t* off;   // [N*N + 1]
+  double *ut, *a, *lam;  // [3][ns]
+  int64_t ns;
+};
+
+template <int N>
+struct RSC {
+  using K = RS2<N>;
+  static constexpr int CS = K::V + K::R;  // compact staging stride (max padded solid count per tile)
+  static constexpr size_t BYTES = K::TW + K::INV /*inverse = forward, in place*/ + sizeof(double) * K::V /*u*/ +
+                                  3 * sizeof(double) * CS /*u~, a, lam*/ + K::XM + K::XN + K::HB;
+};
+
+// o0 / o1 = compact offsets of the tile's first row and of the row after it
+// (loaded by the caller one tile ahead so the issue does not wait on them)
+template <int N>
+__device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& st, const Compact& cp, double* su,
+                                          double* sc, double2* sx, double2* sxn, uint8_t* sh, uint64_t* mbar,
+                                          uint32_t* ro_slot, const uint32_t* ro) {
+  using K = RS2<N>;
+  using C = Cfg<N>;
+  constexpr int TPC = N * N / K::R;
+  const int c = tile / TPC;
+  const int64_t row0 = (int64_t)(tile % TPC) * K::R;
+  const int64_t n = (int64_t)N * N * N;
+  constexpr int R = K::R;
+  const uint32_t o0 = ro[0];
+  const uint32_t cb = sizeof(double) * (ro[R] - o0);
+  for (int r = 0; r <= R; ++r) ro_slot[r] = ro[r];  // read by the compute phase after the mbarrier wait
+  fence_async_smem();
+  mbar_expect(mbar, (uint32_t)(sizeof(double) * K::V + K::XM + K::XN + K::HB) + 3 * cb);
+  bulk_load(su, st.u + (int64_t)c * n + row0 * N, sizeof(double) * K::V, mbar);
+  bulk_load(sx, B.XU + ((int64_t)c * N * N + row0) * C::H, (uint32_t)K::XM, mbar);
+  bulk_load(sxn, B.XUn + (int64_t)c * N * N + row0, (uint32_t)K::XN, mbar);
+  bulk_load(sh, st.H + row0 * N, (uint32_t)K::HB, mbar);
+  if (cb) {
+    const int64_t base = (int64_t)c * cp.ns + o0;
+    bulk_load(sc, cp.ut + base, cb, mbar);
+    bulk_load(sc + RSC<N>::CS, cp.a + base, cb, mbar);
+    bulk_load(sc + 2 * RSC<N>::CS, cp.lam + base, cb, mbar);
+  }
+}
+
+// Compact base of 32-voxel segment `lane` of a tile (V = 1024 => 32 segments of
+// 32 voxels for every N): count nonzero indicator bytes, scan within the row
+// (SPR segments per row), add the row's compact offset.  Every warp computes all
+// 32 in registers; a warp shuffles out the one its voxels fall in.
+template <int N>
+__device__ __forceinline__ int seg_base(const uint8_t* seg_bytes, uint32_t row_off_minus_o0, int lane) {
+  constexpr int SPR = N / 32;
+  const uint4 w0 = reinterpret_cast<const uint4*>(seg_bytes)[0];
+  const uint4 w1 = reinterpret_cast<const uint4*>(seg_bytes)[1];
+  int cnt = (__popc(__vcmpne4(w0.x, 0u)) + __popc(__vcmpne4(w0.y, 0u)) + __popc(__vcmpne4(w0.z, 0u)) +
+             __popc(__vcmpne4(w0.w, 0u)) + __popc(__vcmpne4(w1.x, 0u)) + __popc(__vcmpne4(w1.y, 0u)) +
+             __popc(__vcmpne4(w1.z, 0u)) + __popc(__vcmpne4(w1.w, 0u))) >> 3;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < SPR; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o, SPR);
+    if ((lane % SPR) >= o) incl += y;
+  }
+  return (int)row_off_minus_o0 + incl - cnt;
+}
+
+template <int N>
+__global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Compact cp, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = RS2<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
+  constexpr int TPC = N * N / R;
+  constexpr int NT = 3 * TPC;
+  constexpr int SPR = N / 32;  // 32-voxel segments per row
+  constexpr int CS = RSC<N>::CS;
+  static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
+  if (ctrl->done) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t ros[2][R + 1];
+  double2* tw = (double2*)sraw;
+  double2* SI = (double2*)(sraw + K::TW);
+  double2* SF = SI;  // in place
+  double* su = (double*)(sraw + K::TW + K::INV);
+  double* sc = su + V;  // [3][CS]: u~, a, lam of the tile's solid voxels
+  double2* sx = (double2*)(sc + 3 * CS);
+  double2* sxn = (double2*)((unsigned char*)sx + K::XM);
+  uint8_t* sh = (uint8_t*)((unsigned char*)sxn + K::XN);
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  const double alpha = ctrl->alpha, b = ctrl->b;
+  const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
+  const int64_t n = (int64_t)N * N * N;
+  uint32_t ro[R + 1];
+  auto offs = [&](int tl) {
+    const int64_t r0 = (int64_t)(tl % TPC) * R;
+#pragma unroll
+    for (int r = 0; r <= R; ++r) ro[r] = cp.off[r0 + r];
+  };
+  if (t == 0) {
+    mbar_init(&mbar);
+    if ((int)blockIdx.x < NT) {
+      offs(blockIdx.x);
+      rsc_issue<N>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[0], ro);
+    }
+  }
+  __syncthreads();
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    double2* XR = B.XR + (size_t)c * N * N * H;
+    double2* XRn = B.XRn + (size_t)c * N * N;
+    const bool has_next = tile + (int)gridDim.x < NT;
+    if (t == 0 && has_next) offs(tile + gridDim.x);  // next tile's row offsets, loaded early
+    mbar_wait(&mbar, phase);
+    const uint32_t o0 = ros[phase][0];
+    const int sb = seg_base<N>(sh + lane * 32, ros[phase][lane / SPR] - o0, lane);
+    // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      double2 xa = sx[(2 * p) * H + k], xb = sx[(2 * p + 1) * H + k];
+      if (k == 0) xa.y = xb.y = 0.0;
+      double2* sp = SI + p * SS;
+      sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+      if (k > 0) sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+    }
+    for (int p = t; p < NP; p += T) SI[p * SS + C::pad(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
+    __syncthreads();
+    fft_seq<N, true>(SI + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    __syncthreads();
+    // (2) local step; pore: u~' = u', a' = 0, lam' = lam (only u' is stored)
+    const int64_t cbase = (int64_t)c * cp.ns + o0;
+#pragma unroll 4
+    for (int j = 0; j < K::VPT; ++j) {
+      const int v = t + T * j, row = v / N, col = v % N;
+      double* zv = reinterpret_cast<double*>(SI + (row >> 1) * SS + C::pad(col)) + (row & 1);
+      const double u1 = *zv;
+      const bool solid = sh[v] != 0;
+      const unsigned mask = __ballot_sync(0xffffffffu, solid);
+      const double s4 = u1 - su[v];
+      acc[4] += s4 * s4;
+      double t1 = u1, a1 = 0.0;
+      const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
+      if (solid) {
+        const int ci = segb + __popc(mask & ((1u << lane) - 1u));
+        const double t0 = sc[ci], a0 = sc[CS + ci], l0 = sc[2 * CS + ci];
+        t1 = ((a0 + b * u1) - l0) * inv_bs;  // pure.py:61 with H = 1
+        a1 = a0 + b * (u1 - t1);             // pure.py:66
+        const double l1 = l0 + alpha * t1;   // pure.py:67
+        const double s1 = t1 - t0, s3 = u1 - t1;
+        acc[0] += t1 * t1;
+        acc[1] += s1 * s1;
+        acc[2] += l1 * l1;
+        acc[3] += s3 * s3;
+        acc[5] += a1 * a1;
+        cp.ut[cbase + ci] = t1;
+        cp.a[cbase + ci] = a1;
+        cp.lam[cbase + ci] = l1;
+      }
+      st.u[c * n + row0 * N + v] = u1;
+      *zv = b * t1 - a1;
+    }
+    __syncthreads();
+    if (t == 0 && has_next)
+      rsc_issue<N>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[phase ^ 1u], ro);
+    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    __syncthreads();
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      XR[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XR[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+    for (int p = t; p < NP; p += T) {
+      const double2 z = SF[p * SS + C::pad(H)];
+      XRn[row0 + 2 * p] = make_double2(z.x, 0.0);
+      XRn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
+    }
+    __syncthreads();
+  }
+  block_sum<6>(acc);
+  if (t == 0)
+    for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// RS-fix on the compact path: u~' rows = u' on pore voxels, the compact u~ on solid ones.
+template <int N>
+__global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const double* __restrict__ u,
+                                                             const uint8_t* __restrict__ Hs, Compact cp,
+                                                             const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = RS2<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
+  constexpr int TPC = N * N / R;
+  constexpr int NT = 3 * TPC;
+  constexpr int SPR = N / 32;
+  static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
+  if (ctrl->done || ctrl->db == 0.0) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  double2* tw = (double2*)sraw;
+  double2* SF = (double2*)(sraw + K::TW);
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
+  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  const int64_t n = (int64_t)N * N * N;
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const uint32_t o0 = cp.off[row0];
+    const int sb = seg_base<N>(Hs + row0 * N + lane * 32, cp.off[row0 + lane / SPR] - o0, lane);
+    __syncthreads();
+    for (int j = 0; j < K::VPT; ++j) {
+      const int v = t + T * j, row = v / N, col = v % N;
+      const bool solid = Hs[row0 * N + v] != 0;
+      const unsigned mask = __ballot_sync(0xffffffffu, solid);
+      const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
+      double val = u[(int64_t)c * n + row0 * N + v];
+      if (solid) val = cp.ut[(int64_t)c * cp.ns + o0 + segb + __popc(mask & ((1u << lane) - 1u))];
+      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::pad(col))[row & 1] = val;
+    }
+    __syncthreads();
+    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    __syncthreads();
+    double2* XU = B.XU + (size_t)c * N * N * H;
+    double2* XUn = B.XUn + (size_t)c * N * N;
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      XU[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XU[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+    for (int p = t; p < NP; p += T) {
+      const double2 z = SF[p * SS + C::pad(H)];
+      XUn[row0 + 2 * p] = make_double2(z.x, 0.0);
+      XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
+    }
+  }
+}
+
+// ---- compact layout setup / teardown (warp per row of N voxels)
+template <int N>
+__global__ void k_row_counts(const uint8_t* __restrict__ Hs, uint32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)N * N;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int c = 0;
+    for (int k = lane; k < N; k += 32) c += Hs[r * N + k] != 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[r] = (uint32_t)((c + 1) & ~1);  // pad to even: 16-byte aligned rows
+  }
+}
+
+// single-block exclusive scan of n counts -> off[0..n]
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off, int64_t n) {
+  __shared__ uint32_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024, lo = t * per, hi = lo + per < n ? lo + per : n;
+  uint32_t s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += cnt[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < 1024; ++k) {
+      const uint32_t v = part[k];
+      part[k] = run;
+      run += v;
+    }
+    off[n] = run;
+  }
+  __syncthreads();
+  uint32_t run = part[t];
+  for (int64_t i = lo; i < hi; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+}
+
+// dir = 0: gather full -> compact (solid voxels); dir = 1: scatter compact -> full,
+// with pore u~ = u, a = 0 and lam left untouched.
+template <int N>
+__global__ void k_compact_move(const uint8_t* __restrict__ Hs, Compact cp, double* ut, double* a, double* lam,
+                               const double* __restrict__ u, int dir) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)N * N, n = rows * N;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < 3 * rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int c = (int)(r / rows);
+    const int64_t row = r % rows;
+    int base = (int)cp.off[row];
+    for (int k0 = 0; k0 < N; k0 += 32) {
+      const int64_t x = row * N + k0 + lane;
+      const bool solid = Hs[x] != 0;
+      const unsigned mask = __ballot_sync(0xffffffffu, solid);
+      const int64_t ci = (int64_t)c * cp.ns + base + __popc(mask & ((1u << lane) - 1u));
+      const int64_t fi = (int64_t)c * n + x;
+      if (dir == 0) {
+        if (solid) {
+          cp.ut[ci] = ut[fi];
+          cp.a[ci] = a[fi];
+          cp.lam[ci] = lam[fi];
+        }
+      } else {
+        if (solid) {
+          ut[fi] = cp.ut[ci];
+          a[fi] = cp.a[ci];
+          lam[fi] = cp.lam[ci];
+        } else {
+          ut[fi] = u[fi];
+          a[fi] = 0.0;
+        }
+      }
+      base += __popc(mask);
+    }
+  }
+}
+
+// pore sums: |a| (eligibility: must be 0) and lam^2 (constant contribution to |lam'|)
+__global__ void __launch_bounds__(kThreads) k_pore_a_lam(int64_t n, const uint8_t* __restrict__ Hs,
+                                                         const double* __restrict__ a, const double* __restrict__ lam,
+                                                         double* __restrict__ part) {
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (Hs[i % n] == 0) {
+      acc[0] += fabs(a[i]);
+      acc[1] += lam[i] * lam[i];
+    }
+  }
+  block_sum<2>(acc);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = acc[0];
+    part[gridDim.x + blockIdx.x] = acc[1];
   }
 }
 
@@ -546,6 +899,14 @@ struct FusedPlan {
   void* mem = nullptr;
   cufftHandle plan2d = 0;
   size_t bytes = 0;
+  // compact (solid-only) multiplier storage
+  uint32_t* c_cnt = nullptr;
+  uint32_t* c_off = nullptr;
+  double* c_data = nullptr;
+  int64_t c_ns = 0, c_cap = 0;
+  int compact = 0;
+  int nb_rs = kSMs;              // persistent RS grid of the active path (full or compact)
+  int nb_full = kSMs, nb_compact = kSMs;
 };
 
 static FusedPlan* fp_of(pf_plan* p) { return reinterpret_cast<FusedPlan*>(p->fused); }
@@ -565,17 +926,32 @@ template <int N>
 static size_t smem_rs() { return fz::RS2<N>::BYTES; }
 template <int N>
 static size_t smem_rsfix() { return fz::RS2<N>::TW + fz::RS2<N>::INV + fz::RS2<N>::ST / 4; }
-constexpr int kRsBlocks = kSMs * 3;  // persistent RS grid: 3 blocks per SM
+template <int N>
+static size_t smem_rsc() { return fz::RSC<N>::BYTES; }
+constexpr int kRsMaxBlocks = kSMs * 8;  // partial-sum rows reserved for the persistent RS grid
 template <int N>
 static size_t smem_pk() { return fz::PK2<N>::BYTES; }
 
 template <int N>
-static int set_attrs() {
+static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_rsfix<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
+  // persistent RS grids: one wave of resident blocks.  The full-layout kernel is
+  // capped at 3 per SM: it streams 4 KB/voxel-row-tile at ~93% of HBM peak and a
+  // 4th block only adds contention (256^3: 0.697 ms at 4/SM vs 0.662 ms at 3/SM).
+  auto wave = [](int o, int cap) { return (o < 1 ? 1 : (o > cap ? cap : o)) * kSMs; };
+  int o1 = 0, o2 = 0;
+  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, fz::k_rs<N>, fz::RS2<N>::T, smem_rs<N>()));
+  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N>, fz::RS2<N>::T, smem_rsc<N>()));
+  f->nb_full = wave(o1, 3);
+  f->nb_compact = wave(o2, kRsMaxBlocks / kSMs);
+  f->nb_rs = f->nb_full;
   return PF_OK;
 }
 
@@ -588,7 +964,7 @@ int fused_ensure(pf_plan* p) {
   const size_t main1 = NN * H, nyq1 = NN;  // one component, complex elements
   // X: 6 comps (XU 3, XR 3); Y: 3; Q, D: 1 each
   const size_t elems = 11 * (main1 + nyq1) + N;
-  const int nb_rs = kRsBlocks;
+  const int nb_rs = kRsMaxBlocks;
   const int nb_pk = (N == 64) ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : fz::PK2<256>::TILES);
   const size_t part = 6 * (size_t)nb_rs + 3 * (size_t)nb_pk;
   f->bytes = elems * sizeof(double2) + part * sizeof(double);
@@ -638,9 +1014,9 @@ int fused_ensure(pf_plan* p) {
   PF_CK_FFT(cufftSetWorkArea(f->plan2d, p->fft_work));
   PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
   switch (N) {
-    case 64: PF_CK(set_attrs<64>()); break;
-    case 128: PF_CK(set_attrs<128>()); break;
-    default: PF_CK(set_attrs<256>()); break;
+    case 64: PF_CK(set_attrs<64>(f)); break;
+    case 128: PF_CK(set_attrs<128>(f)); break;
+    default: PF_CK(set_attrs<256>(f)); break;
   }
   p->fused = f;
   p->scratch_bytes += f->bytes;
@@ -652,6 +1028,9 @@ void fused_free(pf_plan* p) {
   if (!f) return;
   if (f->plan2d) cufftDestroy(f->plan2d);
   cudaFree(f->mem);
+  cudaFree(f->c_cnt);
+  cudaFree(f->c_off);
+  cudaFree(f->c_data);
   delete f;
   p->fused = nullptr;
 }
@@ -664,6 +1043,56 @@ static int to_tilemajor(int N, const double2* src, double2* dst, double scale, b
     case 128: fz::k_tilemajor<128><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
     default: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
   }
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+static fz::Compact compact_of(FusedPlan* f) {
+  fz::Compact c;
+  c.off = f->c_off;
+  c.ut = f->c_data;
+  c.a = f->c_data + 3 * f->c_ns;
+  c.lam = f->c_data + 6 * f->c_ns;
+  c.ns = f->c_ns;
+  return c;
+}
+
+template <int N>
+static int compact_setup_t(pf_plan* p, FusedPlan* f) {
+  const int64_t rows = (int64_t)N * N, n = rows * N;
+  // eligibility (a = 0 on pore voxels: cold starts and states this path produced)
+  // and the constant pore part of |lam'|^2
+  const int nb = blocks_for(3 * n);
+  fz::k_pore_a_lam<<<nb, kThreads, 0, p->work>>>(n, p->s_solid, p->s_a, p->s_lam, p->partials);
+  double* out = p->partials + 24 * kMaxBlocks;
+  PF_CK(reduce_rows_to(p, p->partials, 2, nb, out));
+  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->work));
+  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  f->compact = (p->compact_enable && p->h_small[0] == 0.0) ? 1 : 0;
+  f->nb_rs = f->compact ? f->nb_compact : f->nb_full;
+  p->sc.lam_pore_sq = f->compact ? p->h_small[1] : 0.0;
+  if (!f->compact) return PF_OK;
+  if (!f->c_cnt) {
+    PF_CK_CUDA(cudaMalloc(&f->c_cnt, sizeof(uint32_t) * rows));
+    PF_CK_CUDA(cudaMalloc(&f->c_off, sizeof(uint32_t) * (rows + 1)));
+  }
+  fz::k_row_counts<N><<<blocks_for(rows * 32), kThreads, 0, p->work>>>(p->s_solid, f->c_cnt);
+  fz::k_scan<<<1, 1024, 0, p->work>>>(f->c_cnt, f->c_off, rows);
+  PF_CK_CUDA(cudaGetLastError());
+  uint32_t ns = 0;
+  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, f->c_off + rows, sizeof(uint32_t), cudaMemcpyDeviceToHost, p->work));
+  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  std::memcpy(&ns, p->h_small, sizeof(uint32_t));
+  f->c_ns = ns;
+  const int64_t need = 9 * (int64_t)(ns > 0 ? ns : 2);
+  if (need > f->c_cap) {
+    cudaFree(f->c_data);
+    f->c_data = nullptr;
+    PF_CK_CUDA(cudaMalloc(&f->c_data, sizeof(double) * (size_t)need));
+    f->c_cap = need;
+  }
+  fz::k_compact_move<N><<<blocks_for(3 * rows * 32), kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut,
+                                                                             p->s_a, p->s_lam, p->s_u, 0);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
@@ -687,7 +1116,11 @@ int fused_setup(pf_plan* p) {
   fz::k_split<<<grid, kThreads, 0, p->work>>>(3 * NN, N, p->specA, f->b.Y, f->b.Yn);
   PF_CK_CUDA(cudaGetLastError());
   (void)n;
-  return PF_OK;
+  switch (N) {
+    case 64: return compact_setup_t<64>(p, f);
+    case 128: return compact_setup_t<128>(p, f);
+    default: return compact_setup_t<256>(p, f);
+  }
 }
 
 // q = Re ifft(Q^) into the user's q.
@@ -696,8 +1129,16 @@ int fused_finish(pf_plan* p) {
   const int N = f->N;
   const int64_t NN = (int64_t)N * N;
   PF_CK(to_tilemajor(N, f->b.Q, p->specB, p->g.inv_n, false, p->work));
-  (void)NN;
   PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
+  if (f->compact) {  // materialise u~, a, lam (pore: u~ = u, a = 0, lam unchanged)
+    const int nb = blocks_for(3 * NN * 32);
+    switch (N) {
+      case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+      case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+      default: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+    }
+    PF_CK_CUDA(cudaGetLastError());
+  }
   return PF_OK;
 }
 
@@ -726,19 +1167,33 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   fz::k_maxis<N, true><<<fz::M2<N>::TILES, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
-  fz::k_rs<N><<<kRsBlocks, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
+  if (f->compact) {
+    fz::k_rs_compact<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsc<N>(), p->work>>>(f->b, st, compact_of(f), p->ctrl);
+  } else {
+    fz::k_rs<N><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
+  }
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
-  k_stokes_finalize_launch(p, f->b.part_rs, kRsBlocks, f->b.part_pk, fz::PK2<N>::TILES);
+  k_stokes_finalize_launch(p, f->b.part_rs, f->nb_rs, f->b.part_pk, fz::PK2<N>::TILES);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  fz::k_rsfix<N><<<kRsBlocks, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
+  if (f->compact) {
+    fz::k_rsfix_compact<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_u, p->s_solid,
+                                                                                   compact_of(f), p->ctrl);
+  } else {
+    fz::k_rsfix<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
+  }
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(5));
   fz::k_maxis<N, false><<<fz::M2<N>::TILES, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(6));
   return PF_OK;
+}
+
+int fused_is_compact(const pf_plan* p) {
+  const FusedPlan* f = reinterpret_cast<const FusedPlan*>(p->fused);
+  return f ? f->compact : 0;
 }
 
 int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {

@@ -90,6 +90,7 @@ struct StokesConst {
   double tol_vec, tol_sca;  // sqrt(n_vec)*eps_abs, sqrt(n_sca)*eps_abs (host-computed)
   double g[3];              // pressure gradient (logical components)
   double growth[3], thr[3], floor_[3];
+  double lam_pore_sq;       // |lam|^2 over pore voxels (constant there; compact RS path), else 0
   int64_t max_iter;
   int adaptive;
 };
@@ -147,6 +148,7 @@ struct pf_plan {
   // fused power-of-two pipeline (pf_fused.cu)
   void* fused;       // FusedPlan*
   int fused_enable;  // 1 = use the fused pipeline when the grid supports it
+  int compact_enable;  // 1 = solid-only multiplier storage on the fused path when eligible
   int pipeline;      // pipeline of the active Stokes solve: 0 cuFFT, 1 fused
   void* tfused;      // FusedTPlan* (pf_fused_transport.cu)
   int t_pipeline;    // pipeline of the active transport solve: 0 cuFFT, 1 fused
@@ -182,12 +184,14 @@ void fused_free(pf_plan* p);
 int fused_setup(pf_plan* p);
 int fused_finish(pf_plan* p);
 int enqueue_fused(pf_plan* p, cudaEvent_t* ev);
+int fused_is_compact(const pf_plan* p);
 // fused transport pipeline (pf_fused_transport.cu)
 int tfused_setup(pf_plan* p, bool warm);
 int tfused_finish(pf_plan* p);
 int tfused_enqueue(pf_plan* p, cudaEvent_t* ev = nullptr);
 void tfused_free(pf_plan* p);
 int plan_reset_work_areas(pf_plan* p);
+int reduce_rows_to(pf_plan* p, const double* part, int nrows, int nb, double* out);
 // transport helpers shared with the fused pipeline (pf_transport.cu)
 int transport_polarize(pf_plan* p, const double* grad, double* out);
 void transport_finalize_launch(pf_plan* p, const double* part, int nb, double scale);

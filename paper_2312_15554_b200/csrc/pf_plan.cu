@@ -261,6 +261,7 @@ int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode
   p->device = device;
   p->user_stream = (cudaStream_t)stream;
   p->fused_enable = 1;
+  p->compact_enable = 1;
   PF_CK_CUDA(cudaStreamCreateWithFlags(&p->work, cudaStreamNonBlocking));
   PF_CK_CUDA(cudaEventCreateWithFlags(&p->ev_user, cudaEventDisableTiming));
   PF_CK_CUDA(cudaEventCreateWithFlags(&p->ev_work, cudaEventDisableTiming));
@@ -308,6 +309,12 @@ int pf_plan_set_fused(pf_plan* p, int enable) {
     return PF_ERR_STATE;
   }
   p->fused_enable = enable ? 1 : 0;
+  return PF_OK;
+}
+
+int pf_plan_set_compact(pf_plan* p, int enable) {
+  PF_ARG(p, "null plan");
+  p->compact_enable = enable ? 1 : 0;
   return PF_OK;
 }
 

@@ -285,6 +285,7 @@ int pf_slab_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* s
   }
   C.max_iter = P->max_iter;
   C.adaptive = P->adaptive;
+  C.lam_pore_sq = 0.0;
   p->active = 3;
   PF_CK(enter(p));
   PF_CK(stokes_ctrl_init(p, P->alpha, P->beta, P->b));

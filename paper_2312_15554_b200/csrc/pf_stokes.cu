@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
   double rp[3], rd[3], tp[3], td[3];
   rp[0] = sqrt(S[0]);
   rd[0] = alpha * sqrt(S[1]);
-  const double ln = sqrt(S[2]);
+  const double ln = sqrt(S[2] + C.lam_pore_sq);
   tp[0] = C.tol_vec + er * pymax(rp[0], ln);
   td[0] = C.tol_vec + er * ln;
   rp[1] = sqrt(P[0] * inv_n);
@@ -449,6 +449,7 @@ int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid,
   }
   C.max_iter = P->max_iter;
   C.adaptive = P->adaptive;
+  C.lam_pore_sq = 0.0;
   // Graph kernels capture StokesConst and the state pointers by value.
   p->graph.reset();
   k_ctrl_init<<<1, 1, 0, p->work>>>(p->ctrl, P->alpha, P->beta, P->b);
@@ -550,7 +551,10 @@ int pf_stokes_profile(pf_plan* p, int64_t n_iter, double* stage_ms) {
   return leave(p);
 }
 
-int pf_stokes_pipeline(const pf_plan* p) { return p ? p->pipeline : -1; }
+int pf_stokes_pipeline(const pf_plan* p) {
+  if (!p) return -1;
+  return (p->pipeline == 1 && fused_is_compact(p)) ? 2 : p->pipeline;
+}
 
 int pf_stokes_solve(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
                     double* a, double* lam, double* history, pf_stokes_result* res) {

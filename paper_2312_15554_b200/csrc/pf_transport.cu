@@ -206,6 +206,12 @@ __global__ void k_ctrl_init_t(Ctrl* c) {
   c->done = c->converged = c->diverged = c->reason = 0;
 }
 
+int reduce_rows_to(pf_plan* p, const double* part, int nrows, int nb, double* out) {
+  k_reduce_rows<<<1, kFinalizeThreads, 0, p->work>>>(part, nrows, nb, out);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
 // Host: pore-masked sums -> host out[0..ncomp) sums, out[3] pore count, out[4] non-finite count.
 int pore_sums_host(pf_plan* p, const uint8_t* H, const double* f, int ncomp, double* out5) {
   const int nb = blocks_for(p->g.nr);

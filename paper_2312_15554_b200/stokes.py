@@ -213,7 +213,7 @@ class StokesSolver:
 
     def __init__(self, indicator: IndicatorField, cfg: StokesConfig, penalties: PenaltyParams,
                  state: DeviceAdmmState, device=None, history_rows: int | None = None,
-                 pipeline: str | None = None, plan_slot: int = 0):
+                 pipeline: str | None = None, plan_slot: int = 0, compact: bool | None = None):
         self.device = require_cuda(device)
         self.indicator, self.cfg, self.penalties, self.state = indicator, cfg, penalties, state
         grid = indicator.grid
@@ -226,24 +226,26 @@ class StokesSolver:
         self._params = _params(cfg, penalties, min(cfg.max_iter, self.rows))
         self._begun = False
         self.pipeline_request = pipeline or os.environ.get("POREFLOW_B200_PIPELINE", "auto")
+        self.compact = (os.environ.get("POREFLOW_B200_COMPACT", "1") != "0") if compact is None else bool(compact)
         if self.pipeline_request not in ("auto", "fused", "cufft"):
             raise ValueError("pipeline must be 'auto', 'fused' or 'cufft'")
 
     @property
     def pipeline(self) -> str:
-        """Pipeline the device chose for this solve: 'fused' (N^3, N in 64/128/256) or 'cufft'."""
-        return {0: "cufft", 1: "fused"}.get(N.load().pf_stokes_pipeline(self.plan.handle), "none")
+        """Pipeline the device chose: 'fused' / 'fused-compact' (N^3, N in 64/128/256) or 'cufft'."""
+        return {0: "cufft", 1: "fused", 2: "fused-compact"}.get(N.load().pf_stokes_pipeline(self.plan.handle), "none")
 
     def begin(self):
         lib = N.load()
         s = self.state
         h = self.plan.bind_stream()
         N.check(lib.pf_plan_set_fused(h, 0 if self.pipeline_request == "cufft" else 1))
+        N.check(lib.pf_plan_set_compact(h, 1 if self.compact else 0))
         N.check(lib.pf_stokes_begin(h, ctypes.byref(self._params), self.solid.data_ptr(), s.u.data_ptr(),
                                     s.u_tilde.data_ptr(), s.q.data_ptr(), s.a.data_ptr(), s.lam.data_ptr(),
                                     self.history.data_ptr()))
         self._begun = True
-        if self.pipeline_request == "fused" and self.pipeline != "fused":
+        if self.pipeline_request == "fused" and not self.pipeline.startswith("fused"):
             raise ValueError(f"fused pipeline unsupported for grid {self.indicator.grid.dims}")
         return self
 
@@ -272,7 +274,7 @@ class StokesSolver:
 
 def solve_stokes_device(indicator: IndicatorField, cfg: StokesConfig | None = None,
                         penalties: PenaltyParams | None = None, init=None, device=None,
-                        pipeline: str | None = None):
+                        pipeline: str | None = None, compact: bool | None = None):
     """Device-resident ``solve_stokes``: returns (DeviceAdmmState, ConvergenceReport)."""
     cfg = cfg or StokesConfig()
     penalties = penalties or PenaltyParams()
@@ -294,7 +296,7 @@ def solve_stokes_device(indicator: IndicatorField, cfg: StokesConfig | None = No
             state = DeviceAdmmState.from_host(init, dev)
     else:
         state = DeviceAdmmState.zeros(grid, dev)
-    solver = StokesSolver(indicator, cfg, penalties, state, dev, pipeline=pipeline)
+    solver = StokesSolver(indicator, cfg, penalties, state, dev, pipeline=pipeline, compact=compact)
     solver.begin()
     solver.iterate(cfg.max_iter, poll=True)
     solver.end()

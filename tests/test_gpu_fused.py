@@ -32,16 +32,17 @@ def _hist_close(mine, ref, rtol=1e-5):
     assert err.max() <= rtol, (err.max(), np.unravel_index(err.argmax(), err.shape))
 
 
+@pytest.mark.parametrize("compact", [True, False])
 @pytest.mark.parametrize("n,iters,geom", [(64, 30, "packing"), (64, 12, "sphere"), (128, 4, "packing")])
-def test_fused_truncated_vs_oracle(pf, n, iters, geom):
+def test_fused_truncated_vs_oracle(pf, n, iters, geom, compact):
     from oracle import poreflow_oracle as O
 
     ind = (pf.random_packing_geometry(n, seed=3) if geom == "packing"
            else pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25))
     g = (0.3, 1.0, -0.5)
     cfg = pf.StokesConfig.with_tolerance(1e-7, pressure_gradient=g, max_iter=iters)
-    st, rep = pf.solve_stokes_device(ind, cfg, pipeline="fused")
-    assert rep.meta["pipeline"] == "fused"
+    st, rep = pf.solve_stokes_device(ind, cfg, pipeline="fused", compact=compact)
+    assert rep.meta["pipeline"] == ("fused-compact" if compact else "fused")
     ost, ohist, _, oit, ofp = O.solve_stokes(ind.values, g, 1e-7, 1e-7, max_iter=iters)
     assert rep.iterations == oit == iters
     h = st.to_host()
@@ -58,7 +59,7 @@ def test_fused_matches_cufft_pipeline_full_solve(pf):
     cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(0.0, 0.0, 1.0))
     a, ra = pf.solve_stokes_device(ind, cfg, pen, pipeline="fused")
     b, rb = pf.solve_stokes_device(ind, cfg, pen, pipeline="cufft")
-    assert ra.meta["pipeline"] == "fused" and rb.meta["pipeline"] == "cufft"
+    assert ra.meta["pipeline"] == "fused-compact" and rb.meta["pipeline"] == "cufft"
     assert ra.converged and rb.converged and ra.iterations == rb.iterations
     for k in ("u", "u_tilde", "q", "a", "lam"):
         x, y = getattr(a, k).cpu().numpy(), getattr(b, k).cpu().numpy()
@@ -80,7 +81,7 @@ def test_fused_warm_start_and_gauge(pf):
     ost, ohist, _, oit, _ = O.solve_stokes(ind.values, g, 1e-6, 1e-6, max_iter=10,
                                            init=dict(u=init.u, u_tilde=init.u_tilde, q=init.q, a=init.a,
                                                      lam=init.lam))
-    assert rep.meta["pipeline"] == "fused" and rep.iterations == oit
+    assert rep.meta["pipeline"] == "fused" and rep.iterations == oit  # pore a != 0: full storage
     for k in ("u", "u_tilde", "q", "a", "lam"):
         assert rel_l2(getattr(st, k), ost[k]) <= FIELD_TOL, k
     assert abs(st.q.mean()) <= 1e-12 * np.abs(st.q).max()
@@ -106,7 +107,7 @@ def test_fused_cfg1_sphere64_matches_reference_golden(pf, golden):
         g = [0.0] * 3
         g[ax] = 1.0
         st, rep = pf.solve_stokes(ind, pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=tuple(g)), pen)
-        assert rep.meta["pipeline"] == "fused"
+        assert rep.meta["pipeline"] == "fused-compact"
         assert rep.iterations == int(z["iterations"][ax])
         ref_h = z["history"][ax][: rep.iterations]
         _hist_close(rep.history, ref_h)
@@ -127,6 +128,7 @@ def test_fused_pipelines_bitwise_deterministic(pf):
     cfg = pf.StokesConfig.with_tolerance(1e-6, pressure_gradient=(0.2, 1.0, 0.0), max_iter=25)
     a, ra = pf.solve_stokes_device(ind, cfg, pipeline="fused")
     b, rb = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    assert ra.meta["pipeline"] == "fused-compact"
     assert np.array_equal(ra.history, rb.history)
     for k in ("u", "u_tilde", "q", "a", "lam"):
         assert bool((getattr(a, k) == getattr(b, k)).all()), k
@@ -143,8 +145,29 @@ def test_fused_exact_symbols_vs_oracle(pf):
     ind = pf.make_model_geometry(pf.UnitCellGrid((64, 64, 64)), radius=0.3)
     cfg = pf.StokesConfig.with_tolerance(1e-7, pressure_gradient=(0.0, 0.0, 1.0), max_iter=10, symbol_mode="exact")
     st, rep = pf.solve_stokes(ind, cfg)
-    assert rep.meta["pipeline"] == "fused"
+    assert rep.meta["pipeline"] == "fused-compact"
     ost, ohist, _, oit, _ = O.solve_stokes(ind.values, (0.0, 0.0, 1.0), 1e-7, 1e-7, max_iter=10, mode="exact")
     for k in ("u", "u_tilde", "q", "a", "lam"):
         assert rel_l2(getattr(st, k), ost[k]) <= FIELD_TOL, k
     _hist_close(rep.history, ohist)
+
+
+def test_compact_warm_start_continues_exactly(pf):
+    """A state produced by the compact path (pore a == 0 exactly) warm-starts the
+    compact path again; the two halves equal one uninterrupted run."""
+    ind = pf.random_packing_geometry(64, seed=12)
+    g = (1.0, 0.0, 0.5)
+    full, rf = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-7, pressure_gradient=g, max_iter=20))
+    half, rh = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-7, pressure_gradient=g, max_iter=10))
+    assert float(half.a[:, torch_pore(ind, half.a)].abs().max()) == 0.0
+    rest, rr = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-7, pressure_gradient=g, max_iter=10),
+                                      pf.PenaltyParams(*rh.meta["final_penalties"]), init=half)
+    assert rr.meta["pipeline"] == "fused-compact"
+    for k in ("u", "u_tilde", "a", "lam"):
+        assert rel_l2(getattr(rest, k).cpu().numpy(), getattr(full, k).cpu().numpy()) <= 1e-12, k
+
+
+def torch_pore(ind, like):
+    import torch
+
+    return torch.from_numpy(ind.values == 0).to(like.device)

@@ -86,8 +86,9 @@ def main():
                      f"{d.get('warps_active_pct', 0):.1f} | {d.get('regs', 0):.0f} | {d.get('fp64_pipe_pct', 0):.1f} | "
                      f"{', '.join(d['top_stalls'])} |\n")
     traffic = {}
-    names = {"k_rs": "RS_rows_local", "k_pk": "PK_axis0_spectral", "k_maxis<256, 1>": "MI_axis1_inverse",
-             "k_maxis<256, 0>": "MF_axis1_forward"}
+    names = {"k_rs<": "RS_rows_local", "k_rs_compact<": "RS_rows_local", "k_pk<": "PK_axis0_spectral",
+             "k_maxis<256, 1>": "MI_axis1_inverse", "k_maxis<256, 0>": "MF_axis1_forward",
+             "k_tpk<": "PK_axis0_spectral", "k_trs<": "RS_rows_local"}
     for d in fl:
         for key, stage in names.items():
             if key in d["kernel"] and stage not in traffic:
