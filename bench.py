@@ -272,6 +272,7 @@ def run_ours(args):
         except Exception:
             traffic = None
     achieved = stages[dom]["GB_s"]
+    pipe_b = sum(v for v in sb.values() if v) / n_real
     iter_ms_profile = sum(float(stage_ms[k]) for k in range(6))
 
     # end-to-end through the public numpy API: host indicator in, host state out
@@ -314,7 +315,10 @@ def run_ours(args):
                      "peak_source": peak_src},
         "iteration_roofline": {"alg_bytes_per_voxel_iter": B_ALG_ITER,
                                "achieved_GB_s": B_ALG_ITER * value / world / 1e9,
-                               "frac": B_ALG_ITER * value / world / 1e9 / peak},
+                               "frac": B_ALG_ITER * value / world / 1e9 / peak,
+                               # bytes this pipeline actually has to move (solid-only storage moves fewer)
+                               "pipeline_bytes_per_voxel_iter": pipe_b,
+                               "pipeline_frac": pipe_b * value / world / 1e9 / peak},
         "stages": stages, "stage_profile_ms_per_iter": iter_ms_profile,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_iters,
                 "d2h_bytes_per_step": d2h / e2e_iters, "iterations": e2e_iters,

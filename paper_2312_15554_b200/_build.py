@@ -55,16 +55,21 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile every source and link the C-ABI library.  ``out``/``defines`` build a
+    tuning variant (extra -D flags) next to the product library, for A/B timing via
+    POREFLOW_B200_LIB; the product build uses neither."""
+    lib = Path(out) if out else LIB
+    if out is None and not force and not needs_build():
         return LIB
     cc = nvcc()
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = PKG / "build" if out is None else PKG / "build" / ("v_" + lib.stem)
+    objdir.mkdir(parents=True, exist_ok=True)
+    extra = [f"-D{d}" for d in defines]
 
     def compile_one(src: Path):
         obj = objdir / (src.stem + ".o")
-        cmd = [cc, "-c", str(src), "-o", str(obj)] + _flags(src.name)
+        cmd = [cc, "-c", str(src), "-o", str(obj)] + _flags(src.name) + extra
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
@@ -73,18 +78,25 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
         "-L/usr/local/cuda/lib64", "-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
     ]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB} ({LIB.stat().st_size / 1e6:.1f} MB)", file=sys.stderr)
-    return LIB
+        print(f"built {lib} ({lib.stat().st_size / 1e6:.1f} MB)", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python _build.py [--force] [--variant NAME -DX=1 -DY=2 ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        defs = [a[2:] for a in args if a.startswith("-D")]
+        build(verbose=True, out=PKG / "build" / f"lib_{name}.so", defines=defs)
+    else:
+        build(force="--force" in args, verbose=True)

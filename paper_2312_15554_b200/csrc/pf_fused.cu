@@ -33,6 +33,12 @@
 #ifndef PF_PK_PREFETCH
 #define PF_PK_PREFETCH 1
 #endif
+#ifndef PF_PK_TWG
+#define PF_PK_TWG 0  // 1: k_pk reads twiddles from global (L1) instead of staging them in smem
+#endif
+#ifndef PF_PK_MINB
+#define PF_PK_MINB 3  // __launch_bounds__ min blocks per SM for k_pk (1 lets ptxas take 216 regs: 2 blocks/SM, slower)
+#endif
 #ifndef PF_PK_THREADS
 #define PF_PK_THREADS 128
 #endif
@@ -713,7 +719,8 @@ struct PK2 {
   using C = Cfg<N>;
   static constexpr int T = PF_PK_THREADS;
   static constexpr int NGP = T / C::G;
-  static constexpr int CP = NGP / 2;  // 3 components x CP columns over NGP groups
+  // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
+  static constexpr int CP = (NGP % 3 == 0) ? NGP / 3 : NGP / 2;
   static constexpr int NSEQ = 3 * CP;
   static constexpr int NCH = C::H / CP;
   static constexpr int TILES = N * NCH + N / CP;
@@ -721,18 +728,23 @@ struct PK2 {
   // sequence stride with an 8-bank shift: the (q fastest, 4 columns) staging
   // pattern of 8-lane phases is then conflict-free
   static constexpr int SS = C::SS + 1;
-  static constexpr size_t BYTES = sizeof(double2) * (N + NSEQ * SS);
+  static constexpr size_t BYTES = sizeof(double2) * ((PF_PK_TWG ? 0 : N) + NSEQ * SS);
 };
 
 template <int N>
-__global__ void __launch_bounds__(PK2<N>::T) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = PK2<N>;
   constexpr int H = C::H, SS = K::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
+#if PF_PK_TWG
+  const double2* tw = B.tw;
+  double2* S = smem;
+#else
   double2* tw = smem;
   double2* S = smem + N;
+#endif
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const double beta = ctrl->beta, b = ctrl->b;
   const int tile = blockIdx.x;
@@ -760,7 +772,9 @@ __global__ void __launch_bounds__(PK2<N>::T) k_pk(Bufs B, SpecArgs P, const Ctrl
     }
   }
 #endif
+#if !PF_PK_TWG
   for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+#endif
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 #pragma unroll

@@ -9,6 +9,7 @@ instances" contract (tests/test_backends.py:131-149).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -141,8 +142,8 @@ def solid_on_device(indicator, device):
     return cache[key]
 
 
-_STAGE_BYTES = 32 << 20
-_STAGES = 4
+_STAGE_BYTES = 16 << 20
+_STAGES = max(4, min(8, os.cpu_count() or 4))
 _stage = threading.local()
 
 
@@ -158,37 +159,77 @@ def _stage_buffers():
     return _stage.bufs, _stage.events, _stage.pool
 
 
-def to_host(x) -> np.ndarray:
-    """CUDA tensor -> new numpy array.  Device-to-host DMA into a ring of pinned
-    staging buffers (~55 GB/s) overlapped with parallel host copies out of them
-    (numpy releases the GIL), several times faster than a pageable ``.cpu()`` for
-    multi-GB solver states."""
+_NP = None
+
+
+def _np_dtype(dt):
+    global _NP
+    if _NP is None:
+        t = torch()
+        _NP = {t.float64: np.float64, t.uint8: np.uint8, t.complex128: np.complex128, t.float32: np.float32}
+    return _NP[dt]
+
+
+# Results up to this many bytes per call come back in pinned host memory: one direct
+# DMA per field at full PCIe rate, with the blocks recycled by torch's caching host
+# allocator once the caller drops the arrays.  Larger states (or 0 here) use the
+# staged ring below, whose output is ordinary pageable memory.
+_PINNED_OUT_BYTES = int(float(os.environ.get("POREFLOW_B200_PINNED_OUT_GB", "8")) * (1 << 30))
+
+
+def to_host_many(xs) -> list:
+    """CUDA tensors -> new numpy arrays.
+
+    Small results (see ``_PINNED_OUT_BYTES``): arrays backed by pinned host memory,
+    filled by direct device-to-host copies.  Otherwise ONE pipeline: device-to-host DMA
+    into a ring of pinned staging buffers (~55 GB/s) overlapped with parallel host
+    copies out of them (numpy releases the GIL).  The host side is bound by
+    first-touch page faults of the fresh output arrays (~4 GB/s per thread), so
+    the ring is as wide as the host has threads and runs across all fields
+    instead of draining per field."""
     t = torch()
-    x = x.contiguous()
-    out = np.empty(tuple(x.shape), dtype={t.float64: np.float64, t.uint8: np.uint8,
-                                          t.complex128: np.complex128}[x.dtype])
-    nbytes = out.nbytes
-    if nbytes <= (4 << 20):
-        return x.cpu().numpy().copy()
-    src = x.view(-1).view(t.uint8)
-    dst = out.reshape(-1).view(np.uint8)
+    xs = [x.contiguous() for x in xs]
+    total = sum(x.numel() * x.element_size() for x in xs)
+    if total <= _PINNED_OUT_BYTES:
+        hs = [t.empty(tuple(x.shape), dtype=x.dtype, pin_memory=True) for x in xs]
+        for h, x in zip(hs, xs):
+            h.copy_(x, non_blocking=True)
+        if xs:
+            t.cuda.current_stream(xs[0].device).synchronize()
+        return [h.numpy() for h in hs]
+    outs = [np.empty(tuple(x.shape), dtype=_np_dtype(x.dtype)) for x in xs]
+    big = [i for i, o in enumerate(outs) if o.nbytes > (4 << 20)]
+    for i, o in enumerate(outs):
+        if i not in big:
+            o[...] = xs[i].cpu().numpy()
+    if not big:
+        return outs
     bufs, evs, pool = _stage_buffers()
-    stream = t.cuda.current_stream(x.device)
-    chunks = [(o, min(_STAGE_BYTES, nbytes - o)) for o in range(0, nbytes, _STAGE_BYTES)]
+    chunks = []
+    for i in big:
+        nb = outs[i].nbytes
+        chunks += [(i, o, min(_STAGE_BYTES, nb - o)) for o in range(0, nb, _STAGE_BYTES)]
+    srcs = {i: xs[i].view(-1).view(t.uint8) for i in big}
+    dsts = {i: outs[i].reshape(-1).view(np.uint8) for i in big}
     pending = [None] * _STAGES
 
-    def host_copy(j, o, k):
+    def host_copy(j, i, o, k):
         evs[j].synchronize()
-        np.copyto(dst[o:o + k], bufs[j][:k].numpy())
+        np.copyto(dsts[i][o:o + k], bufs[j][:k].numpy())
 
-    for i, (o, k) in enumerate(chunks):
-        j = i % _STAGES
+    for n, (i, o, k) in enumerate(chunks):
+        j = n % _STAGES
         if pending[j] is not None:
             pending[j].result()  # staging buffer j is free again
-        bufs[j][:k].copy_(src[o:o + k], non_blocking=True)
-        evs[j].record(stream)
-        pending[j] = pool.submit(host_copy, j, o, k)
+        bufs[j][:k].copy_(srcs[i][o:o + k], non_blocking=True)
+        evs[j].record(t.cuda.current_stream(xs[i].device))
+        pending[j] = pool.submit(host_copy, j, i, o, k)
     for f in pending:
         if f is not None:
             f.result()
-    return out
+    return outs
+
+
+def to_host(x) -> np.ndarray:
+    """CUDA tensor -> new numpy array (see ``to_host_many``)."""
+    return to_host_many([x])[0]

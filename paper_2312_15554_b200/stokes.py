@@ -17,7 +17,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native as N
-from .device import get_plan, require_cuda, solid_on_device, to_device, to_host, torch
+from .device import get_plan, require_cuda, solid_on_device, to_device, to_host_many, torch
 from .grid import IndicatorField
 from .report import ConvergenceReport
 from .spectral import CENTRAL, SYMBOL_MODES
@@ -160,8 +160,8 @@ class DeviceAdmmState:
         return cls(f(st.u), f(st.u_tilde), f(st.q), f(st.a), f(st.lam), st.iterations)
 
     def to_host(self) -> AdmmState:
-        g = lambda x: to_host(x.detach())  # noqa: E731
-        return AdmmState(g(self.u), g(self.u_tilde), g(self.q), g(self.a), g(self.lam), self.iterations)
+        u, ut, q, a, lam = to_host_many([x.detach() for x in (self.u, self.u_tilde, self.q, self.a, self.lam)])
+        return AdmmState(u, ut, q, a, lam, self.iterations)
 
 
 def _params(cfg: StokesConfig, pen: PenaltyParams, max_iter: int) -> N.StokesParams:

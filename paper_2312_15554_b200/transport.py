@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .device import get_plan, require_cuda, solid_on_device, to_device, to_host, torch
+from .device import get_plan, require_cuda, solid_on_device, to_device, to_host_many, torch
 from .grid import IndicatorField
 from .report import ConvergenceReport
 from .spectral import CENTRAL, SYMBOL_MODES
@@ -82,7 +82,8 @@ class DeviceTransportState:
     iterations: int = 0
 
     def to_host(self) -> TransportState:
-        return TransportState(to_host(self.chi), to_host(self.grad_chi), self.iterations)
+        chi, gch = to_host_many([self.chi, self.grad_chi])
+        return TransportState(chi, gch, self.iterations)
 
 
 @dataclass(frozen=True)
