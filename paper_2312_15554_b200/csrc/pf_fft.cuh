@@ -4,7 +4,13 @@
 // TMA bulk-copy / LDGSTS helpers.
 #pragma once
 
+#include <cmath>
+
 #include "pf_internal.cuh"
+
+#ifndef PF_TW_FACTORED
+#define PF_TW_FACTORED 1  // 1: pass-1 twiddles from 6 table loads (see fft_seq)
+#endif
 
 namespace pf {
 namespace fz {
@@ -152,6 +158,20 @@ struct Dft<16, INV> {
   static __device__ __forceinline__ void run(double2* x) { dft_pq<4, 4, INV>(x); }
 };
 
+// Pass-1 twiddle table, laid out [k1][l] (A x B = N entries): entry k1*B + l =
+// exp(-2 pi i l k1 / N).  Lane l's loads for fixed k1 are then consecutive, so a
+// quarter-warp never hits the same bank twice (the natural tw[l*k1] layout is
+// 2..8-way conflicted for even k1).
+template <int N>
+inline void pass1_twiddles(double2* out) {
+  using C = Cfg<N>;
+  for (int k1 = 0; k1 < C::A; ++k1)
+    for (int l = 0; l < C::B; ++l) {
+      const double a = 2.0 * M_PI * (double)(l * k1) / (double)N;
+      out[k1 * C::B + l] = make_double2(std::cos(a), -std::sin(a));
+    }
+}
+
 // One N-point complex FFT (unnormalised) of the padded smem sequence s by the
 // G lanes of a group (lane l).  Pass 1: B sub-FFTs of size A over stride-B
 // elements + twiddles; pass 2: A sub-FFTs of size B.  Output in natural order.
@@ -167,12 +187,29 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
 #pragma unroll
     for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
     Dft<A, INV>::run(x);
+#if PF_TW_FACTORED
+    // w^(4a+b) = w^(4a) * w^b from 3 + A/4-1 table loads instead of A-1 (shared
+    // memory bandwidth is the scarce resource of these kernels); <= 2 ulp.
+    double2 wb[4], wa[A / 4];
+#pragma unroll
+    for (int b = 1; b < 4; ++b) wb[b] = tw[b * B + l];
+#pragma unroll
+    for (int a = 1; a < A / 4; ++a) wa[a] = tw[4 * a * B + l];
 #pragma unroll
     for (int k1 = 1; k1 < A; ++k1) {
-      double2 w = tw[l * k1];
+      const int a = k1 / 4, b = k1 % 4;
+      double2 w = (a == 0) ? wb[b] : (b == 0 ? wa[a] : cmul(wa[a], wb[b]));
       if (INV) w.y = -w.y;
       x[k1] = cmul(x[k1], w);
     }
+#else
+#pragma unroll
+    for (int k1 = 1; k1 < A; ++k1) {
+      double2 w = tw[k1 * B + l];
+      if (INV) w.y = -w.y;
+      x[k1] = cmul(x[k1], w);
+    }
+#endif
   }
   __syncwarp();
   if (p1) {

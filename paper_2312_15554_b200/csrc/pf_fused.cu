@@ -33,6 +33,9 @@
 #ifndef PF_PK_PREFETCH
 #define PF_PK_PREFETCH 1
 #endif
+#ifndef PF_RS_WARP
+#define PF_RS_WARP 0  // 1: compact RS runs warp-per-tile (k_rsw_compact)
+#endif
 #ifndef PF_PK_TWG
 #define PF_PK_TWG 0  // 1: k_pk reads twiddles from global (L1) instead of staging them in smem
 #endif
@@ -165,33 +168,41 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     __syncthreads();
     fft_seq<N, true>(SI + (g < NP ? g : 0) * SS, tw, l, g < NP);
     __syncthreads();
-    // (2) local projection + multipliers (pure.py:59-68) and six squared norms
-#pragma unroll 4
-    for (int j = 0; j < K::VPT; ++j) {
-      const int v = t + T * j, row = v / N, col = v % N;
-      double* zv = reinterpret_cast<double*>(SI + (row >> 1) * SS + C::pad(col)) + (row & 1);
-      const double u1 = *zv;
-      const double h = sh[v] ? 1.0 : 0.0;
-      const double u0 = sst[v], t0 = sst[V + v], a0 = sst[2 * V + v], l0 = sst[3 * V + v];
-      // (a + b u - H lam) / (b + alpha H): the divisor takes two values, so divide by
-      // multiplying with the hoisted reciprocals (<= 1 ulp from the quotient)
-      const double t1 = ((a0 + b * u1) - h * l0) * (h != 0.0 ? inv_bs : inv_bp);
-      const double a1 = a0 + b * (u1 - t1);
-      const double l1 = l0 + alpha * (h * t1);
-      const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
-      acc[0] += s0 * s0;
-      acc[1] += s1 * s1;
-      acc[2] += l1 * l1;
-      acc[3] += s3 * s3;
-      acc[4] += s4 * s4;
-      acc[5] += a1 * a1;
-      const int64_t i = c * n + row0 * N + v;
-      st.u[i] = u1;
-      st.ut[i] = t1;
-      st.a[i] = a1;
-      st.lam[i] = l1;
-      // R = b u~' - a' with the pre-adaptation b (stokes.py:405-407); rows 2p, 2p+1 -> Re, Im
-      *zv = b * t1 - a1;
+    // (2) local projection + multipliers (pure.py:59-68) and six squared norms; a
+    // lane takes both rows of a pair at one column (one 16-byte sequence access)
+#pragma unroll 2
+    for (int j = 0; j < K::VPT / 2; ++j) {
+      const int w = t + T * j, p = w / N, col = w % N;
+      double2* zp = SI + p * SS + C::pad(col);
+      const double2 z = *zp;
+      double rr[2];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int v = (2 * p + hh) * N + col;
+        const double u1 = hh ? z.y : z.x;
+        const double h = sh[v] ? 1.0 : 0.0;
+        const double u0 = sst[v], t0 = sst[V + v], a0 = sst[2 * V + v], l0 = sst[3 * V + v];
+        // (a + b u - H lam) / (b + alpha H): the divisor takes two values, so divide by
+        // multiplying with the hoisted reciprocals (<= 1 ulp from the quotient)
+        const double t1 = ((a0 + b * u1) - h * l0) * (h != 0.0 ? inv_bs : inv_bp);
+        const double a1 = a0 + b * (u1 - t1);
+        const double l1 = l0 + alpha * (h * t1);
+        const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
+        acc[0] += s0 * s0;
+        acc[1] += s1 * s1;
+        acc[2] += l1 * l1;
+        acc[3] += s3 * s3;
+        acc[4] += s4 * s4;
+        acc[5] += a1 * a1;
+        const int64_t i = c * n + row0 * N + v;
+        st.u[i] = u1;
+        st.ut[i] = t1;
+        st.a[i] = a1;
+        st.lam[i] = l1;
+        // R = b u~' - a' with the pre-adaptation b (stokes.py:405-407); rows 2p, 2p+1 -> Re, Im
+        rr[hh] = b * t1 - a1;
+      }
+      *zp = make_double2(rr[0], rr[1]);
     }
     __syncthreads();
     // staged inputs consumed: prefetch the next tile while this one finishes
@@ -419,37 +430,46 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Comp
     __syncthreads();
     fft_seq<N, true>(SI + (g < NP ? g : 0) * SS, tw, l, g < NP);
     __syncthreads();
-    // (2) local step; pore: u~' = u', a' = 0, lam' = lam (only u' is stored)
+    // (2) local step; pore: u~' = u', a' = 0, lam' = lam (only u' is stored).
+    // A lane takes both rows of a pair at one column: one 16-byte access of the
+    // sequence element (rows 2p, 2p+1 = Re, Im) instead of two strided 8-byte ones.
     const int64_t cbase = (int64_t)c * cp.ns + o0;
-#pragma unroll 4
-    for (int j = 0; j < K::VPT; ++j) {
-      const int v = t + T * j, row = v / N, col = v % N;
-      double* zv = reinterpret_cast<double*>(SI + (row >> 1) * SS + C::pad(col)) + (row & 1);
-      const double u1 = *zv;
-      const bool solid = sh[v] != 0;
-      const unsigned mask = __ballot_sync(0xffffffffu, solid);
-      const double s4 = u1 - su[v];
-      acc[4] += s4 * s4;
-      double t1 = u1, a1 = 0.0;
-      const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
-      if (solid) {
-        const int ci = segb + __popc(mask & ((1u << lane) - 1u));
-        const double t0 = sc[ci], a0 = sc[CS + ci], l0 = sc[2 * CS + ci];
-        t1 = ((a0 + b * u1) - l0) * inv_bs;  // pure.py:61 with H = 1
-        a1 = a0 + b * (u1 - t1);             // pure.py:66
-        const double l1 = l0 + alpha * t1;   // pure.py:67
-        const double s1 = t1 - t0, s3 = u1 - t1;
-        acc[0] += t1 * t1;
-        acc[1] += s1 * s1;
-        acc[2] += l1 * l1;
-        acc[3] += s3 * s3;
-        acc[5] += a1 * a1;
-        cp.ut[cbase + ci] = t1;
-        cp.a[cbase + ci] = a1;
-        cp.lam[cbase + ci] = l1;
+#pragma unroll 2
+    for (int j = 0; j < K::VPT / 2; ++j) {
+      const int w = t + T * j, p = w / N, col = w % N;
+      double2* zp = SI + p * SS + C::pad(col);
+      const double2 z = *zp;
+      double rr[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = (2 * p + h) * N + col;
+        const double u1 = h ? z.y : z.x;
+        const bool solid = sh[v] != 0;
+        const unsigned mask = __ballot_sync(0xffffffffu, solid);
+        const double s4 = u1 - su[v];
+        acc[4] += s4 * s4;
+        double t1 = u1, a1 = 0.0;
+        const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
+        if (solid) {
+          const int ci = segb + __popc(mask & ((1u << lane) - 1u));
+          const double t0 = sc[ci], a0 = sc[CS + ci], l0 = sc[2 * CS + ci];
+          t1 = ((a0 + b * u1) - l0) * inv_bs;  // pure.py:61 with H = 1
+          a1 = a0 + b * (u1 - t1);             // pure.py:66
+          const double l1 = l0 + alpha * t1;   // pure.py:67
+          const double s1 = t1 - t0, s3 = u1 - t1;
+          acc[0] += t1 * t1;
+          acc[1] += s1 * s1;
+          acc[2] += l1 * l1;
+          acc[3] += s3 * s3;
+          acc[5] += a1 * a1;
+          cp.ut[cbase + ci] = t1;
+          cp.a[cbase + ci] = a1;
+          cp.lam[cbase + ci] = l1;
+        }
+        st.u[c * n + row0 * N + v] = u1;
+        rr[h] = b * t1 - a1;
       }
-      st.u[c * n + row0 * N + v] = u1;
-      *zv = b * t1 - a1;
+      *zp = make_double2(rr[0], rr[1]);
     }
     __syncthreads();
     if (t == 0 && has_next)
@@ -471,6 +491,121 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Comp
   }
   block_sum<6>(acc);
   if (t == 0)
+    for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// ------------------------------------------------------------------ warp-per-tile compact RS
+// One warp per tile of R = 2 * (32 / G) rows: the paired-row sequences occupy
+// every lane during both FFTs, and with no staging (X, u, H and the compact
+// multipliers load straight from global into the sequence buffer / registers)
+// a block needs only the twiddles and its sequences in shared memory, so many
+// single-warp blocks fit per SM and their memory phases overlap one another's FFTs.
+template <int N>
+struct RSW {
+  using C = Cfg<N>;
+  static constexpr int NP = 32 / C::G;  // paired-row sequences per warp
+  static constexpr int R = 2 * NP;      // rows per tile
+  static constexpr int V = R * N;       // voxels per tile
+  static constexpr int VPT = V / 32;    // voxels per lane (= 32-voxel segments per tile)
+  static constexpr size_t BYTES = sizeof(double2) * (N + NP * C::SS);
+};
+
+template <int N>
+__global__ void __launch_bounds__(32) k_rsw_compact(Bufs B, State st, Compact cp, const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = RSW<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, NP = K::NP, VPT = K::VPT;
+  constexpr int SPR = N / 32;
+  constexpr int TPC = N * N / R;
+  constexpr int NT = 3 * TPC;
+  static_assert(VPT <= 32 && 32 % SPR == 0, "one segment base per lane");
+  if (ctrl->done) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  double2* tw = (double2*)sraw;
+  double2* S = tw + N;
+  const int lane = threadIdx.x, g = lane / C::G, l = lane % C::G;
+  for (int j = lane; j < N; j += 32) tw[j] = B.tw[j];
+  const double alpha = ctrl->alpha, b = ctrl->b;
+  const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
+  const int64_t n = (int64_t)N * N * N;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const double2* XU = B.XU + ((size_t)c * N * N + row0) * H;
+    const double2* XUn = B.XUn + (size_t)c * N * N + row0;
+    const uint8_t* Ht = st.H + row0 * N;
+    const uint32_t o0 = __ldg(cp.off + row0);
+    const int sl = lane % VPT;  // this lane's segment (lanes >= VPT duplicate, unused)
+    const int sb = seg_base<N>(Ht + sl * 32, __ldg(cp.off + row0 + sl / SPR) - o0, lane);
+    __syncwarp();  // previous tile's readers of S are done
+    // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
+#pragma unroll
+    for (int it = 0; it < NP * H / 32; ++it) {
+      const int idx = lane + 32 * it, p = idx / H, k = idx % H;
+      double2 xa = __ldg(XU + (2 * p) * H + k), xb = __ldg(XU + (2 * p + 1) * H + k);
+      if (k == 0) xa.y = xb.y = 0.0;
+      double2* sp = S + p * SS;
+      sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+      if (k > 0) sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+    }
+    if (lane < NP) S[lane * SS + C::pad(H)] = make_double2(__ldg(&XUn[2 * lane].x), __ldg(&XUn[2 * lane + 1].x));
+    __syncwarp();
+    fft_seq<N, true>(S + g * SS, tw, l, true);
+    __syncwarp();
+    // (2) local step; pore: u~' = u', a' = 0, lam' = lam (only u' is stored)
+    const int64_t ubase = (int64_t)c * n + row0 * N;
+    const int64_t cbase = (int64_t)c * cp.ns + o0;
+#pragma unroll 4
+    for (int j = 0; j < VPT; ++j) {
+      const int v = lane + 32 * j, row = v / N, col = v % N;
+      double* zv = reinterpret_cast<double*>(S + (row >> 1) * SS + C::pad(col)) + (row & 1);
+      const double u1 = *zv;
+      const bool solid = Ht[v] != 0;
+      const unsigned mask = __ballot_sync(0xffffffffu, solid);
+      const int segb = __shfl_sync(0xffffffffu, sb, j);
+      const double s4 = u1 - __ldg(st.u + ubase + v);
+      acc[4] += s4 * s4;
+      double t1 = u1, a1 = 0.0;
+      if (solid) {
+        const int64_t ci = cbase + segb + __popc(mask & ((1u << lane) - 1u));
+        const double t0 = cp.ut[ci], a0 = cp.a[ci], l0 = cp.lam[ci];
+        t1 = ((a0 + b * u1) - l0) * inv_bs;  // pure.py:61 with H = 1
+        a1 = a0 + b * (u1 - t1);             // pure.py:66
+        const double l1 = l0 + alpha * t1;   // pure.py:67
+        const double s1 = t1 - t0, s3 = u1 - t1;
+        acc[0] += t1 * t1;
+        acc[1] += s1 * s1;
+        acc[2] += l1 * l1;
+        acc[3] += s3 * s3;
+        acc[5] += a1 * a1;
+        cp.ut[ci] = t1;
+        cp.a[ci] = a1;
+        cp.lam[ci] = l1;
+      }
+      st.u[ubase + v] = u1;
+      *zv = b * t1 - a1;
+    }
+    __syncwarp();
+    fft_seq<N, false>(S + g * SS, tw, l, true);
+    __syncwarp();
+    double2* XR = B.XR + ((size_t)c * N * N + row0) * H;
+    double2* XRn = B.XRn + (size_t)c * N * N + row0;
+#pragma unroll
+    for (int it = 0; it < NP * H / 32; ++it) {
+      const int idx = lane + 32 * it, p = idx / H, k = idx % H;
+      const double2 zk = S[p * SS + C::pad(k)], zm = S[p * SS + C::pad((N - k) & (N - 1))];
+      XR[(2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XR[(2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+    if (lane < NP) {
+      const double2 z = S[lane * SS + C::pad(H)];
+      XRn[2 * lane] = make_double2(z.x, 0.0);
+      XRn[2 * lane + 1] = make_double2(z.y, 0.0);
+    }
+  }
+  block_sum<6>(acc);
+  if (lane == 0)
     for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
 }
 
@@ -942,7 +1077,7 @@ template <int N>
 static size_t smem_rsfix() { return fz::RS2<N>::TW + fz::RS2<N>::INV + fz::RS2<N>::ST / 4; }
 template <int N>
 static size_t smem_rsc() { return fz::RSC<N>::BYTES; }
-constexpr int kRsMaxBlocks = kSMs * 8;  // partial-sum rows reserved for the persistent RS grid
+constexpr int kRsMaxBlocks = kSMs * 32;  // partial-sum rows reserved for the persistent RS grid
 template <int N>
 static size_t smem_pk() { return fz::PK2<N>::BYTES; }
 
@@ -953,6 +1088,8 @@ static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem_rsfix<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsw_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)fz::RSW<N>::BYTES));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
@@ -965,6 +1102,11 @@ static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N>, fz::RS2<N>::T, smem_rsc<N>()));
   f->nb_full = wave(o1, 3);
   f->nb_compact = wave(o2, kRsMaxBlocks / kSMs);
+#if PF_RS_WARP
+  int o3 = 0;
+  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, fz::k_rsw_compact<N>, 32, fz::RSW<N>::BYTES));
+  f->nb_compact = wave(o3, kRsMaxBlocks / kSMs);
+#endif
   f->nb_rs = f->nb_full;
   return PF_OK;
 }
@@ -1001,9 +1143,10 @@ int fused_ensure(pf_plan* p) {
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
   std::vector<double2> tw(N);
-  for (int j = 0; j < N; ++j) {
-    const double a = 2.0 * M_PI * (double)j / (double)N;
-    tw[j] = make_double2(std::cos(a), -std::sin(a));
+  switch (N) {
+    case 64: fz::pass1_twiddles<64>(tw.data()); break;
+    case 128: fz::pass1_twiddles<128>(tw.data()); break;
+    default: fz::pass1_twiddles<256>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
@@ -1182,7 +1325,11 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
   if (f->compact) {
+#if PF_RS_WARP
+    fz::k_rsw_compact<N><<<f->nb_rs, 32, fz::RSW<N>::BYTES, p->work>>>(f->b, st, compact_of(f), p->ctrl);
+#else
     fz::k_rs_compact<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsc<N>(), p->work>>>(f->b, st, compact_of(f), p->ctrl);
+#endif
   } else {
     fz::k_rs<N><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
   }

@@ -493,9 +493,10 @@ static int tfused_ensure(pf_plan* p) {
   f->b.tw = take(N);
   f->b.part = (double*)m;
   std::vector<double2> tw(N);
-  for (int j = 0; j < N; ++j) {
-    const double a = 2.0 * M_PI * (double)j / (double)N;
-    tw[j] = make_double2(std::cos(a), -std::sin(a));
+  switch (N) {
+    case 64: fz::pass1_twiddles<64>(tw.data()); break;
+    case 128: fz::pass1_twiddles<128>(tw.data()); break;
+    default: fz::pass1_twiddles<256>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
   size_t ws = 0;
