@@ -36,6 +36,9 @@
 #ifndef PF_RS_WARP
 #define PF_RS_WARP 0  // 1: compact RS runs warp-per-tile (k_rsw_compact)
 #endif
+#ifndef PF_M_MINB
+#define PF_M_MINB 5  // min blocks per SM for the axis-1 passes: 96 regs, 5 blocks (smem-limited too)
+#endif
 #ifndef PF_PK_TWG
 #define PF_PK_TWG 0  // 1: k_pk reads twiddles from global (L1) instead of staging them in smem
 #endif
@@ -783,7 +786,7 @@ struct M2 {
 };
 
 template <int N, bool INV>
-__global__ void __launch_bounds__(128) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = M2<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;

@@ -30,6 +30,10 @@
 
 #include "pf_fft.cuh"
 
+#ifndef PF_T_MINB
+#define PF_T_MINB 5  // min blocks per SM for the transport spectral / axis-1 passes (smem allows 5)
+#endif
+
 namespace pf {
 namespace ft {
 
@@ -69,7 +73,7 @@ struct TPK {
 };
 
 template <int N>
-__global__ void __launch_bounds__(128) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, PF_T_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = TPK<N>;
   constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
@@ -167,7 +171,7 @@ struct TM {
 // INV (MI_T): outputs oc = 0 X(chi) <- Y0; 1 X(d0 chi) <- Y1; 2 X(d1 chi) <- i k1 Y0.
 // FWD (MF_T): outputs oc = 0 Y_b <- FFT(X0) + i k1 FFT(X2); 1 Y_w0 <- FFT(X1).
 template <int N, bool INV>
-__global__ void __launch_bounds__(128) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, PF_T_MINB) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = TM<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
