@@ -249,7 +249,11 @@ struct TRS {
   static constexpr size_t XN = sizeof(double2) * 3 * R;
   static constexpr size_t UB = sizeof(double) * 3 * V;
   static constexpr size_t HB = V;
-  static constexpr size_t BYTES = TW + SI + SF + XM + XN + UB + HB;
+  // the forward sequences overwrite the inverse ones (the local step reads its
+  // gradients into registers first), so one buffer of max(SI, SF) bytes
+  static constexpr size_t SQ = SI > SF ? SI : SF;
+  static constexpr size_t BYTES = TW + SQ + XM + XN + UB + HB;
+  static constexpr int MINB = T <= 64 ? 4 : 3;  // register cap that keeps the smem-allowed blocks
   static constexpr uint32_t TX = (uint32_t)(XM + XN + UB + HB);
 };
 
@@ -272,7 +276,7 @@ __device__ __forceinline__ void trs_issue(int tile, const TBufs& B, const double
 }
 
 template <int N>
-__global__ void __launch_bounds__(TRS<N>::T) k_trs(TBufs B, TP P, const double* __restrict__ u,
+__global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, const double* __restrict__ u,
                                                    const uint8_t* __restrict__ Hs, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = TRS<N>;
@@ -283,11 +287,11 @@ __global__ void __launch_bounds__(TRS<N>::T) k_trs(TBufs B, TP P, const double* 
   __shared__ uint64_t mbar;
   double2* tw = (double2*)sraw;
   double2* SIq = (double2*)(sraw + K::TW);
-  double2* SFq = (double2*)(sraw + K::TW + K::SI);
-  double2* sx = (double2*)(sraw + K::TW + K::SI + K::SF);
-  double2* sxn = (double2*)(sraw + K::TW + K::SI + K::SF + K::XM);
-  double* su = (double*)(sraw + K::TW + K::SI + K::SF + K::XM + K::XN);
-  uint8_t* sh = (uint8_t*)(sraw + K::TW + K::SI + K::SF + K::XM + K::XN + K::UB);
+  double2* SFq = SIq;  // aliased (see TRS::BYTES)
+  double2* sx = (double2*)(sraw + K::TW + K::SQ);
+  double2* sxn = (double2*)(sraw + K::TW + K::SQ + K::XM);
+  double* su = (double*)(sraw + K::TW + K::SQ + K::XM + K::XN);
+  uint8_t* sh = (uint8_t*)(sraw + K::TW + K::SQ + K::XM + K::XN + K::UB);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   for (int j = t; j < N; j += T) tw[j] = B.tw[j];
   const double* kap2 = P.kap[2];
@@ -325,12 +329,22 @@ __global__ void __launch_bounds__(TRS<N>::T) k_trs(TBufs B, TP P, const double* 
     __syncthreads();
     fft_seq<N, true>(SIq + (g < K::NSI ? g : 0) * SS, tw, l, g < K::NSI);
     __syncthreads();
-    // (2) polarization (pure.py:71-87) with A, B, F from H and u (transport.py:112-121)
+    // (2) polarization (pure.py:71-87) with A, B, F from H and u (transport.py:112-121);
+    // gradients to registers first: the forward sequences overwrite the inverse ones
+    double gv[K::VPT][3];
+#pragma unroll
     for (int j = 0; j < K::VPT; ++j) {
       const int v = t + T * j, row = v / N, col = v % N;
       const double2 z01 = SIq[row * SS + C::pad(col)];
-      const double2 z2 = SIq[(R + (row >> 1)) * SS + C::pad(col)];
-      const double gr[3] = {z01.x, z01.y, (row & 1) ? z2.y : z2.x};
+      gv[j][0] = z01.x;
+      gv[j][1] = z01.y;
+      gv[j][2] = reinterpret_cast<const double*>(SIq + (R + (row >> 1)) * SS + C::pad(col))[row & 1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < K::VPT; ++j) {
+      const int v = t + T * j, row = v / N, col = v % N;
+      const double* gr = gv[j];
       const double h = (double)sh[v];
       const double pore = 1.0 - h;
       const double contrast = (pore + eta * h) - a0;
@@ -458,18 +472,20 @@ struct FusedTPlan {
   void* mem = nullptr;
   double2* g0mem = nullptr;
   cufftHandle plan2d = 0;
+  int nb_trs = kSMs;  // persistent RS grid: one wave of resident blocks (occupancy API)
 };
-
-constexpr int kTrsBlocks = kSMs * 3;
 
 static FusedTPlan* ftp(pf_plan* p) { return reinterpret_cast<FusedTPlan*>(p->tfused); }
 
 template <int N>
-static int tset_attrs() {
+static int tset_attrs(FusedTPlan* f) {
   PF_CK_CUDA(cudaFuncSetAttribute(ft::k_tpk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TPK<N>::BYTES));
   PF_CK_CUDA(cudaFuncSetAttribute(ft::k_taxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TM<N>::BYTES));
   PF_CK_CUDA(cudaFuncSetAttribute(ft::k_taxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TM<N>::BYTES));
   PF_CK_CUDA(cudaFuncSetAttribute(ft::k_trs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TRS<N>::BYTES));
+  int o = 0;
+  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ft::k_trs<N>, ft::TRS<N>::T, ft::TRS<N>::BYTES));
+  f->nb_trs = (o < 1 ? 1 : o) * kSMs;
   return PF_OK;
 }
 
@@ -519,9 +535,9 @@ static int tfused_ensure(pf_plan* p) {
   PF_CK_FFT(cufftSetWorkArea(f->plan2d, p->fft_work));
   PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
   switch (N) {
-    case 64: PF_CK(tset_attrs<64>()); break;
-    case 128: PF_CK(tset_attrs<128>()); break;
-    default: PF_CK(tset_attrs<256>()); break;
+    case 64: PF_CK(tset_attrs<64>(f)); break;
+    case 128: PF_CK(tset_attrs<128>(f)); break;
+    default: PF_CK(tset_attrs<256>(f)); break;
   }
   p->tfused = f;
   p->scratch_bytes += bytes;
@@ -607,7 +623,7 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
-  ft::k_trs<N><<<kTrsBlocks, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work>>>(f->b, P, p->t_u, p->s_solid, p->ctrl);
+  ft::k_trs<N><<<f->nb_trs, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work>>>(f->b, P, p->t_u, p->s_solid, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
   transport_finalize_launch(p, f->b.part, ft::TPK<N>::TILES, p->g.inv_n);
