@@ -30,6 +30,11 @@
 
 #include "pf_fft.cuh"
 
+#ifndef PF_TF_MINB
+// the same for the forward axis-1 pass, which holds a register stash (measured:
+// 3 blocks/SM best at 256^3, 4 at 128^3)
+#define PF_TF_MINB (N >= 256 ? 3 : 4)
+#endif
 #ifndef PF_T_MINB
 #define PF_T_MINB 5  // min blocks per SM for the transport spectral / axis-1 passes (smem allows 5)
 #endif
@@ -165,13 +170,16 @@ struct TM {
   static constexpr int NCH = C::H / CM;
   static constexpr int TPC = N * NCH + N / CM;  // tiles per output component
   static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
-  static constexpr size_t BYTES = sizeof(double2) * N + 2 * SEQ;
+  // one sequence set: Y_b = FFT(X0) + i k1 FFT(X2) runs its two transforms one
+  // after the other, stashing i k1 FFT(X2) in registers (IPT items per thread)
+  static constexpr size_t BYTES = sizeof(double2) * N + SEQ;
+  static constexpr int IPT = N * CM / T;
 };
 
 // INV (MI_T): outputs oc = 0 X(chi) <- Y0; 1 X(d0 chi) <- Y1; 2 X(d1 chi) <- i k1 Y0.
 // FWD (MF_T): outputs oc = 0 Y_b <- FFT(X0) + i k1 FFT(X2); 1 Y_w0 <- FFT(X1).
 template <int N, bool INV>
-__global__ void __launch_bounds__(128, PF_T_MINB) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = TM<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
@@ -179,7 +187,6 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_taxis(TBufs B, const double*
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
   double2* S = smem + N;
-  double2* S2 = S + K::NGM * SS;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int oc = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
   const bool nyq = tile >= N * NCH;
@@ -189,25 +196,35 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_taxis(TBufs B, const double*
   auto off_of = [&](int c, int e, int q) -> size_t {
     return nyq ? (size_t)(c * N + i0b + q) * N + e : ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
   };
-  const int cin = INV ? (oc == 1 ? 1 : 0) : (oc == 1 ? 1 : 0);
+  const int cin = oc == 1 ? 1 : 0;
   const bool two = !INV && oc == 0;  // Y_b needs X0 and X2
-  for (int idx = t; idx < N * CM; idx += T) {
-    const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
-    const size_t o = off_of(cin, e, q);
-    if (INV) {
-      cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
-    } else {
-      cp16(S + q * SS + C::pad(e), nyq ? B.Xn + o : B.X + o);
-      if (two) {
-        const size_t o2 = off_of(2, e, q);
-        cp16(S2 + q * SS + C::pad(e), nyq ? B.Xn + o2 : B.X + o2);
-      }
-    }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  static_assert(K::IPT * K::T == N * CM, "whole items per thread");
   for (int j = t; j < N; j += T) tw[j] = B.tw[j];
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
+  auto stage = [&](int c) {  // one input component of the tile -> S (LDGSTS)
+    for (int idx = t; idx < N * CM; idx += T) {
+      const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+      const size_t o = off_of(c, e, q);
+      if (INV) cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
+      else cp16(S + q * SS + C::pad(e), nyq ? B.Xn + o : B.X + o);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  };
+  double2 v2[K::IPT];
+  if (two) {  // i k1 FFT(X2) first, kept in registers
+    stage(2);
+    fft_seq<N, false>(S + g * SS, tw, l, true);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < K::IPT; ++j) {
+      const int idx = t + T * j;
+      const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
+      v2[j] = cik(__ldg(kap1 + e), S[q * SS + C::pad(e)]);
+    }
+    __syncthreads();
+  }
+  stage(cin);
   if (INV && oc == 2) {  // i k1 Y(chi) before the inverse axis-1 transform
     for (int idx = t; idx < N * CM; idx += T) {
       const int q = idx / N, e = idx % N;
@@ -217,12 +234,13 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_taxis(TBufs B, const double*
     __syncthreads();
   }
   fft_seq<N, INV>(S + g * SS, tw, l, true);
-  if (two) fft_seq<N, false>(S2 + g * SS, tw, l, true);
   __syncthreads();
-  for (int idx = t; idx < N * CM; idx += T) {
+#pragma unroll
+  for (int j = 0; j < K::IPT; ++j) {
+    const int idx = t + T * j;
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
     double2 v = S[q * SS + C::pad(e)];
-    if (two) v = cadd(v, cik(__ldg(kap1 + e), S2[q * SS + C::pad(e)]));
+    if (two) v = cadd(v, v2[j]);
     const size_t o = off_of(oc, e, q);
     if (INV) {
       if (nyq) B.Xn[o] = v; else B.X[o] = v;
