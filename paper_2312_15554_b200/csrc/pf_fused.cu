@@ -33,9 +33,6 @@
 #ifndef PF_PK_PREFETCH
 #define PF_PK_PREFETCH 1
 #endif
-#ifndef PF_RS_WARP
-#define PF_RS_WARP 0  // 1: compact RS runs warp-per-tile (k_rsw_compact)
-#endif
 #ifndef PF_M_MINB
 #define PF_M_MINB 5  // min blocks per SM for the axis-1 passes: 96 regs, 5 blocks (smem-limited too)
 #endif
@@ -497,121 +494,6 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Comp
     for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
 }
 
-// ------------------------------------------------------------------ warp-per-tile compact RS
-// One warp per tile of R = 2 * (32 / G) rows: the paired-row sequences occupy
-// every lane during both FFTs, and with no staging (X, u, H and the compact
-// multipliers load straight from global into the sequence buffer / registers)
-// a block needs only the twiddles and its sequences in shared memory, so many
-// single-warp blocks fit per SM and their memory phases overlap one another's FFTs.
-template <int N>
-struct RSW {
-  using C = Cfg<N>;
-  static constexpr int NP = 32 / C::G;  // paired-row sequences per warp
-  static constexpr int R = 2 * NP;      // rows per tile
-  static constexpr int V = R * N;       // voxels per tile
-  static constexpr int VPT = V / 32;    // voxels per lane (= 32-voxel segments per tile)
-  static constexpr size_t BYTES = sizeof(double2) * (N + NP * C::SS);
-};
-
-template <int N>
-__global__ void __launch_bounds__(32) k_rsw_compact(Bufs B, State st, Compact cp, const Ctrl* __restrict__ ctrl) {
-  using C = Cfg<N>;
-  using K = RSW<N>;
-  constexpr int H = C::H, SS = C::SS, R = K::R, NP = K::NP, VPT = K::VPT;
-  constexpr int SPR = N / 32;
-  constexpr int TPC = N * N / R;
-  constexpr int NT = 3 * TPC;
-  static_assert(VPT <= 32 && 32 % SPR == 0, "one segment base per lane");
-  if (ctrl->done) return;
-  extern __shared__ __align__(128) unsigned char sraw[];
-  double2* tw = (double2*)sraw;
-  double2* S = tw + N;
-  const int lane = threadIdx.x, g = lane / C::G, l = lane % C::G;
-  for (int j = lane; j < N; j += 32) tw[j] = B.tw[j];
-  const double alpha = ctrl->alpha, b = ctrl->b;
-  const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
-  const int64_t n = (int64_t)N * N * N;
-  double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x) {
-    const int c = tile / TPC;
-    const int64_t row0 = (int64_t)(tile % TPC) * R;
-    const double2* XU = B.XU + ((size_t)c * N * N + row0) * H;
-    const double2* XUn = B.XUn + (size_t)c * N * N + row0;
-    const uint8_t* Ht = st.H + row0 * N;
-    const uint32_t o0 = __ldg(cp.off + row0);
-    const int sl = lane % VPT;  // this lane's segment (lanes >= VPT duplicate, unused)
-    const int sb = seg_base<N>(Ht + sl * 32, __ldg(cp.off + row0 + sl / SPR) - o0, lane);
-    __syncwarp();  // previous tile's readers of S are done
-    // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
-#pragma unroll
-    for (int it = 0; it < NP * H / 32; ++it) {
-      const int idx = lane + 32 * it, p = idx / H, k = idx % H;
-      double2 xa = __ldg(XU + (2 * p) * H + k), xb = __ldg(XU + (2 * p + 1) * H + k);
-      if (k == 0) xa.y = xb.y = 0.0;
-      double2* sp = S + p * SS;
-      sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
-      if (k > 0) sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
-    }
-    if (lane < NP) S[lane * SS + C::pad(H)] = make_double2(__ldg(&XUn[2 * lane].x), __ldg(&XUn[2 * lane + 1].x));
-    __syncwarp();
-    fft_seq<N, true>(S + g * SS, tw, l, true);
-    __syncwarp();
-    // (2) local step; pore: u~' = u', a' = 0, lam' = lam (only u' is stored)
-    const int64_t ubase = (int64_t)c * n + row0 * N;
-    const int64_t cbase = (int64_t)c * cp.ns + o0;
-#pragma unroll 4
-    for (int j = 0; j < VPT; ++j) {
-      const int v = lane + 32 * j, row = v / N, col = v % N;
-      double* zv = reinterpret_cast<double*>(S + (row >> 1) * SS + C::pad(col)) + (row & 1);
-      const double u1 = *zv;
-      const bool solid = Ht[v] != 0;
-      const unsigned mask = __ballot_sync(0xffffffffu, solid);
-      const int segb = __shfl_sync(0xffffffffu, sb, j);
-      const double s4 = u1 - __ldg(st.u + ubase + v);
-      acc[4] += s4 * s4;
-      double t1 = u1, a1 = 0.0;
-      if (solid) {
-        const int64_t ci = cbase + segb + __popc(mask & ((1u << lane) - 1u));
-        const double t0 = cp.ut[ci], a0 = cp.a[ci], l0 = cp.lam[ci];
-        t1 = ((a0 + b * u1) - l0) * inv_bs;  // pure.py:61 with H = 1
-        a1 = a0 + b * (u1 - t1);             // pure.py:66
-        const double l1 = l0 + alpha * t1;   // pure.py:67
-        const double s1 = t1 - t0, s3 = u1 - t1;
-        acc[0] += t1 * t1;
-        acc[1] += s1 * s1;
-        acc[2] += l1 * l1;
-        acc[3] += s3 * s3;
-        acc[5] += a1 * a1;
-        cp.ut[ci] = t1;
-        cp.a[ci] = a1;
-        cp.lam[ci] = l1;
-      }
-      st.u[ubase + v] = u1;
-      *zv = b * t1 - a1;
-    }
-    __syncwarp();
-    fft_seq<N, false>(S + g * SS, tw, l, true);
-    __syncwarp();
-    double2* XR = B.XR + ((size_t)c * N * N + row0) * H;
-    double2* XRn = B.XRn + (size_t)c * N * N + row0;
-#pragma unroll
-    for (int it = 0; it < NP * H / 32; ++it) {
-      const int idx = lane + 32 * it, p = idx / H, k = idx % H;
-      const double2 zk = S[p * SS + C::pad(k)], zm = S[p * SS + C::pad((N - k) & (N - 1))];
-      XR[(2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-      XR[(2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-    }
-    if (lane < NP) {
-      const double2 z = S[lane * SS + C::pad(H)];
-      XRn[2 * lane] = make_double2(z.x, 0.0);
-      XRn[2 * lane + 1] = make_double2(z.y, 0.0);
-    }
-  }
-  block_sum<6>(acc);
-  if (lane == 0)
-    for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
-}
-
 // RS-fix on the compact path: u~' rows = u' on pore voxels, the compact u~ on solid ones.
 template <int N>
 __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const double* __restrict__ u,
@@ -772,6 +654,23 @@ __global__ void __launch_bounds__(kThreads) k_pore_a_lam(int64_t n, const uint8_
 //        -> Y-space R~ = FFT_1(b' u~' - a')
 //   INV: Y-space U^ -> X-space u'                                 (IFFT_1)
 template <int N>
+struct PK2 {
+  using C = Cfg<N>;
+  static constexpr int T = PF_PK_THREADS;
+  static constexpr int NGP = T / C::G;
+  // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
+  static constexpr int CP = (NGP % 3 == 0) ? NGP / 3 : NGP / 2;
+  static constexpr int NSEQ = 3 * CP;
+  static constexpr int NCH = C::H / CP;
+  static constexpr int TILES = N * NCH + N / CP;
+  static constexpr int MPT = (CP * N + T - 1) / T;  // modes per thread (last one guarded)
+  // sequence stride with an 8-bank shift: the (q fastest, 4 columns) staging
+  // pattern of 8-lane phases is then conflict-free
+  static constexpr int SS = C::SS + 1;
+  static constexpr size_t BYTES = sizeof(double2) * ((PF_PK_TWG ? 0 : N) + NSEQ * SS);
+};
+
+template <int N>
 struct M2 {
   using C = Cfg<N>;
   static constexpr int T = 128;
@@ -852,22 +751,6 @@ struct SpecArgs {
 // padded sequences; Q^ and D^ live in tile-major order ([tile][q][k0]) so the
 // spectral step reads and writes them fully coalesced, prefetched into
 // registers before the forward FFTs.
-template <int N>
-struct PK2 {
-  using C = Cfg<N>;
-  static constexpr int T = PF_PK_THREADS;
-  static constexpr int NGP = T / C::G;
-  // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
-  static constexpr int CP = (NGP % 3 == 0) ? NGP / 3 : NGP / 2;
-  static constexpr int NSEQ = 3 * CP;
-  static constexpr int NCH = C::H / CP;
-  static constexpr int TILES = N * NCH + N / CP;
-  static constexpr int MPT = (CP * N + T - 1) / T;  // modes per thread (last one guarded)
-  // sequence stride with an 8-bank shift: the (q fastest, 4 columns) staging
-  // pattern of 8-lane phases is then conflict-free
-  static constexpr int SS = C::SS + 1;
-  static constexpr size_t BYTES = sizeof(double2) * ((PF_PK_TWG ? 0 : N) + NSEQ * SS);
-};
 
 template <int N>
 __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
@@ -1091,8 +974,6 @@ static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsw_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)fz::RSW<N>::BYTES));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
@@ -1105,11 +986,6 @@ static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N>, fz::RS2<N>::T, smem_rsc<N>()));
   f->nb_full = wave(o1, 3);
   f->nb_compact = wave(o2, kRsMaxBlocks / kSMs);
-#if PF_RS_WARP
-  int o3 = 0;
-  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, fz::k_rsw_compact<N>, 32, fz::RSW<N>::BYTES));
-  f->nb_compact = wave(o3, kRsMaxBlocks / kSMs);
-#endif
   f->nb_rs = f->nb_full;
   return PF_OK;
 }
@@ -1328,11 +1204,7 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
   if (f->compact) {
-#if PF_RS_WARP
-    fz::k_rsw_compact<N><<<f->nb_rs, 32, fz::RSW<N>::BYTES, p->work>>>(f->b, st, compact_of(f), p->ctrl);
-#else
     fz::k_rs_compact<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsc<N>(), p->work>>>(f->b, st, compact_of(f), p->ctrl);
-#endif
   } else {
     fz::k_rs<N><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
   }

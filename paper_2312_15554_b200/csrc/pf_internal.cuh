@@ -53,7 +53,13 @@ const char* cufft_name(cufftResult r);
 constexpr int kThreads = 256;
 constexpr int kSMs = 148;
 constexpr int kMaxBlocks = kSMs * 8;  // 8 x 256-thread CTAs fill an SM (2048 threads)
-constexpr int kFinalizeThreads = 512;
+#ifndef PF_FINALIZE_THREADS
+#define PF_FINALIZE_THREADS 1024
+#endif
+#ifndef PF_REDUCE_UNROLL
+#define PF_REDUCE_UNROLL 4  // independent running sums (loads in flight) per thread in reduce_partials
+#endif
+constexpr int kFinalizeThreads = PF_FINALIZE_THREADS;
 
 inline int blocks_for(int64_t work) {
   int64_t b = (work + kThreads - 1) / kThreads;
@@ -262,24 +268,33 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
 // combined in a fixed order, then a fixed-shape block tree.
 template <int NQ>
 __device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nblk, double (&tot)[NQ]) {
-  double s4[NQ][4];
+  constexpr int U = PF_REDUCE_UNROLL;
+  double s4[NQ][U];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s4[q][u] = 0.0;
+    for (int u = 0; u < U; ++u) s4[q][u] = 0.0;
   const int stride = blockDim.x;
   int i = threadIdx.x;
-  for (; i + 3 * stride < nblk; i += 4 * stride) {
+  for (; i + (U - 1) * stride < nblk; i += U * stride) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) s4[q][u] += part[(int64_t)q * nblk + i + u * stride];
+      for (int u = 0; u < U; ++u) s4[q][u] += part[(int64_t)q * nblk + i + u * stride];
   }
   for (; i < nblk; i += stride)
 #pragma unroll
     for (int q = 0; q < NQ; ++q) s4[q][0] += part[(int64_t)q * nblk + i];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) tot[q] = (s4[q][0] + s4[q][1]) + (s4[q][2] + s4[q][3]);
+  for (int q = 0; q < NQ; ++q) {
+    double x = 0.0;  // fixed pairwise order
+#pragma unroll
+    for (int w = 1; w < U; w <<= 1)
+#pragma unroll
+      for (int u = 0; u < U; u += 2 * w) s4[q][u] += s4[q][u + w];
+    x = s4[q][0];
+    tot[q] = x;
+  }
   block_sum<NQ>(tot);
 }
 
