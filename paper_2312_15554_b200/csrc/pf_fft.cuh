@@ -8,9 +8,6 @@
 
 #include "pf_internal.cuh"
 
-#ifndef PF_TW_FACTORED
-#define PF_TW_FACTORED 1  // 1: pass-1 twiddles from 6 table loads (see fft_seq)
-#endif
 
 namespace pf {
 namespace fz {
@@ -31,6 +28,8 @@ struct Cfg {
   static constexpr int M_TILES = N * NCHM + N / CM;
   static constexpr int PK_TILES = N * NCHP + N / CP;
   static constexpr int RS_TILES = N * N / RSR;
+  // compact pass-1 twiddle table: rows w^b (b = 1..3) and w^(4a) (a = 1..A/4-1), B lanes each
+  static constexpr int TWN = (3 + A / 4 - 1) * B;
   static __device__ __forceinline__ int pad(int e) { return e + e / A; }
 };
 
@@ -158,18 +157,23 @@ struct Dft<16, INV> {
   static __device__ __forceinline__ void run(double2* x) { dft_pq<4, 4, INV>(x); }
 };
 
-// Pass-1 twiddle table, laid out [k1][l] (A x B = N entries): entry k1*B + l =
-// exp(-2 pi i l k1 / N).  Lane l's loads for fixed k1 are then consecutive, so a
-// quarter-warp never hits the same bank twice (the natural tw[l*k1] layout is
-// 2..8-way conflicted for even k1).
+// Pass-1 twiddle table (Cfg::TWN entries): the rows fft_seq reads, w^(b l) for
+// b = 1..3 then w^(4a l) for a = 1..A/4-1, each laid out over the lanes l < B
+// (w = exp(-2 pi i / N)).  Lane-consecutive, so a quarter-warp never hits the
+// same bank twice (the natural tw[l*k1] layout is 2..8-way conflicted for even k1).
 template <int N>
 inline void pass1_twiddles(double2* out) {
   using C = Cfg<N>;
-  for (int k1 = 0; k1 < C::A; ++k1)
+  int r = 0;
+  auto row = [&](int k1) {
     for (int l = 0; l < C::B; ++l) {
       const double a = 2.0 * M_PI * (double)(l * k1) / (double)N;
-      out[k1 * C::B + l] = make_double2(std::cos(a), -std::sin(a));
+      out[r * C::B + l] = make_double2(std::cos(a), -std::sin(a));
     }
+    ++r;
+  };
+  for (int b = 1; b < 4; ++b) row(b);
+  for (int a = 1; a < C::A / 4; ++a) row(4 * a);
 }
 
 // One N-point complex FFT (unnormalised) of the padded smem sequence s by the
@@ -187,14 +191,13 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
 #pragma unroll
     for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
     Dft<A, INV>::run(x);
-#if PF_TW_FACTORED
     // w^(4a+b) = w^(4a) * w^b from 3 + A/4-1 table loads instead of A-1 (shared
     // memory bandwidth is the scarce resource of these kernels); <= 2 ulp.
     double2 wb[4], wa[A / 4];
 #pragma unroll
-    for (int b = 1; b < 4; ++b) wb[b] = tw[b * B + l];
+    for (int b = 1; b < 4; ++b) wb[b] = tw[(b - 1) * B + l];
 #pragma unroll
-    for (int a = 1; a < A / 4; ++a) wa[a] = tw[4 * a * B + l];
+    for (int a = 1; a < A / 4; ++a) wa[a] = tw[(2 + a) * B + l];
 #pragma unroll
     for (int k1 = 1; k1 < A; ++k1) {
       const int a = k1 / 4, b = k1 % 4;
@@ -202,14 +205,6 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
       if (INV) w.y = -w.y;
       x[k1] = cmul(x[k1], w);
     }
-#else
-#pragma unroll
-    for (int k1 = 1; k1 < A; ++k1) {
-      double2 w = tw[k1 * B + l];
-      if (INV) w.y = -w.y;
-      x[k1] = cmul(x[k1], w);
-    }
-#endif
   }
   __syncwarp();
   if (p1) {

@@ -33,11 +33,16 @@
 #ifndef PF_PK_PREFETCH
 #define PF_PK_PREFETCH 1
 #endif
+#ifndef PF_RSC_MINB
+// min CTAs/SM for the compact RS (measured: N = 256 at 4 keeps 240 registers,
+// forcing 5 squeezes ptxas to 168 with spills and is 16 % slower; N <= 128 at 3)
+#define PF_RSC_MINB (RS2<N>::T == 64 ? 4 : 3)
+#endif
+#ifndef PF_RSC_MAXNREG
+#define PF_RSC_MAXNREG
+#endif
 #ifndef PF_M_MINB
 #define PF_M_MINB 5  // min blocks per SM for the axis-1 passes: 96 regs, 5 blocks (smem-limited too)
-#endif
-#ifndef PF_PK_TWG
-#define PF_PK_TWG 0  // 1: k_pk reads twiddles from global (L1) instead of staging them in smem
 #endif
 #ifndef PF_PK_MINB
 #define PF_PK_MINB 3  // __launch_bounds__ min blocks per SM for k_pk (1 lets ptxas take 216 regs: 2 blocks/SM, slower)
@@ -64,11 +69,6 @@ struct State {
   const uint8_t* H;
 };
 
-template <int N>
-__device__ __forceinline__ void load_tw(double2* tw, const double2* __restrict__ g) {
-  for (int j = threadIdx.x; j < N; j += blockDim.x) tw[j] = g[j];
-}
-
 // ------------------------------------------------------------------ RS
 // Persistent: grid = 3 blocks per SM; each block walks tiles of R2 rows of one
 // velocity component.  Per tile, one thread issues TMA bulk copies of the
@@ -85,7 +85,7 @@ struct RS2 {
   static constexpr int VPT = V / T;             // voxels per thread
   static constexpr int NP = R / 2;              // inverse sequences (two rows each)
   // shared-memory carve (bytes)
-  static constexpr size_t TW = sizeof(double2) * N;
+  static constexpr size_t TW = sizeof(double2) * C::TWN;
   static constexpr size_t INV = sizeof(double2) * NP * C::SS;
   static constexpr size_t FWD = sizeof(double2) * NP * C::SS;
   static constexpr size_t ST = sizeof(double) * 4 * V;     // u, u~, a, lam rows
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   double2* sxn = (double2*)(sraw + K::TW + K::INV + K::ST + K::XM);
   uint8_t* sh = (uint8_t*)(sraw + K::TW + K::INV + K::ST + K::XM + K::XN);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
   const double inv_bp = 1.0 / b, inv_bs = 1.0 / (b + alpha);  // pore / solid divisors of pure.py:61
   const int64_t n = (int64_t)N * N * N;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   double2* SF = (double2*)(sraw + K::TW);
   double* sst = (double*)(sraw + K::TW + K::INV);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const int64_t n = (int64_t)N * N * N;
   auto issue = [&](int tile) {
     const int c = tile / TPC;
@@ -303,14 +303,19 @@ struct Compact {
   const uint32_t* off;   // [N*N + 1]
   double *ut, *a, *lam;  // [3][ns]
   int64_t ns;
+  int cs;                // staging capacity per tile: max padded solid count of any tile, rounded to 16
 };
 
 template <int N>
 struct RSC {
   using K = RS2<N>;
-  static constexpr int CS = K::V + K::R;  // compact staging stride (max padded solid count per tile)
-  static constexpr size_t BYTES = K::TW + K::INV /*inverse = forward, in place*/ + sizeof(double) * K::V /*u*/ +
-                                  3 * sizeof(double) * CS /*u~, a, lam*/ + K::XM + K::XN + K::HB;
+  static constexpr int CS = K::V + K::R + 16;  // worst-case staging capacity (every voxel solid)
+  // dynamic smem for staging capacity cs (sized per geometry at setup)
+  static constexpr size_t bytes(int cs) {
+    return K::TW + K::INV /*inverse = forward, in place*/ + sizeof(double) * K::V /*u*/ +
+           3 * sizeof(double) * (size_t)cs /*u~, a, lam*/ + K::XM + K::XN + K::HB;
+  }
+  static constexpr size_t BYTES = bytes(CS);
 };
 
 // o0 / o1 = compact offsets of the tile's first row and of the row after it
@@ -338,8 +343,8 @@ __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& 
   if (cb) {
     const int64_t base = (int64_t)c * cp.ns + o0;
     bulk_load(sc, cp.ut + base, cb, mbar);
-    bulk_load(sc + RSC<N>::CS, cp.a + base, cb, mbar);
-    bulk_load(sc + 2 * RSC<N>::CS, cp.lam + base, cb, mbar);
+    bulk_load(sc + cp.cs, cp.a + base, cb, mbar);
+    bulk_load(sc + 2 * cp.cs, cp.lam + base, cb, mbar);
   }
 }
 
@@ -365,14 +370,14 @@ __device__ __forceinline__ int seg_base(const uint8_t* seg_bytes, uint32_t row_o
 }
 
 template <int N>
-__global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Compact cp, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_compact(Bufs B, State st, Compact cp, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   constexpr int TPC = N * N / R;
   constexpr int NT = 3 * TPC;
   constexpr int SPR = N / 32;  // 32-voxel segments per row
-  constexpr int CS = RSC<N>::CS;
+  const int CS = cp.cs;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Comp
   double2* sxn = (double2*)((unsigned char*)sx + K::XM);
   uint8_t* sh = (uint8_t*)((unsigned char*)sxn + K::XN);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
   const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
   const int64_t n = (int64_t)N * N * N;
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs_compact(Bufs B, State st, Comp
     }
     __syncthreads();
   }
-  block_sum<6>(acc);
+  block_sum<6, RS2<N>::T / 32>(acc);
   if (t == 0)
     for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
 }
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   double2* tw = (double2*)sraw;
   double2* SF = (double2*)(sraw + K::TW);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const int64_t n = (int64_t)N * N * N;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x) {
     const int c = tile / TPC;
@@ -548,6 +553,19 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
 }
 
 // ---- compact layout setup / teardown (warp per row of N voxels)
+// largest padded solid count of any RS tile -> mx (zeroed by the caller)
+template <int N>
+__global__ void k_tile_max(const uint32_t* __restrict__ off, uint32_t* __restrict__ mx) {
+  constexpr int R = RS2<N>::R;
+  const int64_t tiles = (int64_t)N * N / R;
+  uint32_t m = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tiles; t += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, off[(t + 1) * R] - off[t * R]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
 template <int N>
 __global__ void k_row_counts(const uint8_t* __restrict__ Hs, uint32_t* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
@@ -667,7 +685,7 @@ struct PK2 {
   // sequence stride with an 8-bank shift: the (q fastest, 4 columns) staging
   // pattern of 8-lane phases is then conflict-free
   static constexpr int SS = C::SS + 1;
-  static constexpr size_t BYTES = sizeof(double2) * ((PF_PK_TWG ? 0 : N) + NSEQ * SS);
+  static constexpr size_t BYTES = sizeof(double2) * (C::TWN + NSEQ * SS);
 };
 
 template <int N>
@@ -680,8 +698,8 @@ struct M2 {
   static constexpr int TPC = N * NCH + N / CM;  // tiles per component
   static constexpr int TILES = 3 * TPC;
   static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
-  static constexpr size_t BYTES_INV = sizeof(double2) * N + SEQ;
-  static constexpr size_t BYTES_FWD = sizeof(double2) * N + SEQ;
+  static constexpr size_t BYTES_INV = sizeof(double2) * C::TWN + SEQ;
+  static constexpr size_t BYTES_FWD = sizeof(double2) * C::TWN + SEQ;
 };
 
 template <int N, bool INV>
@@ -692,7 +710,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
-  double2* S = smem + N;
+  double2* S = smem + Cfg<N>::TWN;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int c = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
   const bool nyq = tile >= N * NCH;
@@ -709,7 +727,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     if (INV) cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
     else cp16(S + q * SS + C::pad(e), nyq ? B.XRn + o : B.XR + o);
   }
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   cp_commit_wait_all();
   __syncthreads();
   if (!INV) {
@@ -759,13 +777,8 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   constexpr int H = C::H, SS = K::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
-#if PF_PK_TWG
-  const double2* tw = B.tw;
-  double2* S = smem;
-#else
   double2* tw = smem;
-  double2* S = smem + N;
-#endif
+  double2* S = smem + Cfg<N>::TWN;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const double beta = ctrl->beta, b = ctrl->b;
   const int tile = blockIdx.x;
@@ -793,9 +806,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
     }
   }
 #endif
-#if !PF_PK_TWG
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
-#endif
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 #pragma unroll
@@ -939,6 +950,7 @@ struct FusedPlan {
   uint32_t* c_off = nullptr;
   double* c_data = nullptr;
   int64_t c_ns = 0, c_cap = 0;
+  int c_cs = 16;  // staging capacity per tile (Compact::cs)
   int compact = 0;
   int nb_rs = kSMs;              // persistent RS grid of the active path (full or compact)
   int nb_full = kSMs, nb_compact = kSMs;
@@ -1021,13 +1033,13 @@ int fused_ensure(pf_plan* p) {
   f->b.tw = take(N);
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
-  std::vector<double2> tw(N);
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
     default: fz::pass1_twiddles<256>(tw.data()); break;
   }
-  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
   size_t ws = 0;
@@ -1090,6 +1102,7 @@ static fz::Compact compact_of(FusedPlan* f) {
   c.a = f->c_data + 3 * f->c_ns;
   c.lam = f->c_data + 6 * f->c_ns;
   c.ns = f->c_ns;
+  c.cs = f->c_cs;
   return c;
 }
 
@@ -1110,16 +1123,29 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
   if (!f->compact) return PF_OK;
   if (!f->c_cnt) {
     PF_CK_CUDA(cudaMalloc(&f->c_cnt, sizeof(uint32_t) * rows));
-    PF_CK_CUDA(cudaMalloc(&f->c_off, sizeof(uint32_t) * (rows + 1)));
+    PF_CK_CUDA(cudaMalloc(&f->c_off, sizeof(uint32_t) * (rows + 2)));  // + the tile max
   }
   fz::k_row_counts<N><<<blocks_for(rows * 32), kThreads, 0, p->work>>>(p->s_solid, f->c_cnt);
   fz::k_scan<<<1, 1024, 0, p->work>>>(f->c_cnt, f->c_off, rows);
+  PF_CK_CUDA(cudaMemsetAsync(f->c_off + rows + 1, 0, sizeof(uint32_t), p->work));
+  fz::k_tile_max<N><<<blocks_for(rows / fz::RS2<N>::R), kThreads, 0, p->work>>>(f->c_off, f->c_off + rows + 1);
   PF_CK_CUDA(cudaGetLastError());
-  uint32_t ns = 0;
-  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, f->c_off + rows, sizeof(uint32_t), cudaMemcpyDeviceToHost, p->work));
+  uint32_t nm[2] = {0, 0};
+  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, f->c_off + rows, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, p->work));
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
-  std::memcpy(&ns, p->h_small, sizeof(uint32_t));
+  std::memcpy(nm, p->h_small, 2 * sizeof(uint32_t));
+  const uint32_t ns = nm[0];
   f->c_ns = ns;
+  // staging sized by this geometry's densest tile: fewer bytes of smem -> more resident RS CTAs
+  f->c_cs = (int)((nm[1] + 15u) & ~15u);
+  if (f->c_cs < 16) f->c_cs = 16;
+  {
+    int o = 0;
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fz::k_rs_compact<N>, fz::RS2<N>::T,
+                                                             fz::RSC<N>::bytes(f->c_cs)));
+    f->nb_compact = (o < 1 ? 1 : (o > kRsMaxBlocks / kSMs ? kRsMaxBlocks / kSMs : o)) * kSMs;
+    f->nb_rs = f->nb_compact;
+  }
   const int64_t need = 9 * (int64_t)(ns > 0 ? ns : 2);
   if (need > f->c_cap) {
     cudaFree(f->c_data);
@@ -1204,7 +1230,8 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
   if (f->compact) {
-    fz::k_rs_compact<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsc<N>(), p->work>>>(f->b, st, compact_of(f), p->ctrl);
+    fz::k_rs_compact<N><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(f->b, st, compact_of(f),
+                                                                                          p->ctrl);
   } else {
     fz::k_rs<N><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
   }

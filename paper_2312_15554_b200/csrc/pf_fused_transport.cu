@@ -74,7 +74,7 @@ struct TPK {
   static constexpr int NCH = C::H / CP;
   static constexpr int TILES = N * NCH + N / CP;
   static constexpr int MPT = CP * N / T;
-  static constexpr size_t BYTES = sizeof(double2) * (N + NSEQ * C::SS);
+  static constexpr size_t BYTES = sizeof(double2) * (C::TWN + NSEQ * C::SS);
 };
 
 template <int N>
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_tpk(TBufs B, TP P, const Ctr
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
-  double2* S = smem + N;
+  double2* S = smem + Cfg<N>::TWN;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int tile = blockIdx.x;
   const bool nyq = tile >= N * NCH;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_tpk(TBufs B, TP P, const Ctr
     cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const bool first = (B.G0 != nullptr) && ctrl->iter == 0;
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -172,7 +172,7 @@ struct TM {
   static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
   // one sequence set: Y_b = FFT(X0) + i k1 FFT(X2) runs its two transforms one
   // after the other, stashing i k1 FFT(X2) in registers (IPT items per thread)
-  static constexpr size_t BYTES = sizeof(double2) * N + SEQ;
+  static constexpr size_t BYTES = sizeof(double2) * C::TWN + SEQ;
   static constexpr int IPT = N * CM / T;
 };
 
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
-  double2* S = smem + N;
+  double2* S = smem + Cfg<N>::TWN;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int oc = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
   const bool nyq = tile >= N * NCH;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
   const int cin = oc == 1 ? 1 : 0;
   const bool two = !INV && oc == 0;  // Y_b needs X0 and X2
   static_assert(K::IPT * K::T == N * CM, "whole items per thread");
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   auto stage = [&](int c) {  // one input component of the tile -> S (LDGSTS)
     for (int idx = t; idx < N * CM; idx += T) {
       const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
@@ -260,7 +260,7 @@ struct TRS {
   static constexpr int T = NSF * C::G;       // one group per forward sequence
   static constexpr int V = R * N;
   static constexpr int VPT = V / T;
-  static constexpr size_t TW = sizeof(double2) * N;
+  static constexpr size_t TW = sizeof(double2) * C::TWN;
   static constexpr size_t SI = sizeof(double2) * NSI * C::SS;
   static constexpr size_t SF = sizeof(double2) * NSF * C::SS;
   static constexpr size_t XM = sizeof(double2) * 3 * R * C::H;   // X comps 0..2, R rows each
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
   double* su = (double*)(sraw + K::TW + K::SQ + K::XM + K::XN);
   uint8_t* sh = (uint8_t*)(sraw + K::TW + K::SQ + K::XM + K::XN + K::UB);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  for (int j = t; j < N; j += T) tw[j] = B.tw[j];
+  for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double* kap2 = P.kap[2];
   if (t == 0) {
     fz::mbar_init(&mbar);
@@ -530,13 +530,13 @@ static int tfused_ensure(pf_plan* p) {
   f->b.Yn = take(2 * NN);
   f->b.tw = take(N);
   f->b.part = (double*)m;
-  std::vector<double2> tw(N);
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
     default: fz::pass1_twiddles<256>(tw.data()); break;
   }
-  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   size_t ws = 0;
   long long dims2[2] = {N, N};
   PF_CK_FFT(cufftCreate(&f->plan2d));

@@ -239,9 +239,9 @@ __device__ __forceinline__ double2 cdiv_np(double2 a, double2 b) {
 }
 
 // Block-wide sum of NQ per-thread values; thread 0 returns the totals in v.
-template <int NQ>
+template <int NQ, int MAXW = 32>
 __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
-  __shared__ double sh[NQ][32];
+  __shared__ double sh[NQ][MAXW];  // MAXW >= warps per block
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
