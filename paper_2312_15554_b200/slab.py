@@ -128,13 +128,19 @@ class SlabStokes:
     """
 
     def __init__(self, backend, dims, cfg: StokesConfig, penalties: PenaltyParams | None, solid_local, state,
-                 group=None, poll_every: int = 8):
+                 group=None, poll_every: int = 8, comm=None):
+        """``comm``: an object with torch.distributed's ``get_world_size`` /
+        ``all_to_all_single`` / ``all_reduce`` (default: torch.distributed when
+        initialised); tests inject an in-process loopback to run P ranks on one GPU."""
         import torch.distributed as dist
 
         self.b, self.dims, self.cfg = backend, tuple(int(x) for x in dims), cfg
         self.pen = penalties or PenaltyParams()
         self.solid, self.state, self.group, self.poll = solid_local, state, group, max(1, int(poll_every))
-        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        if comm is not None:
+            self.dist = comm
+        else:
+            self.dist = dist if dist.is_available() and dist.is_initialized() else None
         self.world = self.dist.get_world_size(group) if self.dist else 1
         be = backend
         self.send = be.alloc_complex(3 * be.exch)
@@ -224,7 +230,7 @@ class SlabStokes:
 
 
 def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalties: PenaltyParams | None = None,
-                      init_local: dict | None = None, group=None, device=None):
+                      init_local: dict | None = None, group=None, device=None, comm=None):
     """Device slab solve on this rank: ``solid_local`` is the rank's x-slab of the
     indicator (uint8, (N0/P, N1, N2)); returns (local state dict of CUDA tensors,
     ConvergenceReport — identical on every rank)."""
@@ -234,8 +240,11 @@ def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalt
     cfg = cfg or StokesConfig(pressure_gradient=(1.0, 0.0, 0.0))
     if len(cfg.pressure_gradient) != 3 or len(dims) != 3:
         raise ValueError("slab decomposition is 3D")
-    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-    rank = dist.get_rank(group) if world > 1 else 0
+    if comm is not None:
+        world, rank = comm.get_world_size(group), comm.get_rank(group)
+    else:
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        rank = dist.get_rank(group) if world > 1 else 0
     lo, hi = slab_range(int(dims[0]), world, rank)
     if tuple(np.shape(solid_local)) != (hi - lo, int(dims[1]), int(dims[2])):
         raise ValueError("solid_local must be this rank's x-slab")
@@ -250,7 +259,7 @@ def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalt
         st = {k: t.as_tensor(np.asarray(init_local[k], dtype=np.float64)).reshape(-1).to(dev).clone()
               for k in ("u", "u_tilde", "q", "a", "lam")}
     solid = t.as_tensor(np.array(solid_local, dtype=np.uint8, copy=True)).reshape(-1).to(dev)
-    solver = SlabStokes(be, dims, cfg, penalties, solid, st, group)
+    solver = SlabStokes(be, dims, cfg, penalties, solid, st, group, comm=comm)
     rep = solver.solve()
     t.cuda.synchronize(dev)
     shp3, shp1 = (3, hi - lo, int(dims[1]), int(dims[2])), (hi - lo, int(dims[1]), int(dims[2]))

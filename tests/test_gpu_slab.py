@@ -49,3 +49,33 @@ def test_device_slab_matches_fused_at_64(pf):
     for k in ("u", "u_tilde", "q", "a", "lam"):
         assert rel_l2(st[k].cpu().numpy(), getattr(ref, k).cpu().numpy()) <= 1e-10, k
     np.testing.assert_allclose(rep.history, rref.history, rtol=1e-6, atol=1e-9 * np.abs(rref.history).max())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", ["stokes_sphere16_stiff", "stokes_sphere12_adaptive"])
+def test_device_slab_multi_rank_loopback(pf, golden, case, world):
+    """P ranks' device backends on one GPU (tests/slab_loopback.py): every
+    rank's slab offsets, zero-mode ownership and packing, against the reference."""
+    from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
+    from slab_loopback import run_ranks
+
+    z = golden(case)
+    n0 = z["solid"].shape[0]
+    if n0 % world:
+        pytest.skip("slab count must divide the first axis")
+    pen = z["penalties"]
+    penalties = pf.PenaltyParams(alpha=float(pen[0]), beta=float(pen[1]), b=float(pen[2]), adaptive=bool(pen[3]))
+    cfg = pf.StokesConfig.with_tolerance(float(z["eps"]), pressure_gradient=tuple(z["g_p"]),
+                                         max_iter=int(z["max_iter"]))
+
+    def rank_fn(r, comm):
+        lo, hi = slab_range(n0, world, r)
+        st, rep = solve_stokes_slab(z["solid"][lo:hi], z["solid"].shape, cfg, penalties, comm=comm)
+        return {k: v.cpu().numpy() for k, v in st.items()}, rep
+
+    res = run_ranks(world, rank_fn)
+    for _, rep in res:
+        assert rep.iterations == int(z["iterations"]) and rep.converged == bool(z["converged"])
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        full = np.concatenate([st[k] for st, _ in res], axis=0 if k == "q" else 1)
+        assert rel_l2(full, z[k]) <= 1e-10, k
