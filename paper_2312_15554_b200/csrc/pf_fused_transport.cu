@@ -30,6 +30,12 @@
 
 #include "pf_fft.cuh"
 
+#ifndef PF_TPK_PREFETCH
+#define PF_TPK_PREFETCH 1  // previous chi^ loaded into registers under the forward FFT (needs 4 CTAs/SM of regs)
+#endif
+#ifndef PF_TPK_MINB
+#define PF_TPK_MINB 4
+#endif
 #ifndef PF_TF_MINB
 // the same for the forward axis-1 pass, which holds a register stash (measured:
 // 3 blocks/SM best at 256^3, 4 at 128^3)
@@ -78,7 +84,7 @@ struct TPK {
 };
 
 template <int N>
-__global__ void __launch_bounds__(128, PF_T_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = TPK<N>;
   constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
@@ -102,14 +108,23 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_tpk(TBufs B, TP P, const Ctr
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const bool first = (B.G0 != nullptr) && ctrl->iter == 0;
+  const size_t tbase = (size_t)tile * CP * N;
+#if PF_TPK_PREFETCH
+  double2 chp[K::MPT];  // previous chi^ of this thread's modes, loaded under the forward FFT
+#pragma unroll
+  for (int j = 0; j < K::MPT; ++j) chp[j] = B.CH[tbase + t + T * j];
+#endif
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   fft_seq<N, false>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
   __syncthreads();
-  const size_t tbase = (size_t)tile * CP * N;
   const size_t nh = (size_t)K::TILES * CP * N;
   double acc[2] = {0.0, 0.0};
+#if PF_TPK_PREFETCH
+#pragma unroll
+#else
 #pragma unroll 2
+#endif
   for (int j = 0; j < K::MPT; ++j) {
     const int m = t + T * j, q = m / N, k0 = m % N;
     const int kk1 = nyq ? k1b + q : k1, k2 = nyq ? H : ch * CP + q;
@@ -127,7 +142,11 @@ __global__ void __launch_bounds__(128, PF_T_MINB) k_tpk(TBufs B, TP P, const Ctr
     const double2 f = cadd(fb, cik(kc[0], fw0));  // F^ = S^ + i k.W^   (pure.py:104-105)
     const bool zero = (k0 | kk1 | k2) == 0;
     const double2 chi = zero ? make_double2(0.0, 0.0) : cdiv_np(f, make_double2(P.a0 * L, bk));
+#if PF_TPK_PREFETCH
+    const double2 prev = chp[j];
+#else
     const double2 prev = B.CH[tbase + m];
+#endif
     const double2 dch = csub(chi, prev);
     const double w = (k2 == 0 || k2 == H) ? 1.0 : 2.0;
     acc[0] += w * cabs2(dch);
