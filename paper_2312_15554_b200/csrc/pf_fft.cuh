@@ -20,6 +20,7 @@ struct Cfg {
   static constexpr int NG = 256 / G;            // groups per 256-thread block
   static constexpr int SS = N + N / A + 1;      // padded smem sequence stride (complex)
   static constexpr int H = N / 2;               // stored half-spectrum columns (k2 < N/2)
+  static constexpr int LOGN = N == 64 ? 6 : (N == 128 ? 7 : 8);
   static constexpr int RSR = NG;                // rows per RS tile
   static constexpr int CM = NG;                 // k2 columns per MF / MI tile
   static constexpr int CP = NG / 2;             // k2 columns per PK tile

@@ -62,6 +62,17 @@ struct Bufs {
   double2* D;         // full spectrum D^_prev, same layout
   double2* tw;        // N forward twiddles
   double *part_rs, *part_pk;
+  // slab layout (single GPU: l0 = l1 = N, s1 = log2 N, k1off = 0): this rank's
+  // x-slab holds l0 i0-planes, its y-slab l1 k1-planes starting at k1off; P = N / l1
+  // is a power of two (s1 = log2 l1).  Y (after axes 2, 1; axis 0 real) exists in
+  // two exchange-native layouts so the all-to-alls move contiguous blocks (one
+  // exchange per component for the main arrays, one for all Nyquist columns):
+  //   y-slab (PK):     Yy [c][i0][k1 - k1off][k2],   Yn  [i0][c][k1 - k1off]
+  //   x-slab (MI, MF): Yx [c][r][i0 - i0off][k1 - r l1][k2],   Yxn [r][i0 - i0off][c][k1 - r l1]
+  // (r = owner of k1); at P = 1 they coincide.  X and the real state are x-slab
+  // [c][l0 N rows][...].
+  int l0, l1, s1, k1off;
+  double2 *Yx, *Yxn;  // x-slab Y (== Y, Yn at P = 1)
 };
 
 struct State {
@@ -98,15 +109,15 @@ struct RS2 {
   static constexpr uint32_t TX = (uint32_t)(ST + XM + XN + HB);
 };
 
-template <int N>
+template <int N, bool SL>
 __device__ __forceinline__ void rs_issue(int tile, const Bufs& B, const State& st, double* sst, double2* sx,
                                          double2* sxn, uint8_t* sh, uint64_t* mbar) {
   using K = RS2<N>;
   using C = Cfg<N>;
-  constexpr int TPC = N * N / K::R;  // tiles per component
+  const int TPC = (SL ? B.l0 : N) * N / K::R;  // tiles per component
   const int c = tile / TPC;
   const int64_t row0 = (int64_t)(tile % TPC) * K::R;
-  const int64_t n = (int64_t)N * N * N;
+  const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   const int64_t x0 = (int64_t)c * n + row0 * N;
   const uint32_t vb = sizeof(double) * K::V;
   fence_async_smem();
@@ -115,18 +126,18 @@ __device__ __forceinline__ void rs_issue(int tile, const Bufs& B, const State& s
   bulk_load(sst + 1 * K::V, st.ut + x0, vb, mbar);
   bulk_load(sst + 2 * K::V, st.a + x0, vb, mbar);
   bulk_load(sst + 3 * K::V, st.lam + x0, vb, mbar);
-  bulk_load(sx, B.XU + ((int64_t)c * N * N + row0) * C::H, (uint32_t)K::XM, mbar);
-  bulk_load(sxn, B.XUn + (int64_t)c * N * N + row0, (uint32_t)K::XN, mbar);
+  bulk_load(sx, B.XU + ((int64_t)c * (SL ? B.l0 : N) * N + row0) * C::H, (uint32_t)K::XM, mbar);
+  bulk_load(sxn, B.XUn + (int64_t)c * (SL ? B.l0 : N) * N + row0, (uint32_t)K::XN, mbar);
   bulk_load(sh, st.H + row0 * N, (uint32_t)K::HB, mbar);
 }
 
-template <int N>
+template <int N, bool SL>
 __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  constexpr int TPC = N * N / R;
-  constexpr int NT = 3 * TPC;
+  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int NT = 3 * TPC;
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   __shared__ uint64_t mbar;
@@ -141,10 +152,10 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
   const double inv_bp = 1.0 / b, inv_bs = 1.0 / (b + alpha);  // pore / solid divisors of pure.py:61
-  const int64_t n = (int64_t)N * N * N;
+  const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   if (t == 0) {
     mbar_init(&mbar);
-    if ((int)blockIdx.x < NT) rs_issue<N>(blockIdx.x, B, st, sst, sx, sxn, sh, &mbar);
+    if ((int)blockIdx.x < NT) rs_issue<N, SL>(blockIdx.x, B, st, sst, sx, sxn, sh, &mbar);
   }
   __syncthreads();
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -152,8 +163,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
     const int64_t row0 = (int64_t)(tile % TPC) * R;
-    double2* XR = B.XR + (size_t)c * N * N * H;
-    double2* XRn = B.XRn + (size_t)c * N * N;
+    double2* XR = B.XR + (size_t)c * (SL ? B.l0 : N) * N * H;
+    double2* XRn = B.XRn + (size_t)c * (SL ? B.l0 : N) * N;
     mbar_wait(&mbar, phase);
     // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
     for (int idx = t; idx < NP * H; idx += T) {
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     }
     __syncthreads();
     // staged inputs consumed: prefetch the next tile while this one finishes
-    if (t == 0 && tile + (int)gridDim.x < NT) rs_issue<N>(tile + gridDim.x, B, st, sst, sx, sxn, sh, &mbar);
+    if (t == 0 && tile + (int)gridDim.x < NT) rs_issue<N, SL>(tile + gridDim.x, B, st, sst, sx, sxn, sh, &mbar);
     fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
     __syncthreads();
     // (3) separate the two real transforms of each row pair, store X-space rows of R
@@ -231,13 +242,13 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
 // RS-fix: X-space of u~' (row FFTs of the state), needed by MF only in the
 // iterations where residual balancing changed b (ctrl->db != 0); a no-op
 // otherwise.  Persistent, TMA bulk loads, same tiling as RS.
-template <int N>
+template <int N, bool SL>
 __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __restrict__ ut, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  constexpr int TPC = N * N / R;
-  constexpr int NT = 3 * TPC;
+  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int NT = 3 * TPC;
   if (ctrl->done || ctrl->db == 0.0) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   __shared__ uint64_t mbar;
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   double* sst = (double*)(sraw + K::TW + K::INV);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
-  const int64_t n = (int64_t)N * N * N;
+  const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   auto issue = [&](int tile) {
     const int c = tile / TPC;
     const int64_t row0 = (int64_t)(tile % TPC) * R;
@@ -263,8 +274,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
     const int64_t row0 = (int64_t)(tile % TPC) * R;
-    double2* XU = B.XU + (size_t)c * N * N * H;
-    double2* XUn = B.XUn + (size_t)c * N * N;
+    double2* XU = B.XU + (size_t)c * (SL ? B.l0 : N) * N * H;
+    double2* XUn = B.XUn + (size_t)c * (SL ? B.l0 : N) * N;
     mbar_wait(&mbar, phase);
     for (int v = t; v < V; v += T) {
       const int row = v / N, col = v % N;
@@ -320,16 +331,16 @@ struct RSC {
 
 // o0 / o1 = compact offsets of the tile's first row and of the row after it
 // (loaded by the caller one tile ahead so the issue does not wait on them)
-template <int N>
+template <int N, bool SL>
 __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& st, const Compact& cp, double* su,
                                           double* sc, double2* sx, double2* sxn, uint8_t* sh, uint64_t* mbar,
                                           uint32_t* ro_slot, const uint32_t* ro) {
   using K = RS2<N>;
   using C = Cfg<N>;
-  constexpr int TPC = N * N / K::R;
+  const int TPC = (SL ? B.l0 : N) * N / K::R;
   const int c = tile / TPC;
   const int64_t row0 = (int64_t)(tile % TPC) * K::R;
-  const int64_t n = (int64_t)N * N * N;
+  const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   constexpr int R = K::R;
   const uint32_t o0 = ro[0];
   const uint32_t cb = sizeof(double) * (ro[R] - o0);
@@ -337,8 +348,8 @@ __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& 
   fence_async_smem();
   mbar_expect(mbar, (uint32_t)(sizeof(double) * K::V + K::XM + K::XN + K::HB) + 3 * cb);
   bulk_load(su, st.u + (int64_t)c * n + row0 * N, sizeof(double) * K::V, mbar);
-  bulk_load(sx, B.XU + ((int64_t)c * N * N + row0) * C::H, (uint32_t)K::XM, mbar);
-  bulk_load(sxn, B.XUn + (int64_t)c * N * N + row0, (uint32_t)K::XN, mbar);
+  bulk_load(sx, B.XU + ((int64_t)c * (SL ? B.l0 : N) * N + row0) * C::H, (uint32_t)K::XM, mbar);
+  bulk_load(sxn, B.XUn + (int64_t)c * (SL ? B.l0 : N) * N + row0, (uint32_t)K::XN, mbar);
   bulk_load(sh, st.H + row0 * N, (uint32_t)K::HB, mbar);
   if (cb) {
     const int64_t base = (int64_t)c * cp.ns + o0;
@@ -369,13 +380,13 @@ __device__ __forceinline__ int seg_base(const uint8_t* seg_bytes, uint32_t row_o
   return (int)row_off_minus_o0 + incl - cnt;
 }
 
-template <int N>
+template <int N, bool SL>
 __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_compact(Bufs B, State st, Compact cp, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  constexpr int TPC = N * N / R;
-  constexpr int NT = 3 * TPC;
+  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int NT = 3 * TPC;
   constexpr int SPR = N / 32;  // 32-voxel segments per row
   const int CS = cp.cs;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
@@ -395,7 +406,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
   const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
-  const int64_t n = (int64_t)N * N * N;
+  const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   uint32_t ro[R + 1];
   auto offs = [&](int tl) {
     const int64_t r0 = (int64_t)(tl % TPC) * R;
@@ -406,7 +417,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     mbar_init(&mbar);
     if ((int)blockIdx.x < NT) {
       offs(blockIdx.x);
-      rsc_issue<N>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[0], ro);
+      rsc_issue<N, SL>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[0], ro);
     }
   }
   __syncthreads();
@@ -415,8 +426,8 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
     const int64_t row0 = (int64_t)(tile % TPC) * R;
-    double2* XR = B.XR + (size_t)c * N * N * H;
-    double2* XRn = B.XRn + (size_t)c * N * N;
+    double2* XR = B.XR + (size_t)c * (SL ? B.l0 : N) * N * H;
+    double2* XRn = B.XRn + (size_t)c * (SL ? B.l0 : N) * N;
     const bool has_next = tile + (int)gridDim.x < NT;
     if (t == 0 && has_next) offs(tile + gridDim.x);  // next tile's row offsets, loaded early
     mbar_wait(&mbar, phase);
@@ -478,7 +489,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     }
     __syncthreads();
     if (t == 0 && has_next)
-      rsc_issue<N>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[phase ^ 1u], ro);
+      rsc_issue<N, SL>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[phase ^ 1u], ro);
     fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
     __syncthreads();
     for (int idx = t; idx < NP * H; idx += T) {
@@ -500,15 +511,15 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
 }
 
 // RS-fix on the compact path: u~' rows = u' on pore voxels, the compact u~ on solid ones.
-template <int N>
+template <int N, bool SL>
 __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const double* __restrict__ u,
                                                              const uint8_t* __restrict__ Hs, Compact cp,
                                                              const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  constexpr int TPC = N * N / R;
-  constexpr int NT = 3 * TPC;
+  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int NT = 3 * TPC;
   constexpr int SPR = N / 32;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
   if (ctrl->done || ctrl->db == 0.0) return;
@@ -517,7 +528,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   double2* SF = (double2*)(sraw + K::TW);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
-  const int64_t n = (int64_t)N * N * N;
+  const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x) {
     const int c = tile / TPC;
     const int64_t row0 = (int64_t)(tile % TPC) * R;
@@ -536,8 +547,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
     __syncthreads();
     fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
     __syncthreads();
-    double2* XU = B.XU + (size_t)c * N * N * H;
-    double2* XUn = B.XUn + (size_t)c * N * N;
+    double2* XU = B.XU + (size_t)c * (SL ? B.l0 : N) * N * H;
+    double2* XUn = B.XUn + (size_t)c * (SL ? B.l0 : N) * N;
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
       const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
@@ -555,9 +566,9 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
 // ---- compact layout setup / teardown (warp per row of N voxels)
 // largest padded solid count of any RS tile -> mx (zeroed by the caller)
 template <int N>
-__global__ void k_tile_max(const uint32_t* __restrict__ off, uint32_t* __restrict__ mx) {
+__global__ void k_tile_max(const uint32_t* __restrict__ off, uint32_t* __restrict__ mx, int64_t rows) {
   constexpr int R = RS2<N>::R;
-  const int64_t tiles = (int64_t)N * N / R;
+  const int64_t tiles = rows / R;
   uint32_t m = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tiles; t += (int64_t)gridDim.x * blockDim.x)
     m = max(m, off[(t + 1) * R] - off[t * R]);
@@ -567,9 +578,8 @@ __global__ void k_tile_max(const uint32_t* __restrict__ off, uint32_t* __restric
 }
 
 template <int N>
-__global__ void k_row_counts(const uint8_t* __restrict__ Hs, uint32_t* __restrict__ cnt) {
+__global__ void k_row_counts(const uint8_t* __restrict__ Hs, uint32_t* __restrict__ cnt, int64_t rows) {
   const int lane = threadIdx.x & 31;
-  const int64_t rows = (int64_t)N * N;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     int c = 0;
@@ -610,9 +620,9 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt,
 // with pore u~ = u, a = 0 and lam left untouched.
 template <int N>
 __global__ void k_compact_move(const uint8_t* __restrict__ Hs, Compact cp, double* ut, double* a, double* lam,
-                               const double* __restrict__ u, int dir) {
+                               const double* __restrict__ u, int dir, int64_t rows) {
   const int lane = threadIdx.x & 31;
-  const int64_t rows = (int64_t)N * N, n = rows * N;
+  const int64_t n = rows * N;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < 3 * rows;
        r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int c = (int)(r / rows);
@@ -702,7 +712,7 @@ struct M2 {
   static constexpr size_t BYTES_FWD = sizeof(double2) * C::TWN + SEQ;
 };
 
-template <int N, bool INV>
+template <int N, bool INV, bool SL>
 __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = M2<N>;
@@ -712,20 +722,33 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   double2* tw = smem;
   double2* S = smem + Cfg<N>::TWN;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  const int c = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
-  const bool nyq = tile >= N * NCH;
-  const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
-  const int i0b = nyq ? (tile - N * NCH) * CM : 0;
+  const int l0 = (SL ? B.l0 : N), l1 = (SL ? B.l1 : N), s1 = (SL ? B.s1 : Cfg<N>::LOGN);
+  const int TPC = l0 * NCH + l0 / CM;  // tiles per component over this x-slab
+  const int c = blockIdx.x / TPC, tile = blockIdx.x % TPC;
+  const bool nyq = tile >= l0 * NCH;
+  const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;  // i0: local plane
+  const int i0b = nyq ? (tile - l0 * NCH) * CM : 0;
+  // X (x-slab rows [c][l0 N][H], Nyquist [c][l0 N]); e = k1 (MI out / MF in) or i1
   auto off_of = [&](int e, int q) -> size_t {
-    return nyq ? (size_t)(c * N + i0b + q) * N + e : ((size_t)(c * N + i0) * N + e) * H + ch * CM + q;
+    return nyq ? (size_t)(c * l0 + i0b + q) * N + e : ((size_t)(c * l0 + i0) * N + e) * H + ch * CM + q;
+  };
+  // Y in the x-slab exchange layout [r][i0][c][k1 - r l1][k2], r = k1 / l1 (see Bufs)
+  auto yoff_of = [&](int e, int q) -> size_t {
+    const int r = e >> s1, kl = e & (l1 - 1);
+    return nyq ? ((size_t)((r * l0 + i0b + q) * 3 + c)) * l1 + kl
+               : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
   // element mapping: main tiles walk (e, q) with q fastest (contiguous columns);
   // Nyquist tiles walk (q, e) with e fastest (contiguous rows).
   for (int idx = t; idx < N * CM; idx += T) {
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
-    const size_t o = off_of(e, q);
-    if (INV) cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
-    else cp16(S + q * SS + C::pad(e), nyq ? B.XRn + o : B.XR + o);
+    if (INV) {
+      const size_t o = yoff_of(e, q);
+      cp16(S + q * SS + C::pad(e), nyq ? B.Yxn + o : B.Yx + o);
+    } else {
+      const size_t o = off_of(e, q);
+      cp16(S + q * SS + C::pad(e), nyq ? B.XRn + o : B.XR + o);
+    }
   }
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   cp_commit_wait_all();
@@ -747,11 +770,12 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   __syncthreads();
   for (int idx = t; idx < N * CM; idx += T) {
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
-    const size_t o = off_of(e, q);
     const double2 v = S[q * SS + C::pad(e)];
     if (!INV) {
-      if (nyq) B.Yn[o] = v; else B.Y[o] = v;
+      const size_t o = yoff_of(e, q);
+      if (nyq) B.Yxn[o] = v; else B.Yx[o] = v;
     } else {
+      const size_t o = off_of(e, q);
       if (nyq) B.XUn[o] = v; else B.XU[o] = v;
     }
   }
@@ -770,7 +794,7 @@ struct SpecArgs {
 // spectral step reads and writes them fully coalesced, prefetched into
 // registers before the forward FFTs.
 
-template <int N>
+template <int N, bool SL>
 __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
   using C = Cfg<N>;
   using K = PK2<N>;
@@ -782,11 +806,13 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const double beta = ctrl->beta, b = ctrl->b;
   const int tile = blockIdx.x;
-  const bool nyq = tile >= N * NCH;
-  const int k1 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
-  const int k1b = nyq ? (tile - N * NCH) * CP : 0;
+  const int l1 = (SL ? B.l1 : N);
+  const bool nyq = tile >= l1 * NCH;
+  const int k1 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;  // k1: local to the y-slab
+  const int k1b = nyq ? (tile - l1 * NCH) * CP : 0;
+  // Y in the y-slab exchange layout [i0][c][k1 - k1off][k2] (see Bufs)
   auto yoff = [&](int c, int i0, int q) -> size_t {
-    return nyq ? (size_t)(c * N + i0) * N + k1b + q : ((size_t)(c * N + i0) * N + k1) * H + ch * CP + q;
+    return nyq ? (size_t)(i0 * 3 + c) * l1 + k1b + q : ((size_t)(c * N + i0) * l1 + k1) * H + ch * CP + q;
   };
   for (int idx = t; idx < 3 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
@@ -820,7 +846,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   for (int j = 0; j < K::MPT; ++j) {
     const int m = t + T * j, q = m / N, k0 = m % N;
     if (m >= CP * N) break;
-    const int kk1 = nyq ? k1b + q : k1, k2 = nyq ? H : ch * CP + q;
+    const int kk1 = (SL ? B.k1off : 0) + (nyq ? k1b + q : k1), k2 = nyq ? H : ch * CP + q;  // global k1
     const int idx3[3] = {k0, kk1, k2};
     double kc[3];
     double L = 0.0, ksq = 0.0;
@@ -914,25 +940,22 @@ __global__ void k_tilemajor(const double2* __restrict__ nat, double2* __restrict
 }
 
 // ------------------------------------------------------------------ layout conversion (setup / teardown)
-// natural [rows][N/2+1] <-> fused [rows][N/2] + nyq [rows]
-__global__ void k_split(int64_t rows, int N, const double2* __restrict__ src, double2* __restrict__ main,
-                        double2* __restrict__ nyqv) {
-  const int H = N / 2, W = H + 1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * W; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / W;
-    const int k = (int)(i % W);
-    if (k < H) main[r * H + k] = src[i]; else nyqv[r] = src[i];
-  }
-}
-
-__global__ void k_merge(int64_t rows, int N, const double2* __restrict__ main, const double2* __restrict__ nyqv,
-                        double2* __restrict__ dst, double scale) {
-  const int H = N / 2, W = H + 1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * W; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / W;
-    const int k = (int)(i % W);
-    const double2 v = k < H ? main[r * H + k] : nyqv[r];
-    dst[i] = make_double2(v.x * scale, v.y * scale);
+// rows of the axes-(1, 2) transform, natural [c][i0][k1][N/2+1] over this x-slab's
+// l0 planes -> Y in the x-slab exchange layout (Yx, Yxn; see Bufs)
+template <int N>
+__global__ void k_split_yx(const double2* __restrict__ src, Bufs B) {
+  constexpr int H = N / 2, W = H + 1;
+  const int l0 = B.l0, l1 = B.l1, s1 = B.s1;
+  const int64_t total = (int64_t)3 * l0 * N * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k2 = (int)(i % W);
+    int64_t rest = i / W;
+    const int k1 = (int)(rest % N);
+    rest /= N;
+    const int i0 = (int)(rest % l0), c = (int)(rest / l0);
+    const int r = k1 >> s1, kl = k1 & (l1 - 1);
+    if (k2 < H) B.Yx[(((int64_t)(c * (N >> s1) + r) * l0 + i0) * l1 + kl) * H + k2] = src[i];
+    else B.Yxn[((int64_t)(r * l0 + i0) * 3 + c) * l1 + kl] = src[i];
   }
 }
 
@@ -981,21 +1004,21 @@ static size_t smem_pk() { return fz::PK2<N>::BYTES; }
 
 template <int N>
 static int set_attrs(FusedPlan* f) {
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
   // persistent RS grids: one wave of resident blocks.  The full-layout kernel is
   // capped at 3 per SM: it streams 4 KB/voxel-row-tile at ~93% of HBM peak and a
   // 4th block only adds contention (256^3: 0.697 ms at 4/SM vs 0.662 ms at 3/SM).
   auto wave = [](int o, int cap) { return (o < 1 ? 1 : (o > cap ? cap : o)) * kSMs; };
   int o1 = 0, o2 = 0;
-  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, fz::k_rs<N>, fz::RS2<N>::T, smem_rs<N>()));
-  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N>, fz::RS2<N>::T, smem_rsc<N>()));
+  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, fz::k_rs<N, false>, fz::RS2<N>::T, smem_rs<N>()));
+  PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N, false>, fz::RS2<N>::T, smem_rsc<N>()));
   f->nb_full = wave(o1, 3);
   f->nb_compact = wave(o2, kRsMaxBlocks / kSMs);
   f->nb_rs = f->nb_full;
@@ -1031,6 +1054,14 @@ int fused_ensure(pf_plan* p) {
   f->b.XRn = take(3 * nyq1);
   f->b.Yn = take(3 * nyq1);
   f->b.tw = take(N);
+  // single GPU: the whole cube is one slab; x- and y-slab Y layouts coincide
+  f->b.l0 = N;
+  f->b.l1 = N;
+  f->b.s1 = 0;
+  while ((1 << f->b.s1) < N) ++f->b.s1;
+  f->b.k1off = 0;
+  f->b.Yx = f->b.Y;
+  f->b.Yxn = f->b.Yn;
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
   std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
@@ -1108,7 +1139,7 @@ static fz::Compact compact_of(FusedPlan* f) {
 
 template <int N>
 static int compact_setup_t(pf_plan* p, FusedPlan* f) {
-  const int64_t rows = (int64_t)N * N, n = rows * N;
+  const int64_t rows = (int64_t)f->b.l0 * N, n = rows * N;
   // eligibility (a = 0 on pore voxels: cold starts and states this path produced)
   // and the constant pore part of |lam'|^2
   const int nb = blocks_for(3 * n);
@@ -1125,10 +1156,11 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
     PF_CK_CUDA(cudaMalloc(&f->c_cnt, sizeof(uint32_t) * rows));
     PF_CK_CUDA(cudaMalloc(&f->c_off, sizeof(uint32_t) * (rows + 2)));  // + the tile max
   }
-  fz::k_row_counts<N><<<blocks_for(rows * 32), kThreads, 0, p->work>>>(p->s_solid, f->c_cnt);
+  fz::k_row_counts<N><<<blocks_for(rows * 32), kThreads, 0, p->work>>>(p->s_solid, f->c_cnt, rows);
   fz::k_scan<<<1, 1024, 0, p->work>>>(f->c_cnt, f->c_off, rows);
   PF_CK_CUDA(cudaMemsetAsync(f->c_off + rows + 1, 0, sizeof(uint32_t), p->work));
-  fz::k_tile_max<N><<<blocks_for(rows / fz::RS2<N>::R), kThreads, 0, p->work>>>(f->c_off, f->c_off + rows + 1);
+  fz::k_tile_max<N><<<blocks_for(rows / fz::RS2<N>::R), kThreads, 0, p->work>>>(f->c_off, f->c_off + rows + 1,
+                                                                                  rows);
   PF_CK_CUDA(cudaGetLastError());
   uint32_t nm[2] = {0, 0};
   PF_CK_CUDA(cudaMemcpyAsync(p->h_small, f->c_off + rows, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, p->work));
@@ -1141,7 +1173,7 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
   if (f->c_cs < 16) f->c_cs = 16;
   {
     int o = 0;
-    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fz::k_rs_compact<N>, fz::RS2<N>::T,
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fz::k_rs_compact<N, false>, fz::RS2<N>::T,
                                                              fz::RSC<N>::bytes(f->c_cs)));
     f->nb_compact = (o < 1 ? 1 : (o > kRsMaxBlocks / kSMs ? kRsMaxBlocks / kSMs : o)) * kSMs;
     f->nb_rs = f->nb_compact;
@@ -1154,7 +1186,7 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
     f->c_cap = need;
   }
   fz::k_compact_move<N><<<blocks_for(3 * rows * 32), kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut,
-                                                                             p->s_a, p->s_lam, p->s_u, 0);
+                                                                             p->s_a, p->s_lam, p->s_u, 0, rows);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
@@ -1175,8 +1207,13 @@ int fused_setup(pf_plan* p) {
   // Y-space R~ = FFT_{2,1}(b u~ - a)
   PF_CK(stokes_form_r(p, p->realB));
   PF_CK_FFT(cufftExecD2Z(f->plan2d, (cufftDoubleReal*)p->realB, (cufftDoubleComplex*)p->specA));
-  fz::k_split<<<grid, kThreads, 0, p->work>>>(3 * NN, N, p->specA, f->b.Y, f->b.Yn);
+  switch (N) {
+    case 64: fz::k_split_yx<64><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+    case 128: fz::k_split_yx<128><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+    default: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+  }
   PF_CK_CUDA(cudaGetLastError());
+  (void)NN;
   (void)n;
   switch (N) {
     case 64: return compact_setup_t<64>(p, f);
@@ -1189,15 +1226,16 @@ int fused_setup(pf_plan* p) {
 int fused_finish(pf_plan* p) {
   FusedPlan* f = fp_of(p);
   const int N = f->N;
-  const int64_t NN = (int64_t)N * N;
+  const int64_t NN = (int64_t)N * N, rows = (int64_t)f->b.l0 * N;
   PF_CK(to_tilemajor(N, f->b.Q, p->specB, p->g.inv_n, false, p->work));
   PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
   if (f->compact) {  // materialise u~, a, lam (pore: u~ = u, a = 0, lam unchanged)
-    const int nb = blocks_for(3 * NN * 32);
+    const int nb = blocks_for(3 * rows * 32);
+    (void)NN;
     switch (N) {
-      case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
-      case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
-      default: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+      case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      default: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
     }
     PF_CK_CUDA(cudaGetLastError());
   }
@@ -1223,32 +1261,34 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
     return PF_OK;
   };
   PF_CK(mark(0));
-  fz::k_pk<N><<<fz::PK2<N>::TILES, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
+  const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
+  const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
+  fz::k_pk<N, false><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(1));
-  fz::k_maxis<N, true><<<fz::M2<N>::TILES, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
+  fz::k_maxis<N, true, false><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
   if (f->compact) {
-    fz::k_rs_compact<N><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(f->b, st, compact_of(f),
+    fz::k_rs_compact<N, false><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(f->b, st, compact_of(f),
                                                                                           p->ctrl);
   } else {
-    fz::k_rs<N><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
+    fz::k_rs<N, false><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
   }
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
-  k_stokes_finalize_launch(p, f->b.part_rs, f->nb_rs, f->b.part_pk, fz::PK2<N>::TILES);
+  k_stokes_finalize_launch(p, f->b.part_rs, f->nb_rs, f->b.part_pk, pk_tiles);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
   if (f->compact) {
-    fz::k_rsfix_compact<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_u, p->s_solid,
+    fz::k_rsfix_compact<N, false><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_u, p->s_solid,
                                                                                    compact_of(f), p->ctrl);
   } else {
-    fz::k_rsfix<N><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
+    fz::k_rsfix<N, false><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
   }
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(5));
-  fz::k_maxis<N, false><<<fz::M2<N>::TILES, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
+  fz::k_maxis<N, false, false><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(6));
   return PF_OK;
