@@ -459,8 +459,10 @@ def run_ensemble_workload(args):
 
 def run_slab_workload(args):
     """Secondary line: BASELINE cfg 5 — ONE random-packing cell slab-decomposed over
-    the ranks (x-slabs; two all_to_alls of 3 half-spectrum components and one
-    9-double all_reduce per iteration).  Strong scaling: total work fixed."""
+    the ranks (x-slabs; two exchanges of 3 half-spectrum components and one
+    9-double all_reduce per iteration).  The fused slab pipeline where it applies
+    (cubic 64/128/256, power-of-two ranks), else the cuFFT one.  Strong scaling:
+    total work fixed."""
     import torch
 
     import paper_2312_15554_b200 as pf
@@ -484,7 +486,9 @@ def run_slab_workload(args):
     st = {k: torch.zeros(3 * L, dtype=torch.float64, device=dev) for k in ("u", "u_tilde", "a", "lam")}
     st["q"] = torch.zeros(L, dtype=torch.float64, device=dev)
     solid = torch.as_tensor(np.ascontiguousarray(ind.values[lo:hi])).reshape(-1).to(dev)
-    sol = S.SlabStokes(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st)
+    fused = be.fused_sizes()[0] > 0 and not args.slab_cufft
+    cls = S.FusedSlabStokes if fused else S.SlabStokes
+    sol = cls(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st)
     sol.begin()
     sol.iterate(args.warmup, poll=False)
     torch.cuda.synchronize()
@@ -507,7 +511,8 @@ def run_slab_workload(args):
         print(json.dumps({"metric": "Stokes ALM voxel-iters/s, one slab-decomposed cell (secondary, cfg 5)",
                           "value": value, "unit": UNIT, "n_gpus": world, "ms_per_step": ms / args.steps,
                           "steps": args.steps, "warmup": args.warmup, "scaling": "strong", "dtype": "f64",
-                          "pipeline": "slab (cuFFT local transforms + all_to_all)",
+                          "pipeline": ("slab-fused (fused passes, Y all_to_all between PK and the axis-1 passes)"
+                                       if fused else "slab (cuFFT local transforms + all_to_all)"),
                           "config": {"workload": f"slab_random_packing_{n}^3", "ranks": world}}), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -526,6 +531,7 @@ def main():
     ap.add_argument("--workload", default="stokes", choices=("stokes", "transport", "ensemble", "slab"),
                     help="stokes = the headline metric; transport / ensemble = secondary lines")
     ap.add_argument("--cells", type=int, default=8, help="cells per GPU for --workload ensemble")
+    ap.add_argument("--slab-cufft", action="store_true", help="--workload slab: the cuFFT slab pipeline")
     args = ap.parse_args()
     if args.workload == "transport":
         return run_transport_workload(args)

@@ -151,6 +151,27 @@ int pf_slab_form_r(pf_plan* plan, double* R, int gated);
 int pf_slab_scale(pf_plan* plan, const double* src, double* dst, int64_t count, double scale);
 int pf_slab_read(pf_plan* plan, pf_stokes_result* result);
 
+/* Fused slab pipeline (cubic N in {64, 128, 256}, P a power of two, slabs of
+ * whole tiles; pf_slab_fused_sizes reports 0 when unsupported).  Per iteration:
+ * pf_slab_fused_pk (axis 0 + Green's operator on the y-slab Y) -> exchange
+ * Y y-slab -> x-slab -> pf_slab_fused_rs (axis-1 inverse, rows + local step,
+ * the rank's 9 residual sums) -> all-reduce -> pf_slab_finalize ->
+ * pf_slab_fused_mf (axis-1 forward) -> exchange Y x-slab -> y-slab.  Y buffers
+ * (caller-owned, complex as double*): main arrays of y_main elements with one
+ * all_to_all of equal splits per component (y-slab [c][N][N/P][N/2] <-> x-slab
+ * [c][P][N/P][N/P][N/2]), Nyquist arrays of y_nyq elements exchanged in one
+ * (y-slab [N][3][N/P] <-> x-slab [P][N/P][3][N/P]).  Setup takes the T-layout
+ * Q^ / D^ of pf_slab_setup and a real scratch of 3*L0*N*N for R; end returns Q^
+ * in T layout (unscaled) and materialises u~, a, lam.  Replaces the per-iteration
+ * pf_slab_spectral / transforms / pf_slab_local / pf_slab_form_r sequence. */
+int pf_slab_fused_sizes(pf_plan* plan, int64_t* y_main, int64_t* y_nyq);
+int pf_slab_fused_bind(pf_plan* plan, double* Yy, double* Yy_nyq, double* Yx, double* Yx_nyq);
+int pf_slab_fused_setup(pf_plan* plan, const double* Q_tspec, const double* D_tspec, double* R_scratch);
+int pf_slab_fused_pk(pf_plan* plan);
+int pf_slab_fused_rs(pf_plan* plan, double* totals9);
+int pf_slab_fused_mf(pf_plan* plan);
+int pf_slab_fused_end(pf_plan* plan, double* Q_tspec);
+
 /* ------------------------------------------------------------------------
  * Transport — replaces poreflow.transport.solve_transport
  * (transport.py:180-268) including build_coefficients (101-128).

@@ -106,6 +106,13 @@ SIGNATURES = {
     "pf_slab_form_r": [_P, _P, ctypes.c_int],
     "pf_slab_scale": [_P, _P, _P, ctypes.c_int64, ctypes.c_double],
     "pf_slab_read": [_P, ctypes.POINTER(StokesResult)],
+    "pf_slab_fused_sizes": [_P, _I64P, _I64P],
+    "pf_slab_fused_bind": [_P, _P, _P, _P, _P],
+    "pf_slab_fused_setup": [_P, _P, _P, _P],
+    "pf_slab_fused_pk": [_P],
+    "pf_slab_fused_rs": [_P, _P],
+    "pf_slab_fused_mf": [_P],
+    "pf_slab_fused_end": [_P, _P],
     "pf_transport_solve": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_begin": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_iterate": [_P, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(TransportResult)],

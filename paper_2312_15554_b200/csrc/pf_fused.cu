@@ -918,22 +918,25 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
 
 // natural full spectrum [k0][k1][N/2+1] <-> PK tile-major [tile][q][k0]
 template <int N>
-__global__ void k_tilemajor(const double2* __restrict__ nat, double2* __restrict__ tm, double scale, int to_tm) {
+__global__ void k_tilemajor(const double2* __restrict__ nat, double2* __restrict__ tm, double scale, int to_tm,
+                            int l1) {
+  // natural (or slab T-layout) half spectrum [k0][k1 local < l1][N/2+1] <-> PK tile-major
   using K = PK2<N>;
   constexpr int H = N / 2, W = H + 1, CP = K::CP;
-  const int64_t total = (int64_t)K::TILES * CP * N;
+  const int tiles = l1 * K::NCH + l1 / CP;
+  const int64_t total = (int64_t)tiles * CP * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int tile = (int)(i / (CP * N));
     const int q = (int)((i / N) % CP), k0 = (int)(i % N);
     int k1, k2;
-    if (tile < N * K::NCH) {
+    if (tile < l1 * K::NCH) {
       k1 = tile / K::NCH;
       k2 = (tile % K::NCH) * CP + q;
     } else {
-      k1 = (tile - N * K::NCH) * CP + q;
+      k1 = (tile - l1 * K::NCH) * CP + q;
       k2 = H;
     }
-    const int64_t o = ((int64_t)k0 * N + k1) * W + k2;
+    const int64_t o = ((int64_t)k0 * l1 + k1) * W + k2;
     if (to_tm) tm[i] = make_double2(nat[o].x * scale, nat[o].y * scale);
     else tm[o] = make_double2(nat[i].x * scale, nat[i].y * scale);  // here nat = tile-major src, tm = natural dst
   }
@@ -959,6 +962,21 @@ __global__ void k_split_yx(const double2* __restrict__ src, Bufs B) {
   }
 }
 
+// slab: this rank's 9 residual sums (RS 6, PK 3) -> totals, with the pore part of
+// |lam|^2 of the compact layout added locally (totals are then all-reduced)
+__global__ void __launch_bounds__(kFinalizeThreads) k_fslab_totals(const double* __restrict__ prs, int nrs,
+                                                                   const double* __restrict__ ppk, int npk,
+                                                                   double lam_pore, double* __restrict__ totals) {
+  double S[6], Q[3];
+  reduce_partials<6>(prs, nrs, S);
+  reduce_partials<3>(ppk, npk, Q);
+  if (threadIdx.x == 0) {
+    S[2] += lam_pore;
+    for (int k = 0; k < 6; ++k) totals[k] = S[k];
+    for (int k = 0; k < 3; ++k) totals[6 + k] = Q[k];
+  }
+}
+
 }  // namespace fz
 
 // ------------------------------------------------------------------ host
@@ -976,6 +994,12 @@ struct FusedPlan {
   int c_cs = 16;  // staging capacity per tile (Compact::cs)
   int compact = 0;
   int nb_rs = kSMs;              // persistent RS grid of the active path (full or compact)
+  // slab-decomposed use (fused_slab_*): Y buffers owned by the caller (exchanged
+  // between ranks), the pore part of |lam|^2 added to the local totals instead
+  int slab = 0;
+  double lam_pore = 0.0;
+  void* ws = nullptr;        // cuFFT work area of plan2d
+  double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
   int nb_full = kSMs, nb_compact = kSMs;
 };
 
@@ -1012,6 +1036,14 @@ static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
   PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_rsfix<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
+  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
   // persistent RS grids: one wave of resident blocks.  The full-layout kernel is
   // capped at 3 per SM: it streams 4 KB/voxel-row-tile at ~93% of HBM peak and a
   // 4th block only adds contention (256^3: 0.697 ms at 4/SM vs 0.662 ms at 3/SM).
@@ -1110,17 +1142,21 @@ void fused_free(pf_plan* p) {
   cudaFree(f->c_cnt);
   cudaFree(f->c_off);
   cudaFree(f->c_data);
+  cudaFree(f->ws);
+  cudaFree(f->spec);
   delete f;
   p->fused = nullptr;
 }
 
-static int to_tilemajor(int N, const double2* src, double2* dst, double scale, bool to_tm, cudaStream_t s) {
-  const int64_t total = (int64_t)N * N * (N / 2 + 1);
+static int to_tilemajor(int N, const double2* src, double2* dst, double scale, bool to_tm, cudaStream_t s,
+                        int l1 = 0) {
+  if (l1 == 0) l1 = N;
+  const int64_t total = (int64_t)N * l1 * (N / 2 + 1);
   const int nb = blocks_for(total);
   switch (N) {
-    case 64: fz::k_tilemajor<64><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
-    case 128: fz::k_tilemajor<128><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
-    default: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm); break;
+    case 64: fz::k_tilemajor<64><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
+    case 128: fz::k_tilemajor<128><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
+    default: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
@@ -1305,6 +1341,219 @@ int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {
     case 128: return enqueue_fused_t<128>(p, ev);
     default: return enqueue_fused_t<256>(p, ev);
   }
+}
+
+
+// ------------------------------------------------------------------ slab-decomposed fused pipeline
+// One cell over P ranks (slab.py FusedSlabStokes): rank r holds the x-slab of
+// the real state (l0 i0-planes) and of X, and the y-slab (l1 k1-planes from
+// k1off) of Q^, D^; Y lives in the two exchange-native layouts of Bufs, whose
+// buffers the caller owns and all-to-alls between PK and the axis-1 passes.
+static bool fslab_shape_ok(int N, int l0, int l1) {
+  if (N != 64 && N != 128 && N != 256) return false;
+  if (l0 <= 0 || l1 <= 0 || (l1 & (l1 - 1)) || N % l0 || N % l1) return false;
+  const int cm = N == 64 ? fz::M2<64>::CM : (N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM);
+  const int cp = N == 64 ? fz::PK2<64>::CP : (N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP);
+  return l0 % cm == 0 && l1 % cp == 0;
+}
+
+int fused_slab_supported(int N, int l0, int l1) { return fslab_shape_ok(N, l0, l1) ? 1 : 0; }
+
+int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, double2* Yyn, double2* Yx,
+                    double2* Yxn) {
+  if (!fslab_shape_ok(N, l0, l1)) {
+    set_error("fused slab needs N in {64, 128, 256}, a power-of-two rank count and slabs of whole tiles");
+    return PF_ERR_ARG;
+  }
+  if (p->fused) fused_free(p);
+  FusedPlan* f = new FusedPlan();
+  p->fused = f;
+  f->N = N;
+  f->slab = 1;
+  const size_t H = N / 2;
+  const size_t xm = (size_t)l0 * N * H, xn = (size_t)l0 * N;  // X per component
+  const size_t qd = (size_t)l1 * N * H + (size_t)l1 * N;      // Q^ / D^ (tile-major, y-slab)
+  const int pk_max = N == 64 ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : fz::PK2<256>::TILES);
+  const size_t elems = 6 * (xm + xn) + 2 * qd + N;
+  const size_t part = 6 * (size_t)kRsMaxBlocks + 3 * (size_t)pk_max;
+  f->bytes = elems * sizeof(double2) + part * sizeof(double);
+  PF_CK_CUDA(cudaMalloc(&f->mem, f->bytes));
+  double2* m = (double2*)f->mem;
+  auto take = [&](size_t n) {
+    double2* r = m;
+    m += n;
+    return r;
+  };
+  f->b.XU = take(3 * xm);
+  f->b.XR = take(3 * xm);
+  f->b.XUn = take(3 * xn);
+  f->b.XRn = take(3 * xn);
+  f->b.Q = take(qd);
+  f->b.D = take(qd);
+  f->b.tw = take(N);
+  f->b.part_rs = (double*)m;
+  f->b.part_pk = f->b.part_rs + 6 * (size_t)kRsMaxBlocks;
+  f->b.Y = Yy;
+  f->b.Yn = Yyn;
+  f->b.Yx = Yx;
+  f->b.Yxn = Yxn;
+  f->b.l0 = l0;
+  f->b.l1 = l1;
+  f->b.s1 = 0;
+  while ((1 << f->b.s1) < l1) ++f->b.s1;
+  f->b.k1off = k1off;
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
+  switch (N) {
+    case 64: fz::pass1_twiddles<64>(tw.data()); break;
+    case 128: fz::pass1_twiddles<128>(tw.data()); break;
+    default: fz::pass1_twiddles<256>(tw.data()); break;
+  }
+  PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+  // axes-(1, 2) transform of this slab's R at setup
+  size_t ws = 0;
+  long long dims2[2] = {N, N};
+  PF_CK_FFT(cufftCreate(&f->plan2d));
+  PF_CK_FFT(cufftSetAutoAllocation(f->plan2d, 0));
+  PF_CK_FFT(cufftMakePlanMany64(f->plan2d, 2, dims2, nullptr, 1, (long long)N * N, nullptr, 1,
+                                (long long)N * (H + 1), CUFFT_D2Z, 3LL * l0, &ws));
+  PF_CK_CUDA(cudaMalloc(&f->ws, ws > 0 ? ws : 256));
+  PF_CK_CUDA(cudaMalloc(&f->spec, sizeof(double2) * 3 * (size_t)l0 * N * (H + 1)));
+  PF_CK_FFT(cufftSetWorkArea(f->plan2d, f->ws));
+  PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
+  switch (N) {
+    case 64: PF_CK(set_attrs<64>(f)); break;
+    case 128: PF_CK(set_attrs<128>(f)); break;
+    default: PF_CK(set_attrs<256>(f)); break;
+  }
+  p->scratch_bytes += f->bytes + ws + sizeof(double2) * 3 * (size_t)l0 * N * (H + 1);
+  return PF_OK;
+}
+
+// Setup from the slab T-layout spectra Q^ = FFT(q) (gauge applied) and D^ =
+// i k . FFT(u) (pf_slab_setup), and the real R = b u~ - a of this slab (scratch R).
+int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R) {
+  FusedPlan* f = fp_of(p);
+  const int N = f->N;
+  PF_CK(to_tilemajor(N, Tq, f->b.Q, 1.0, true, p->work, f->b.l1));
+  PF_CK(to_tilemajor(N, Td, f->b.D, 1.0, true, p->work, f->b.l1));
+  PF_CK(stokes_form_r_gated(p, R, 0));
+  PF_CK_FFT(cufftExecD2Z(f->plan2d, (cufftDoubleReal*)R, (cufftDoubleComplex*)f->spec));
+  const int grid = blocks_for((int64_t)3 * f->b.l0 * N * (N / 2 + 1));
+  switch (N) {
+    case 64: fz::k_split_yx<64><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+    case 128: fz::k_split_yx<128><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+    default: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  switch (N) {
+    case 64: PF_CK(compact_setup_t<64>(p, f)); break;
+    case 128: PF_CK(compact_setup_t<128>(p, f)); break;
+    default: PF_CK(compact_setup_t<256>(p, f)); break;
+  }
+  f->lam_pore = p->sc.lam_pore_sq;  // local: enters the totals before the all-reduce
+  p->sc.lam_pore_sq = 0.0;
+  return PF_OK;
+}
+
+static fz::SpecArgs spec_args(pf_plan* p) {
+  fz::SpecArgs sa;
+  for (int i = 0; i < 3; ++i) {
+    sa.kap[i] = p->kap[i];
+    sa.ell[i] = p->ell[i];
+    sa.g[i] = p->sc.g[i];
+  }
+  sa.nu = p->sc.nu;
+  sa.inv_n = p->g.inv_n;
+  sa.dn = p->g.dn;
+  return sa;
+}
+
+template <int N>
+static int fslab_pk_t(pf_plan* p) {
+  FusedPlan* f = fp_of(p);
+  const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
+  fz::k_pk<N, true><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, spec_args(p), p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+template <int N>
+static int fslab_rs_t(pf_plan* p, double* totals) {
+  FusedPlan* f = fp_of(p);
+  fz::State st{p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid};
+  const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
+  const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
+  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  if (f->compact) {
+    fz::k_rs_compact<N, true><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(
+        f->b, st, compact_of(f), p->ctrl);
+  } else {
+    fz::k_rs<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  fz::k_fslab_totals<<<1, kFinalizeThreads, 0, p->work>>>(f->b.part_rs, f->nb_rs, f->b.part_pk, pk_tiles,
+                                                         f->lam_pore, totals);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+template <int N>
+static int fslab_mf_t(pf_plan* p) {
+  FusedPlan* f = fp_of(p);
+  const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
+  if (f->compact) {
+    fz::k_rsfix_compact<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_u, p->s_solid,
+                                                                                      compact_of(f), p->ctrl);
+  } else {
+    fz::k_rsfix<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+int fused_slab_pk(pf_plan* p) {
+  switch (fp_of(p)->N) {
+    case 64: return fslab_pk_t<64>(p);
+    case 128: return fslab_pk_t<128>(p);
+    default: return fslab_pk_t<256>(p);
+  }
+}
+
+int fused_slab_rs(pf_plan* p, double* totals) {
+  switch (fp_of(p)->N) {
+    case 64: return fslab_rs_t<64>(p, totals);
+    case 128: return fslab_rs_t<128>(p, totals);
+    default: return fslab_rs_t<256>(p, totals);
+  }
+}
+
+int fused_slab_mf(pf_plan* p) {
+  switch (fp_of(p)->N) {
+    case 64: return fslab_mf_t<64>(p);
+    case 128: return fslab_mf_t<128>(p);
+    default: return fslab_mf_t<256>(p);
+  }
+}
+
+// Q^ back to the slab T layout (unscaled) and the compact multipliers materialised.
+int fused_slab_end(pf_plan* p, double2* Tq) {
+  FusedPlan* f = fp_of(p);
+  const int N = f->N;
+  PF_CK(to_tilemajor(N, f->b.Q, Tq, 1.0, false, p->work, f->b.l1));
+  if (f->compact) {
+    const int64_t rows = (int64_t)f->b.l0 * N;
+    const int nb = blocks_for(3 * rows * 32);
+    switch (N) {
+      case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      default: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+    }
+    PF_CK_CUDA(cudaGetLastError());
+  }
+  return PF_OK;
 }
 
 }  // namespace pf

@@ -190,6 +190,15 @@ void fused_free(pf_plan* p);
 int fused_setup(pf_plan* p);
 int fused_finish(pf_plan* p);
 int enqueue_fused(pf_plan* p, cudaEvent_t* ev);
+// slab-decomposed fused pipeline (pf_fused.cu, driven by pf_slab_fused_*)
+int fused_slab_supported(int N, int l0, int l1);
+int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, double2* Yyn, double2* Yx,
+                    double2* Yxn);
+int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R);
+int fused_slab_pk(pf_plan* p);
+int fused_slab_rs(pf_plan* p, double* totals);
+int fused_slab_mf(pf_plan* p);
+int fused_slab_end(pf_plan* p, double2* Tq);
 int fused_is_compact(const pf_plan* p);
 // fused transport pipeline (pf_fused_transport.cu)
 int tfused_setup(pf_plan* p, bool warm);

@@ -369,4 +369,80 @@ int pf_slab_read(pf_plan* p, pf_stokes_result* res) {
   return PF_OK;
 }
 
+
+int pf_slab_fused_sizes(pf_plan* p, int64_t* y_main, int64_t* y_nyq) {
+  SlabPlan* s;
+  PF_CK(slab_checked(p, &s));
+  PF_ARG(y_main && y_nyq, "null argument");
+  const bool cubic = s->N0 == s->N1 && s->N1 == s->N2;
+  const bool ok = cubic && (s->P & (s->P - 1)) == 0 && fused_slab_supported(s->N0, s->L0, s->L1);
+  *y_main = ok ? 3 * (int64_t)s->N0 * s->L1 * (s->N2 / 2) : 0;
+  *y_nyq = ok ? 3 * (int64_t)s->N0 * s->L1 : 0;
+  return PF_OK;
+}
+
+int pf_slab_fused_bind(pf_plan* p, double* Yy, double* Yyn, double* Yx, double* Yxn) {
+  SlabPlan* s;
+  PF_CK(slab_checked(p, &s));
+  PF_ARG(Yy && Yyn && Yx && Yxn, "null argument");
+  PF_ARG(s->N0 == s->N1 && s->N1 == s->N2 && (s->P & (s->P - 1)) == 0,
+         "fused slab needs a cubic grid and a power-of-two rank count");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_bind(p, s->N0, s->L0, s->L1, s->rank * s->L1, (double2*)Yy, (double2*)Yyn, (double2*)Yx,
+                        (double2*)Yxn));
+  return leave(p);
+}
+
+static int fslab_checked(pf_plan* p, SlabPlan** s) {
+  PF_CK(slab_checked(p, s));
+  if (!p->fused) {
+    set_error("pf_slab_fused_* before pf_slab_fused_bind");
+    return PF_ERR_STATE;
+  }
+  return PF_OK;
+}
+
+int pf_slab_fused_setup(pf_plan* p, const double* Tq, const double* Td, double* R) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(Tq && Td && R, "null argument");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_setup(p, (const double2*)Tq, (const double2*)Td, R));
+  return leave(p);
+}
+
+int pf_slab_fused_pk(pf_plan* p) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_CK(enter(p));
+  PF_CK(fused_slab_pk(p));
+  return leave(p);
+}
+
+int pf_slab_fused_rs(pf_plan* p, double* totals) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(totals, "null argument");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_rs(p, totals));
+  return leave(p);
+}
+
+int pf_slab_fused_mf(pf_plan* p) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_CK(enter(p));
+  PF_CK(fused_slab_mf(p));
+  return leave(p);
+}
+
+int pf_slab_fused_end(pf_plan* p, double* Tq) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(Tq, "null argument");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_end(p, (double2*)Tq));
+  return leave(p);
+}
+
 }  // extern "C"

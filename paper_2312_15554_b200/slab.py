@@ -108,6 +108,30 @@ class DeviceSlabBackend:
     def scale(self, src, dst, count, s):
         N.check(self.lib.pf_slab_scale(self.h, self._p(src), self._p(dst), int(count), float(s)))
 
+    # fused slab pipeline (pf_slab_fused_*)
+    def fused_sizes(self) -> tuple:
+        m, q = ctypes.c_int64(), ctypes.c_int64()
+        N.check(self.lib.pf_slab_fused_sizes(self.h, ctypes.byref(m), ctypes.byref(q)))
+        return int(m.value), int(q.value)
+
+    def fused_bind(self, Yy, Yyn, Yx, Yxn):
+        N.check(self.lib.pf_slab_fused_bind(self.h, self._p(Yy), self._p(Yyn), self._p(Yx), self._p(Yxn)))
+
+    def fused_setup(self, Q, D, R):
+        N.check(self.lib.pf_slab_fused_setup(self.h, self._p(Q), self._p(D), self._p(R)))
+
+    def fused_pk(self):
+        N.check(self.lib.pf_slab_fused_pk(self.h))
+
+    def fused_rs(self, totals):
+        N.check(self.lib.pf_slab_fused_rs(self.h, self._p(totals)))
+
+    def fused_mf(self):
+        N.check(self.lib.pf_slab_fused_mf(self.h))
+
+    def fused_end(self, Q):
+        N.check(self.lib.pf_slab_fused_end(self.h, self._p(Q)))
+
     def read(self) -> dict:
         r = N.StokesResult()
         N.check(self.lib.pf_slab_read(self.h, ctypes.byref(r)))
@@ -229,8 +253,78 @@ class SlabStokes:
         return self.end()
 
 
+class FusedSlabStokes(SlabStokes):
+    """The same ADMM loop on the fused passes (csrc/pf_fused.cu): per iteration PK
+    on this rank's y-slab of Y, an all-to-all of Y to the x-slab, the axis-1
+    inverse + rows + local step (MI, RS), the 9-double all-reduce and finalize,
+    the axis-1 forward (MF), and the all-to-all back.  Y is exchanged in the
+    exchange-native layouts of ``pf_slab_fused_*`` (contiguous equal splits:
+    one all_to_all per component plus one for the Nyquist columns), so there is
+    no packing pass; at P = 1 both layouts coincide and nothing moves."""
+
+    def __init__(self, backend, dims, cfg, penalties, solid_local, state, group=None, poll_every: int = 8,
+                 comm=None):
+        super().__init__(backend, dims, cfg, penalties, solid_local, state, group, poll_every, comm)
+        be = backend
+        ym, yn = be.fused_sizes()
+        if ym == 0:
+            raise ValueError("fused slab pipeline unsupported for this grid / rank count")
+        self.ym, self.yn = ym, yn
+        self.Yy, self.Yyn = be.alloc_complex(ym), be.alloc_complex(yn)
+        if self.world > 1:
+            self.Yx, self.Yxn = be.alloc_complex(ym), be.alloc_complex(yn)
+        else:
+            self.Yx, self.Yxn = self.Yy, self.Yyn
+        be.fused_bind(self.Yy, self.Yyn, self.Yx, self.Yxn)
+
+    def _swap(self, src, srcn, dst, dstn):
+        if self.world == 1:
+            return
+        per = 2 * self.ym // 3  # one component's main array (doubles)
+        for c in range(3):
+            self.dist.all_to_all_single(dst[c * per:(c + 1) * per], src[c * per:(c + 1) * per], group=self.group)
+        self.dist.all_to_all_single(dstn, srcn, group=self.group)
+
+    def begin(self):
+        cfg, st, be = self.cfg, self.state, self.b
+        params = _params(cfg, self.pen, cfg.max_iter)
+        be.begin(params, self.solid, st["u"], st["u_tilde"], st["q"], st["a"], st["lam"], self.hist)
+        self._to_spectrum(st["q"], 1, self.TU)
+        self._to_spectrum(st["u"], 3, self.TR)
+        be.setup(self.TU, self.TR, self.Q, self.D)  # T-layout Q^ (gauged), D^
+        be.fused_setup(self.Q, self.D, self.R)       # tile-major Q^, D^; x-slab Y of R; compact layout
+        self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
+        self.it = 0
+        return self
+
+    def iterate(self, n_iter: int, poll: bool = True) -> dict:
+        be = self.b
+        info = {"done": False}
+        for _ in range(int(n_iter)):
+            be.fused_pk()
+            self._swap(self.Yy, self.Yyn, self.Yx, self.Yxn)
+            be.fused_rs(self.totals)
+            if self.world > 1:
+                self.dist.all_reduce(self.totals, group=self.group)
+            be.finalize(self.totals)
+            be.fused_mf()
+            self.it += 1
+            if poll and (self.it % self.poll == 0 or self.it == self.cfg.max_iter):
+                info = be.read()
+                if info["done"]:
+                    return info
+            self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
+        return info
+
+    def end(self) -> ConvergenceReport:
+        self.b.fused_end(self.Q)  # Q^ back to T layout; u~, a, lam materialised
+        rep = super().end()
+        rep.meta["pipeline"] = "slab-fused"
+        return rep
+
+
 def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalties: PenaltyParams | None = None,
-                      init_local: dict | None = None, group=None, device=None, comm=None):
+                      init_local: dict | None = None, group=None, device=None, comm=None, fused: bool | None = None):
     """Device slab solve on this rank: ``solid_local`` is the rank's x-slab of the
     indicator (uint8, (N0/P, N1, N2)); returns (local state dict of CUDA tensors,
     ConvergenceReport — identical on every rank)."""
@@ -259,7 +353,10 @@ def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalt
         st = {k: t.as_tensor(np.asarray(init_local[k], dtype=np.float64)).reshape(-1).to(dev).clone()
               for k in ("u", "u_tilde", "q", "a", "lam")}
     solid = t.as_tensor(np.array(solid_local, dtype=np.uint8, copy=True)).reshape(-1).to(dev)
-    solver = SlabStokes(be, dims, cfg, penalties, solid, st, group, comm=comm)
+    if fused is None:
+        fused = be.fused_sizes()[0] > 0
+    cls = FusedSlabStokes if fused else SlabStokes
+    solver = cls(be, dims, cfg, penalties, solid, st, group, comm=comm)
     rep = solver.solve()
     t.cuda.synchronize(dev)
     shp3, shp1 = (3, hi - lo, int(dims[1]), int(dims[2])), (hi - lo, int(dims[1]), int(dims[2]))

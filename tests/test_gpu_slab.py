@@ -79,3 +79,60 @@ def test_device_slab_multi_rank_loopback(pf, golden, case, world):
     for k in ("u", "u_tilde", "q", "a", "lam"):
         full = np.concatenate([st[k] for st, _ in res], axis=0 if k == "q" else 1)
         assert rel_l2(full, z[k]) <= 1e-10, k
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_fused_slab_matches_fused_pipeline(pf, world):
+    """The fused slab pipeline (pf_slab_fused_*) over P loopback ranks reproduces
+    the single-GPU fused pipeline: same iterations, fields to round-off."""
+    from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
+    from slab_loopback import run_ranks
+
+    ind = pf.random_packing_geometry(64, seed=7)
+    cfg = pf.StokesConfig.with_tolerance(1e-6, pressure_gradient=(0.0, 1.0, 0.0), max_iter=40)
+    ref, rref = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    vals = np.asarray(ind.values)
+
+    def rank_fn(r, comm):
+        lo, hi = slab_range(64, world, r)
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True)
+        return {k: v.cpu().numpy() for k, v in st.items()}, rep
+
+    res = run_ranks(world, rank_fn)
+    for _, rep in res:
+        assert rep.meta["pipeline"] == "slab-fused"
+        assert rep.iterations == rref.iterations == 40
+        np.testing.assert_allclose(rep.history, rref.history, rtol=1e-6, atol=1e-9 * np.abs(rref.history).max())
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        full = np.concatenate([st[k] for st, _ in res], axis=0 if k == "q" else 1)
+        assert rel_l2(full, getattr(ref, k).cpu().numpy()) <= 1e-10, k
+
+
+def test_fused_slab_full_solve_matches_reference(pf, golden):
+    """BASELINE cfg 1 (64^3 sphere array, e_1, stiff penalties) solved to
+    convergence by the fused slab pipeline over 2 loopback ranks against the
+    live reference: iteration count, history, sampled u."""
+    import os
+
+    from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
+    from slab_loopback import run_ranks
+
+    if not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", "stokes_sphere64_cfg1.npz")):
+        pytest.skip("cfg-1 golden not generated")
+    z = golden("stokes_sphere64_cfg1")
+    n = int(z["dims"][0])
+    solid = np.unpackbits(z["solid_packed"])[: n ** 3].reshape(n, n, n)
+    pen = pf.PenaltyParams(alpha=1000.0, beta=1000.0, b=1000.0, adaptive=False)
+    cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(1.0, 0.0, 0.0))
+
+    def rank_fn(r, comm):
+        lo, hi = slab_range(n, 2, r)
+        st, rep = solve_stokes_slab(solid[lo:hi], solid.shape, cfg, pen, comm=comm, fused=True)
+        return st["u"].cpu().numpy(), rep
+
+    res = run_ranks(2, rank_fn)
+    u = np.concatenate([x for x, _ in res], axis=1)
+    rep = res[0][1]
+    assert rep.iterations == int(z["iterations"][0]) and rep.converged
+    assert np.abs(u.ravel()[z["sample"]] - z["u_sample"][0]).max() <= 1e-10 * z["u_max"][0]
+    assert abs(np.linalg.norm(u) - z["u_norm"][0]) <= 1e-10 * z["u_norm"][0]
