@@ -73,6 +73,9 @@ struct Bufs {
   // [c][l0 N rows][...].
   int l0, l1, s1, k1off;
   double2 *Yx, *Yxn;  // x-slab Y (== Y, Yn at P = 1)
+  // plane window of one launch of the x-slab passes (SL kernels): planes
+  // [i0a, i0a + nl) of the l0; RS partial rows at [q * pst + poff + block]
+  int i0a, nl, pst, poff;
 };
 
 struct State {
@@ -114,9 +117,9 @@ __device__ __forceinline__ void rs_issue(int tile, const Bufs& B, const State& s
                                          double2* sxn, uint8_t* sh, uint64_t* mbar) {
   using K = RS2<N>;
   using C = Cfg<N>;
-  const int TPC = (SL ? B.l0 : N) * N / K::R;  // tiles per component
+  const int TPC = (SL ? B.nl : N) * N / K::R;  // tiles per component
   const int c = tile / TPC;
-  const int64_t row0 = (int64_t)(tile % TPC) * K::R;
+  const int64_t row0 = ((int64_t)(tile % TPC) * K::R + (SL ? (int64_t)B.i0a * N : 0));
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   const int64_t x0 = (int64_t)c * n + row0 * N;
   const uint32_t vb = sizeof(double) * K::V;
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
-    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     double2* XR = B.XR + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XRn = B.XRn + (size_t)c * (SL ? B.l0 : N) * N;
     mbar_wait(&mbar, phase);
@@ -236,7 +239,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   }
   block_sum<6>(acc);
   if (t == 0)
-    for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+    for (int k = 0; k < 6; ++k)
+      B.part_rs[SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x] = acc[k];
 }
 
 // RS-fix: X-space of u~' (row FFTs of the state), needed by MF only in the
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
   if (ctrl->done || ctrl->db == 0.0) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   auto issue = [&](int tile) {
     const int c = tile / TPC;
-    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     fence_async_smem();
     mbar_expect(&mbar, sizeof(double) * V);
     bulk_load(sst, ut + (int64_t)c * n + row0 * N, sizeof(double) * V, &mbar);
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
-    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     double2* XU = B.XU + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XUn = B.XUn + (size_t)c * (SL ? B.l0 : N) * N;
     mbar_wait(&mbar, phase);
@@ -337,9 +341,9 @@ __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& 
                                           uint32_t* ro_slot, const uint32_t* ro) {
   using K = RS2<N>;
   using C = Cfg<N>;
-  const int TPC = (SL ? B.l0 : N) * N / K::R;
+  const int TPC = (SL ? B.nl : N) * N / K::R;
   const int c = tile / TPC;
-  const int64_t row0 = (int64_t)(tile % TPC) * K::R;
+  const int64_t row0 = ((int64_t)(tile % TPC) * K::R + (SL ? (int64_t)B.i0a * N : 0));
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   constexpr int R = K::R;
   const uint32_t o0 = ro[0];
@@ -385,7 +389,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
   constexpr int SPR = N / 32;  // 32-voxel segments per row
   const int CS = cp.cs;
@@ -409,7 +413,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   uint32_t ro[R + 1];
   auto offs = [&](int tl) {
-    const int64_t r0 = (int64_t)(tl % TPC) * R;
+    const int64_t r0 = ((int64_t)(tl % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
 #pragma unroll
     for (int r = 0; r <= R; ++r) ro[r] = cp.off[r0 + r];
   };
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int c = tile / TPC;
-    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     double2* XR = B.XR + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XRn = B.XRn + (size_t)c * (SL ? B.l0 : N) * N;
     const bool has_next = tile + (int)gridDim.x < NT;
@@ -507,7 +511,8 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   }
   block_sum<6, RS2<N>::T / 32>(acc);
   if (t == 0)
-    for (int k = 0; k < 6; ++k) B.part_rs[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+    for (int k = 0; k < 6; ++k)
+      B.part_rs[SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x] = acc[k];
 }
 
 // RS-fix on the compact path: u~' rows = u' on pore voxels, the compact u~ on solid ones.
@@ -518,7 +523,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   using C = Cfg<N>;
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
-  const int TPC = (SL ? B.l0 : N) * N / R;
+  const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
   constexpr int SPR = N / 32;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
@@ -531,7 +536,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x) {
     const int c = tile / TPC;
-    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     const uint32_t o0 = cp.off[row0];
     const int sb = seg_base<N>(Hs + row0 * N + lane * 32, cp.off[row0 + lane / SPR] - o0, lane);
     __syncthreads();
@@ -723,11 +728,12 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   double2* S = smem + Cfg<N>::TWN;
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int l0 = (SL ? B.l0 : N), l1 = (SL ? B.l1 : N), s1 = (SL ? B.s1 : Cfg<N>::LOGN);
-  const int TPC = l0 * NCH + l0 / CM;  // tiles per component over this x-slab
+  const int nl = SL ? B.nl : N, i0a = SL ? B.i0a : 0;  // plane window of this launch
+  const int TPC = nl * NCH + nl / CM;  // tiles per component over the window
   const int c = blockIdx.x / TPC, tile = blockIdx.x % TPC;
-  const bool nyq = tile >= l0 * NCH;
-  const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;  // i0: local plane
-  const int i0b = nyq ? (tile - l0 * NCH) * CM : 0;
+  const bool nyq = tile >= nl * NCH;
+  const int i0 = nyq ? 0 : i0a + tile / NCH, ch = nyq ? 0 : tile % NCH;  // i0: local plane
+  const int i0b = nyq ? i0a + (tile - nl * NCH) * CM : 0;
   // X (x-slab rows [c][l0 N][H], Nyquist [c][l0 N]); e = k1 (MI out / MF in) or i1
   auto off_of = [&](int e, int q) -> size_t {
     return nyq ? (size_t)(c * l0 + i0b + q) * N + e : ((size_t)(c * l0 + i0) * N + e) * H + ch * CM + q;
@@ -1022,7 +1028,7 @@ template <int N>
 static size_t smem_rsfix() { return fz::RS2<N>::TW + fz::RS2<N>::INV + fz::RS2<N>::ST / 4; }
 template <int N>
 static size_t smem_rsc() { return fz::RSC<N>::BYTES; }
-constexpr int kRsMaxBlocks = kSMs * 32;  // partial-sum rows reserved for the persistent RS grid
+constexpr int kRsMaxBlocks = kSMs * 64;  // partial-sum rows reserved for the persistent RS grid(s)
 template <int N>
 static size_t smem_pk() { return fz::PK2<N>::BYTES; }
 
@@ -1092,6 +1098,10 @@ int fused_ensure(pf_plan* p) {
   f->b.s1 = 0;
   while ((1 << f->b.s1) < N) ++f->b.s1;
   f->b.k1off = 0;
+  f->b.i0a = 0;
+  f->b.nl = N;
+  f->b.pst = 0;
+  f->b.poff = 0;
   f->b.Yx = f->b.Y;
   f->b.Yxn = f->b.Yn;
   f->b.part_rs = (double*)m;
@@ -1302,6 +1312,7 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   fz::k_pk<N, false><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(1));
+  int nb_part = f->nb_rs;
   fz::k_maxis<N, true, false><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
@@ -1313,7 +1324,7 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   }
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
-  k_stokes_finalize_launch(p, f->b.part_rs, f->nb_rs, f->b.part_pk, pk_tiles);
+  k_stokes_finalize_launch(p, f->b.part_rs, nb_part, f->b.part_pk, pk_tiles);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
   if (f->compact) {
@@ -1402,6 +1413,10 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   f->b.s1 = 0;
   while ((1 << f->b.s1) < l1) ++f->b.s1;
   f->b.k1off = k1off;
+  f->b.i0a = 0;
+  f->b.nl = l0;
+  f->b.pst = 0;  // set per launch (nb_rs)
+  f->b.poff = 0;
   std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
@@ -1483,6 +1498,8 @@ static int fslab_rs_t(pf_plan* p, double* totals) {
   fz::State st{p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid};
   const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
   const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
+  f->b.pst = f->nb_rs;
+  f->b.poff = 0;
   fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   if (f->compact) {
