@@ -72,7 +72,15 @@ class IndicatorField:
         values = np.asarray(self.values)
         if values.shape != self.grid.dims:
             raise ValueError(f"indicator shape {values.shape} does not match grid {self.grid.dims}")
-        if not ((values == 0) | (values == 1)).all():
+        if values.dtype == np.bool_ or values.size == 0:
+            ok = True
+        elif np.issubdtype(values.dtype, np.unsignedinteger):
+            ok = int(values.max()) <= 1  # one pass instead of two comparison temporaries
+        elif np.issubdtype(values.dtype, np.integer):
+            ok = int(values.min()) >= 0 and int(values.max()) <= 1
+        else:
+            ok = bool(((values == 0) | (values == 1)).all())
+        if not ok:
             raise ValueError("indicator values must be exactly 0 or 1")
         values = values.astype(np.uint8)
         values.setflags(write=False)
