@@ -83,19 +83,21 @@ def permeability_job(cfg_kwargs=None, penalties=None, device=None):
     def solve(job: CellJob) -> dict:
         from . import effective, spectral, stokes
 
+        from .batch import solve_stokes_many_device
+
         ind = job.indicator
         d = ind.grid.dim
-        us, iters, conv = [], [], []
+        cfgs = []
         for ax in range(d):
             g = [0.0] * d
             g[ax] = 1.0
             kw = dict(cfg_kwargs or {})
             eps = kw.pop("eps", 1e-5)
-            cfg = stokes.StokesConfig.with_tolerance(eps, pressure_gradient=tuple(g), **kw)
-            st, rep = stokes.solve_stokes_device(ind, cfg, penalties, device=device)
-            us.append(st.u)
-            iters.append(rep.iterations)
-            conv.append(rep.converged)
+            cfgs.append(stokes.StokesConfig.with_tolerance(eps, pressure_gradient=tuple(g), **kw))
+        res = solve_stokes_many_device([ind] * d, cfgs, penalties, device)  # the d load cases concurrently
+        us = [st.u for st, _ in res]
+        iters = [rep.iterations for _, rep in res]
+        conv = [rep.converged for _, rep in res]
         K = effective.permeability(us, ind, spectral.CENTRAL)
         return {"K": K, "iterations": iters, "converged": conv}
 

@@ -16,8 +16,9 @@ import numpy as np
 from .device import require_cuda, torch
 from .effective import EffectiveTensors, diffusivity, permeability, pore_average_device
 from .grid import IndicatorField, porosity
-from .stokes import PenaltyParams, StokesConfig, solve_stokes_device
-from .transport import TransportConfig, solve_transport_device
+from .batch import solve_stokes_many_device, solve_transport_many_device
+from .stokes import PenaltyParams, StokesConfig
+from .transport import TransportConfig
 
 
 @dataclass
@@ -55,20 +56,18 @@ def effective_tensors(indicator: IndicatorField, stokes_cfg: StokesConfig | None
         return CellResult(EffectiveTensors(zeros, np.full((d, d), np.nan), 0.0, zeros,
                                            meta={"note": "all-solid geometry: zero flow, transport undefined"}),
                           [], [])
-    unit_u, flow_reports = [], []
-    for axis in range(d):
-        st, rep = solve_stokes_device(indicator, replace(stokes_cfg, pressure_gradient=_unit(d, axis)), penalties,
-                                      device=dev)
-        unit_u.append(st.u)
-        flow_reports.append(rep)
+    # the d unit solves of each stage are independent: run them concurrently (batch.py)
+    flows = solve_stokes_many_device([indicator] * d, [replace(stokes_cfg, pressure_gradient=_unit(d, axis))
+                                                       for axis in range(d)], penalties, dev)
+    unit_u = [st.u for st, _ in flows]
+    flow_reports = [rep for _, rep in flows]
     g_p = np.asarray(stokes_cfg.pressure_gradient, dtype=float)
     u_phys = sum(float(g_p[i]) * unit_u[i] for i in range(d))
-    chis, transport_reports = [], []
-    for axis in range(d):
-        ts, rep = solve_transport_device(indicator, u_phys, replace(transport_cfg, composition_gradient=_unit(d, axis)),
-                                         device=dev)
-        chis.append((ts.chi, ts.grad_chi))
-        transport_reports.append(rep)
+    trs = solve_transport_many_device([indicator] * d, [u_phys] * d,
+                                      [replace(transport_cfg, composition_gradient=_unit(d, axis)) for axis in range(d)],
+                                      dev)
+    chis = [(ts.chi, ts.grad_chi) for ts, _ in trs]
+    transport_reports = [rep for _, rep in trs]
     g_chi = np.asarray(transport_cfg.composition_gradient, dtype=float)
     chi_phys = sum(float(g_chi[j]) * chis[j][0] for j in range(d))
     K = permeability(unit_u, indicator, stokes_cfg.symbol_mode)

@@ -21,6 +21,7 @@ from pathlib import Path
 
 import numpy as np
 
+from .batch import solve_stokes_many_device, solve_transport_many_device
 from .device import require_cuda, to_host
 from .effective import EffectiveTensors, diffusivity, permeability, pore_average_device
 from .ensemble import CellJob, run_ensemble
@@ -164,12 +165,13 @@ def run(config: RunConfig, device=None) -> tuple[dict, int]:
     t0_flow = time.perf_counter()
     unit_u, flow_entries, histories = [], [], []
     all_ok = True
-    for axis in range(grid.dim):
-        cfg_i = replace(config.stokes, pressure_gradient=_unit_vector(grid.dim, axis))
-        state, conv = solve_stokes_device(indicator, cfg_i, config.penalties, device=dev)
+    cfgs = [replace(config.stokes, pressure_gradient=_unit_vector(grid.dim, axis)) for axis in range(grid.dim)]
+    # the unit solves are independent: concurrent on one GPU (batch.py), same results
+    for axis, (state, conv) in enumerate(solve_stokes_many_device([indicator] * grid.dim, cfgs, config.penalties,
+                                                                  dev)):
         unit_u.append(state.u)
         entry = solve_report(conv)
-        entry["pressure_gradient"] = list(cfg_i.pressure_gradient)
+        entry["pressure_gradient"] = list(cfgs[axis].pressure_gradient)
         flow_entries.append(entry)
         histories.append((f"flow_history_axis{axis + 1}.csv", conv))
         all_ok &= conv.converged
@@ -183,12 +185,12 @@ def run(config: RunConfig, device=None) -> tuple[dict, int]:
     # transport: one unit solve per axis under the physical flow (cli.py:361-384)
     t0_tra = time.perf_counter()
     chis, tra_entries = [], []
-    for axis in range(grid.dim):
-        cfg_j = replace(config.transport, composition_gradient=_unit_vector(grid.dim, axis))
-        t_state, t_conv = solve_transport_device(indicator, u_phys, cfg_j, device=dev)
+    tcfgs = [replace(config.transport, composition_gradient=_unit_vector(grid.dim, axis)) for axis in range(grid.dim)]
+    for axis, (t_state, t_conv) in enumerate(solve_transport_many_device([indicator] * grid.dim,
+                                                                         [u_phys] * grid.dim, tcfgs, dev)):
         chis.append((t_state.chi, t_state.grad_chi))
         entry = solve_report(t_conv)
-        entry["composition_gradient"] = list(cfg_j.composition_gradient)
+        entry["composition_gradient"] = list(tcfgs[axis].composition_gradient)
         tra_entries.append(entry)
         histories.append((f"transport_history_axis{axis + 1}.csv", t_conv))
         all_ok &= t_conv.converged

@@ -140,10 +140,10 @@ class TransportSolver:
     """Device-resident comparison-medium driver (begin / iterate / end)."""
 
     def __init__(self, indicator, u_dev, cfg: TransportConfig, state: DeviceTransportState, device=None,
-                 history_rows: int | None = None, pipeline: str | None = None):
+                 history_rows: int | None = None, pipeline: str | None = None, plan_slot: int = 0):
         self.device = require_cuda(device)
         self.indicator, self.cfg, self.state, self.u = indicator, cfg, state, u_dev
-        self.plan = get_plan(indicator.grid.dims, cfg.symbol_mode, self.device)
+        self.plan = get_plan(indicator.grid.dims, cfg.symbol_mode, self.device, plan_slot)
         t = torch()
         self.rows = int(history_rows or cfg.max_iter)
         self.history = t.empty(self.rows * 4, dtype=t.float64, device=self.device)
