@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   __shared__ uint64_t mbar;
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
+  pdl_wait();
   if (ctrl->done || ctrl->db == 0.0) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   __shared__ uint64_t mbar;
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   constexpr int SPR = N / 32;  // 32-voxel segments per row
   const int CS = cp.cs;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   __shared__ uint64_t mbar;
@@ -527,6 +530,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   const int NT = 3 * TPC;
   constexpr int SPR = N / 32;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
+  pdl_wait();
   if (ctrl->done || ctrl->db == 0.0) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   double2* tw = (double2*)sraw;
@@ -722,6 +726,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   using C = Cfg<N>;
   using K = M2<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
@@ -805,6 +810,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   using C = Cfg<N>;
   using K = PK2<N>;
   constexpr int H = C::H, SS = K::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(16) double2 smem[];
   double2* tw = smem;
@@ -1309,34 +1315,33 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK(mark(0));
   const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
   const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
-  fz::k_pk<N, false><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, sa, p->ctrl);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(launch_k(fz::k_pk<N, false>, pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
+                      (const Ctrl*)p->ctrl));
   PF_CK(mark(1));
   int nb_part = f->nb_rs;
-  fz::k_maxis<N, true, false><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
+                      (const Ctrl*)p->ctrl));
   PF_CK(mark(2));
   if (f->compact) {
-    fz::k_rs_compact<N, false><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(f->b, st, compact_of(f),
-                                                                                          p->ctrl);
+    PF_CK_CUDA(launch_k(fz::k_rs_compact<N, false>, f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work,
+                        f->b, st, compact_of(f), (const Ctrl*)p->ctrl));
   } else {
-    fz::k_rs<N, false><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
+    PF_CK_CUDA(launch_k(fz::k_rs<N, false>, f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work, f->b, st,
+                        (const Ctrl*)p->ctrl));
   }
-  PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
-  k_stokes_finalize_launch(p, f->b.part_rs, nb_part, f->b.part_pk, pk_tiles);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(k_stokes_finalize_launch_pdl(p, f->b.part_rs, nb_part, f->b.part_pk, pk_tiles));
   PF_CK(mark(4));
   if (f->compact) {
-    fz::k_rsfix_compact<N, false><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_u, p->s_solid,
-                                                                                   compact_of(f), p->ctrl);
+    PF_CK_CUDA(launch_k(fz::k_rsfix_compact<N, false>, f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work, f->b,
+                        (const double*)p->s_u, (const uint8_t*)p->s_solid, compact_of(f), (const Ctrl*)p->ctrl));
   } else {
-    fz::k_rsfix<N, false><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
+    PF_CK_CUDA(launch_k(fz::k_rsfix<N, false>, f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work, f->b,
+                        (const double*)p->s_ut, (const Ctrl*)p->ctrl));
   }
-  PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(5));
-  fz::k_maxis<N, false, false><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work, f->b,
+                      (const Ctrl*)p->ctrl));
   PF_CK(mark(6));
   return PF_OK;
 }

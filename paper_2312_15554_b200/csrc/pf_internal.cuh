@@ -1,5 +1,6 @@
 // Internal declarations shared by the poreflow_b200 translation units.
 #pragma once
+#include <utility>
 
 #include <cuda_runtime.h>
 #include <cufft.h>
@@ -221,6 +222,7 @@ int stokes_form_r_gated(pf_plan* p, double* R, int gated);
 // Stokes helpers shared with the fused pipeline (pf_stokes.cu)
 int stokes_div_spectrum(pf_plan* p, const double* u, double2* tmp, double2* out);
 int stokes_form_r(pf_plan* p, double* R);
+cudaError_t k_stokes_finalize_launch_pdl(pf_plan* p, const double* part3, int nb3, const double* part1, int nb1);
 void k_stokes_finalize_launch(pf_plan* p, const double* part3, int nb3, const double* part1, int nb1);
 
 // ---------------------------------------------------------------- device helpers
@@ -308,5 +310,38 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ part,
 }
 
 __device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }
+
+// Programmatic dependent launch: a kernel launched with launch_k (PF_PDL) may
+// start while its predecessor drains; it must call pdl_wait() before reading
+// anything the predecessor writes (a no-op for ordinary launches).
+#ifndef PF_PDL
+#define PF_PDL 1  // measured: +4 % at 64^3, neutral at 128^3 and 256^3
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if PF_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+#if PF_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+#else
+  kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
+#endif
+}
 
 }  // namespace pf

@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(kThreads) k_stokes_local(
 __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
     Ctrl* __restrict__ ctrl, const double* __restrict__ part3, int nb3, const double* __restrict__ part1,
     int nb1, double* __restrict__ hist, const StokesConst C, const double inv_n) {
+  pdl_wait();
   if (ctrl->done) return;
   double S[6], P[3];
   reduce_partials<6>(part3, nb3, S);
@@ -387,6 +388,11 @@ int stokes_form_r(pf_plan* p, double* R) {
   }
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
+}
+
+cudaError_t k_stokes_finalize_launch_pdl(pf_plan* p, const double* part3, int nb3, const double* part1, int nb1) {
+  return launch_k(k_stokes_finalize, 1, kFinalizeThreads, 0, p->work, p->ctrl, part3, nb3, part1, nb1, p->s_hist,
+                  p->sc, p->g.inv_n);
 }
 
 void k_stokes_finalize_launch(pf_plan* p, const double* part3, int nb3, const double* part1, int nb1) {
