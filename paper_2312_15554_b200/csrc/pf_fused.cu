@@ -36,7 +36,10 @@
 #ifndef PF_RSC_MINB
 // min CTAs/SM for the compact RS (measured: N = 256 at 4 keeps 240 registers,
 // forcing 5 squeezes ptxas to 168 with spills and is 16 % slower; N <= 128 at 3)
-#define PF_RSC_MINB (RS2<N>::T == 64 ? 4 : 3)
+#define PF_RSC_MINB (N == 256 ? 4 : 3)
+#endif
+#ifndef PF_RS_HALFT
+#define PF_RS_HALFT(N) ((N) <= 128)
 #endif
 #ifndef PF_RSC_MAXNREG
 #define PF_RSC_MAXNREG
@@ -94,7 +97,10 @@ template <int N>
 struct RS2 {
   using C = Cfg<N>;
   static constexpr int R = 1024 / N;            // rows per tile (1024 voxels)
-  static constexpr int T = R * C::G;            // threads per block: one FFT group per row
+  // threads per block: one FFT group per row pair (every thread FFT-active) for
+  // N <= 128; for N = 256 one group per row (measured: 128^3 RS 0.071 vs 0.088 ms,
+  // 256^3 0.483 vs 0.512 ms the other way round)
+  static constexpr int T = R * C::G / (PF_RS_HALFT(N) ? 2 : 1);
   static constexpr int V = R * N;               // voxels per tile
   static constexpr int VPT = V / T;             // voxels per thread
   static constexpr int NP = R / 2;              // inverse sequences (two rows each)
