@@ -177,20 +177,15 @@ inline void pass1_twiddles(double2* out) {
   for (int a = 1; a < C::A / 4; ++a) row(4 * a);
 }
 
-// One N-point complex FFT (unnormalised) of the padded smem sequence s by the
-// G lanes of a group (lane l).  Pass 1: B sub-FFTs of size A over stride-B
-// elements + twiddles; pass 2: A sub-FFTs of size B.  Output in natural order.
-// Every lane of the warp must call this (it uses __syncwarp); `active` = false
-// makes a group participate without touching memory.
+// Remainder of fft_seq once pass 1's inputs are in registers: x[n1] = element
+// B*n1 + l (lanes l < B).  Lets a caller stage the sequence elsewhere (e.g. a
+// swizzled TMA tile) and read it straight into registers.
 template <int N, bool INV>
-__device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ tw, int l, bool active) {
+__device__ __forceinline__ void fft_seq_x(double2* x, double2* s, const double2* __restrict__ tw, int l, bool active) {
   using C = Cfg<N>;
   constexpr int A = C::A, B = C::B;
-  double2 x[A > B ? A : B];
   const bool p1 = active && l < B, p2 = active && l < A;
   if (p1) {
-#pragma unroll
-    for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
     Dft<A, INV>::run(x);
     // w^(4a+b) = w^(4a) * w^b from 3 + A/4-1 table loads instead of A-1 (shared
     // memory bandwidth is the scarce resource of these kernels); <= 2 ulp.
@@ -221,6 +216,23 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
     for (int k2 = 0; k2 < B; ++k2) s[C::pad(l + A * k2)] = x[k2];
   }
   __syncwarp();
+}
+
+// One N-point complex FFT (unnormalised) of the padded smem sequence s by the
+// G lanes of a group (lane l).  Pass 1: B sub-FFTs of size A over stride-B
+// elements + twiddles; pass 2: A sub-FFTs of size B.  Output in natural order.
+// Every lane of the warp must call this (it uses __syncwarp); `active` = false
+// makes a group participate without touching memory.
+template <int N, bool INV>
+__device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ tw, int l, bool active) {
+  using C = Cfg<N>;
+  constexpr int A = C::A, B = C::B;
+  double2 x[A > B ? A : B];
+  if (active && l < B) {
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
+  }
+  fft_seq_x<N, INV>(x, s, tw, l, active);
 }
 
 }  // namespace fz

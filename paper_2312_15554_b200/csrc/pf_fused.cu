@@ -28,6 +28,9 @@
 
 #include "pf_internal.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "pf_fft.cuh"
 
 #ifndef PF_PK_PREFETCH
@@ -43,6 +46,9 @@
 #endif
 #ifndef PF_RSC_MAXNREG
 #define PF_RSC_MAXNREG
+#endif
+#ifndef PF_M_TMA
+#define PF_M_TMA 1  // axis-1 passes load their tiles with one 2D TMA copy (single GPU, N = 128/256)
 #endif
 #ifndef PF_M_MINB
 #define PF_M_MINB 5  // min blocks per SM for the axis-1 passes: 96 regs, 5 blocks (smem-limited too)
@@ -702,7 +708,11 @@ struct PK2 {
   static constexpr int T = PF_PK_THREADS;
   static constexpr int NGP = T / C::G;
   // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
+#ifdef PF_PK_CP
+  static constexpr int CP = PF_PK_CP;
+#else
   static constexpr int CP = (NGP % 3 == 0) ? NGP / 3 : NGP / 2;
+#endif
   static constexpr int NSEQ = 3 * CP;
   static constexpr int NCH = C::H / CP;
   static constexpr int TILES = N * NCH + N / CP;
@@ -723,20 +733,28 @@ struct M2 {
   static constexpr int TPC = N * NCH + N / CM;  // tiles per component
   static constexpr int TILES = 3 * TPC;
   static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
-  static constexpr size_t BYTES_INV = sizeof(double2) * C::TWN + SEQ;
-  static constexpr size_t BYTES_FWD = sizeof(double2) * C::TWN + SEQ;
+  // TMA path (single GPU, N = 128 / 256, main tiles): the CM x N tile lands
+  // 128B-swizzled in a 1 KB-aligned region that the padded sequences then reuse
+  static constexpr bool TMA_OK = (N == 128 || N == 256) && CM * 16 == 128;
+  static constexpr size_t TILE = sizeof(double2) * CM * N;
+  static constexpr size_t REGION = SEQ > TILE ? SEQ : TILE;
+  static constexpr size_t BYTES_INV = sizeof(double2) * C::TWN + REGION + 1024;
+  static constexpr size_t BYTES_FWD = BYTES_INV;
 };
 
 template <int N, bool INV, bool SL>
-__global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl,
+                                                             const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = M2<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
   pdl_wait();
   if (ctrl->done) return;
-  extern __shared__ __align__(16) double2 smem[];
-  double2* tw = smem;
-  double2* S = smem + Cfg<N>::TWN;
+  extern __shared__ __align__(16) unsigned char msraw[];
+  // 1 KB-aligned region (TMA tile / padded sequences), twiddles after it
+  unsigned char* reg = msraw + ((1024 - (su32(msraw) & 1023)) & 1023);
+  double2* S = (double2*)reg;
+  double2* tw = (double2*)(reg + K::REGION);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int l0 = (SL ? B.l0 : N), l1 = (SL ? B.l1 : N), s1 = (SL ? B.s1 : Cfg<N>::LOGN);
   const int nl = SL ? B.nl : N, i0a = SL ? B.i0a : 0;  // plane window of this launch
@@ -755,6 +773,48 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     return nyq ? ((size_t)((r * l0 + i0b + q) * 3 + c)) * l1 + kl
                : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
+  constexpr bool TMA = !SL && K::TMA_OK && PF_M_TMA;
+  if (TMA && !nyq) {
+    // one 2D bulk tensor copy of the (N rows x CM columns) tile, 128B-swizzled
+    __shared__ uint64_t mbar;
+    if (t == 0) {
+      mbar_init(&mbar);
+      mbar_expect(&mbar, (uint32_t)K::TILE);
+      const int x0 = 2 * ch * CM;                   // doubles
+      const int y0 = (c * N + i0) * N;              // rows of [c][i0][e] (Y or X, same 2D view)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              su32(S)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(y0), "r"(su32(&mbar))
+          : "memory");
+    }
+    for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+    constexpr int A = C::A, BB = C::B;
+    double2 x[A > BB ? A : BB];
+    const unsigned char* tile = reg;
+    if (l < BB) {
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) {
+        const int e = BB * n1 + l;  // row e, column g: chunk g of the row, XOR-swizzled by e mod 8
+        x[n1] = *reinterpret_cast<const double2*>(tile + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
+      }
+      if (!INV) {
+        const double db = ctrl->db;
+        if (db != 0.0) {  // rare: b changed this iteration; XU holds X(u~') (k_rsfix)
+#pragma unroll
+          for (int n1 = 0; n1 < A; ++n1) {
+            const double2 vu = B.XU[off_of(BB * n1 + l, g)];
+            x[n1] = make_double2(x[n1].x + db * vu.x, x[n1].y + db * vu.y);
+          }
+        }
+      }
+    }
+    __syncthreads();  // the tile is read: the padded sequences may now overwrite it
+    fft_seq_x<N, INV>(x, S + g * SS, tw, l, true);
+    __syncthreads();
+  } else {
   // element mapping: main tiles walk (e, q) with q fastest (contiguous columns);
   // Nyquist tiles walk (q, e) with e fastest (contiguous rows).
   for (int idx = t; idx < N * CM; idx += T) {
@@ -785,6 +845,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   }
   fft_seq<N, INV>(S + g * SS, tw, l, true);
   __syncthreads();
+  }
   for (int idx = t; idx < N * CM; idx += T) {
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
     const double2 v = S[q * SS + C::pad(e)];
@@ -1016,6 +1077,7 @@ struct FusedPlan {
   // between ranks), the pore part of |lam|^2 added to the local totals instead
   int slab = 0;
   double lam_pore = 0.0;
+  CUtensorMap tm_y{}, tm_xr{};  // 2D maps of Y and XR ([c][i0][e] rows x N/2 columns) for the axis-1 TMA loads
   void* ws = nullptr;        // cuFFT work area of plan2d
   double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
   int nb_full = kSMs, nb_compact = kSMs;
@@ -1075,6 +1137,36 @@ static int set_attrs(FusedPlan* f) {
   return PF_OK;
 }
 
+// 2D tensor map of a [3 N N rows][N/2 complex] array, box = (CM complex, N rows),
+// 128B swizzle (the axis-1 passes' tile); encoded through the runtime's driver
+// entry point so the library does not link libcuda directly.
+static int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PF_CK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return PF_ERR_CUDA;
+    }
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const int H = N / 2;
+  cuuint64_t gdim[2] = {(cuuint64_t)2 * H, (cuuint64_t)3 * N * N};
+  cuuint64_t gstride[1] = {(cuuint64_t)H * sizeof(double2)};
+  cuuint32_t box[2] = {(cuuint32_t)2 * cm, (cuuint32_t)N};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, gdim, gstride, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+
 int fused_ensure(pf_plan* p) {
   if (p->fused) return PF_OK;
   const int N = p->g.n[0];
@@ -1125,6 +1217,11 @@ int fused_ensure(pf_plan* p) {
     default: fz::pass1_twiddles<256>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+  if (N == 128 || N == 256) {
+    const int cm = N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM;
+    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm));
+    PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm));
+  }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
   size_t ws = 0;
@@ -1326,7 +1423,7 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK(mark(1));
   int nb_part = f->nb_rs;
   PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
-                      (const Ctrl*)p->ctrl));
+                      (const Ctrl*)p->ctrl, f->tm_y));
   PF_CK(mark(2));
   if (f->compact) {
     PF_CK_CUDA(launch_k(fz::k_rs_compact<N, false>, f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work,
@@ -1347,7 +1444,7 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   }
   PF_CK(mark(5));
   PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work, f->b,
-                      (const Ctrl*)p->ctrl));
+                      (const Ctrl*)p->ctrl, f->tm_xr));
   PF_CK(mark(6));
   return PF_OK;
 }
@@ -1511,7 +1608,7 @@ static int fslab_rs_t(pf_plan* p, double* totals) {
   const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
   f->b.pst = f->nb_rs;
   f->b.poff = 0;
-  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl);
+  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl, f->tm_y);
   PF_CK_CUDA(cudaGetLastError());
   if (f->compact) {
     fz::k_rs_compact<N, true><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(
@@ -1537,7 +1634,7 @@ static int fslab_mf_t(pf_plan* p) {
     fz::k_rsfix<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
   }
   PF_CK_CUDA(cudaGetLastError());
-  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl);
+  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_y);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
