@@ -47,6 +47,9 @@
 #ifndef PF_RSC_MAXNREG
 #define PF_RSC_MAXNREG
 #endif
+#ifndef PF_PK_TMA
+#define PF_PK_TMA 1  // PK loads its pencils with 3D TMA tensor copies (single GPU, N = 128/256)
+#endif
 #ifndef PF_M_TMA
 #define PF_M_TMA 1  // axis-1 passes load their tiles with one 2D TMA copy (single GPU, N = 128/256)
 #endif
@@ -720,7 +723,14 @@ struct PK2 {
   // sequence stride with an 8-bank shift: the (q fastest, 4 columns) staging
   // pattern of 8-lane phases is then conflict-free
   static constexpr int SS = C::SS + 1;
-  static constexpr size_t BYTES = sizeof(double2) * (C::TWN + NSEQ * SS);
+  // TMA path (single GPU, N = 128 / 256, main tiles): each component's CP x N
+  // pencil lands 64B-swizzled; the three boxes sit at the END of the padded
+  // sequence region so the first FFT round's stores never reach the last box
+  static constexpr bool TMA_OK = (N == 128 || N == 256) && CP * 16 == 64;
+  static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
+  static constexpr size_t BOX = sizeof(double2) * CP * N;
+  static constexpr size_t BOX_OFF = ((REGION - 3 * BOX) / 512) * 512;
+  static constexpr size_t BYTES = REGION + sizeof(double2) * C::TWN + 1024;
 };
 
 template <int N>
@@ -873,15 +883,17 @@ struct SpecArgs {
 // registers before the forward FFTs.
 
 template <int N, bool SL>
-__global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl,
+                                                              const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = PK2<N>;
   constexpr int H = C::H, SS = K::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
   pdl_wait();
   if (ctrl->done) return;
-  extern __shared__ __align__(16) double2 smem[];
-  double2* tw = smem;
-  double2* S = smem + Cfg<N>::TWN;
+  extern __shared__ __align__(16) unsigned char psraw[];
+  unsigned char* reg = psraw + ((1024 - (su32(psraw) & 1023)) & 1023);  // 1 KB-aligned
+  double2* S = (double2*)reg;
+  double2* tw = (double2*)(reg + K::REGION);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const double beta = ctrl->beta, b = ctrl->b;
   const int tile = blockIdx.x;
@@ -893,12 +905,28 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   auto yoff = [&](int c, int i0, int q) -> size_t {
     return nyq ? (size_t)(i0 * 3 + c) * l1 + k1b + q : ((size_t)(c * N + i0) * l1 + k1) * H + ch * CP + q;
   };
-  for (int idx = t; idx < 3 * N * CP; idx += T) {
-    const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
-    const size_t o = yoff(c, i0, q);
-    cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+  constexpr bool TMA = !SL && K::TMA_OK && PF_PK_TMA;
+  const bool tma = TMA && !nyq;
+  __shared__ uint64_t mbar;
+  if (tma) {
+    if (t == 0) {  // three 3D tensor copies: component c's (CP columns x N rows i0) pencil
+      mbar_init(&mbar);
+      mbar_expect(&mbar, (uint32_t)(3 * K::BOX));
+      for (int c = 0; c < 3; ++c)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(su32(reg + K::BOX_OFF + c * K::BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(k1), "r"(c * N), "r"(su32(&mbar))
+            : "memory");
+    }
+  } else {
+    for (int idx = t; idx < 3 * N * CP; idx += T) {
+      const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+      const size_t o = yoff(c, i0, q);
+      cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
   const size_t tbase = (size_t)tile * CP * N;  // tile-major Q^, D^
 #if PF_PK_PREFETCH
   double2 qv[K::MPT], dp[K::MPT];
@@ -912,12 +940,35 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   }
 #endif
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
+  if (tma) {
+    __syncthreads();  // mbarrier initialised
+    mbar_wait(&mbar, 0);
+    constexpr int A = C::A, BB = C::B;
 #pragma unroll
-  for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
-    const int sq = g + r * K::NGP;
-    fft_seq<N, false>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
+    for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
+      const int sq = g + r * K::NGP;
+      const bool act = sq < NSEQ;
+      const int cc = act ? sq / CP : 0, q = act ? sq % CP : 0;
+      const unsigned char* box = reg + K::BOX_OFF + cc * K::BOX;
+      double2 x[A > BB ? A : BB];
+      if (act && l < BB) {
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {  // row e = i0, column q: 16B chunk XOR-swizzled by (e / 2) mod 4
+          const int e = BB * n1 + l;
+          x[n1] = *reinterpret_cast<const double2*>(box + (size_t)e * 64 + ((q ^ ((e >> 1) & 3)) << 4));
+        }
+      }
+      __syncthreads();  // this round's boxes are read before its stores may overwrite them
+      fft_seq_x<N, false>(x, S + (act ? sq : 0) * SS, tw, l, act);
+    }
+  } else {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
+      const int sq = g + r * K::NGP;
+      fft_seq<N, false>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
+    }
   }
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
@@ -1077,6 +1128,7 @@ struct FusedPlan {
   // between ranks), the pore part of |lam|^2 added to the local totals instead
   int slab = 0;
   double lam_pore = 0.0;
+  CUtensorMap tm_pk{};          // 3D map of Y for PK ([c i0][k1][k2] pencils)
   CUtensorMap tm_y{}, tm_xr{};  // 2D maps of Y and XR ([c][i0][e] rows x N/2 columns) for the axis-1 TMA loads
   void* ws = nullptr;        // cuFFT work area of plan2d
   double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
@@ -1167,6 +1219,35 @@ static int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm)
   return PF_OK;
 }
 
+// 3D tensor map of Y [3 N (c, i0)][N k1][N/2 complex], box = (CP complex, 1, N i0),
+// 64B swizzle (PK's component pencils).
+static int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PF_CK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return PF_ERR_CUDA;
+    }
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const int H = N / 2;
+  cuuint64_t gdim[3] = {(cuuint64_t)2 * H, (cuuint64_t)N, (cuuint64_t)3 * N};
+  cuuint64_t gstride[2] = {(cuuint64_t)H * sizeof(double2), (cuuint64_t)N * H * sizeof(double2)};
+  cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)N};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, gdim, gstride, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+
 int fused_ensure(pf_plan* p) {
   if (p->fused) return PF_OK;
   const int N = p->g.n[0];
@@ -1221,6 +1302,7 @@ int fused_ensure(pf_plan* p) {
     const int cm = N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM;
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm));
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm));
+    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP));
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
@@ -1419,7 +1501,7 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
   const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
   PF_CK_CUDA(launch_k(fz::k_pk<N, false>, pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
-                      (const Ctrl*)p->ctrl));
+                      (const Ctrl*)p->ctrl, f->tm_pk));
   PF_CK(mark(1));
   int nb_part = f->nb_rs;
   PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
@@ -1595,7 +1677,7 @@ template <int N>
 static int fslab_pk_t(pf_plan* p) {
   FusedPlan* f = fp_of(p);
   const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
-  fz::k_pk<N, true><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, spec_args(p), p->ctrl);
+  fz::k_pk<N, true><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, spec_args(p), p->ctrl, f->tm_pk);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
