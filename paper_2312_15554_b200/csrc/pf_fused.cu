@@ -28,9 +28,6 @@
 
 #include "pf_internal.cuh"
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "pf_fft.cuh"
 
 #ifndef PF_PK_PREFETCH
@@ -1192,7 +1189,7 @@ static int set_attrs(FusedPlan* f) {
 // 2D tensor map of a [3 N N rows][N/2 complex] array, box = (CM complex, N rows),
 // 128B swizzle (the axis-1 passes' tile); encoded through the runtime's driver
 // entry point so the library does not link libcuda directly.
-static int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm) {
+int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm, int ncomp) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -1205,7 +1202,7 @@ static int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm)
     enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
   const int H = N / 2;
-  cuuint64_t gdim[2] = {(cuuint64_t)2 * H, (cuuint64_t)3 * N * N};
+  cuuint64_t gdim[2] = {(cuuint64_t)2 * H, (cuuint64_t)ncomp * N * N};
   cuuint64_t gstride[1] = {(cuuint64_t)H * sizeof(double2)};
   cuuint32_t box[2] = {(cuuint32_t)2 * cm, (cuuint32_t)N};
   cuuint32_t es[2] = {1, 1};
@@ -1221,7 +1218,7 @@ static int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm)
 
 // 3D tensor map of Y [3 N (c, i0)][N k1][N/2 complex], box = (CP complex, 1, N i0),
 // 64B swizzle (PK's component pencils).
-static int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp) {
+int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp, int ncomp) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -1234,7 +1231,7 @@ static int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp) {
     enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
   const int H = N / 2;
-  cuuint64_t gdim[3] = {(cuuint64_t)2 * H, (cuuint64_t)N, (cuuint64_t)3 * N};
+  cuuint64_t gdim[3] = {(cuuint64_t)2 * H, (cuuint64_t)N, (cuuint64_t)ncomp * N};
   cuuint64_t gstride[2] = {(cuuint64_t)H * sizeof(double2), (cuuint64_t)N * H * sizeof(double2)};
   cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)N};
   cuuint32_t es[3] = {1, 1, 1};
@@ -1300,9 +1297,9 @@ int fused_ensure(pf_plan* p) {
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   if (N == 128 || N == 256) {
     const int cm = N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM;
-    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm));
-    PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm));
-    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP));
+    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
+    PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
+    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP, 3));
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.

@@ -30,6 +30,9 @@
 
 #include "pf_fft.cuh"
 
+#ifndef PF_TM_TMA
+#define PF_TM_TMA 1  // transport axis-1 passes load their tiles with 2D TMA tensor copies (N = 128/256)
+#endif
 #ifndef PF_TPK_PREFETCH
 #define PF_TPK_PREFETCH 1  // previous chi^ loaded into registers under the forward FFT (needs 4 CTAs/SM of regs)
 #endif
@@ -191,21 +194,28 @@ struct TM {
   static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
   // one sequence set: Y_b = FFT(X0) + i k1 FFT(X2) runs its two transforms one
   // after the other, stashing i k1 FFT(X2) in registers (IPT items per thread)
-  static constexpr size_t BYTES = sizeof(double2) * C::TWN + SEQ;
+  // TMA path (N = 128 / 256, main tiles): the CM x N tile lands 128B-swizzled in a
+  // 1 KB-aligned region the padded sequences then reuse
+  static constexpr bool TMA_OK = (N == 128 || N == 256) && CM * 16 == 128;
+  static constexpr size_t TILE = sizeof(double2) * CM * N;
+  static constexpr size_t REGION = SEQ > TILE ? SEQ : TILE;
+  static constexpr size_t BYTES = sizeof(double2) * C::TWN + REGION + 1024;
   static constexpr int IPT = N * CM / T;
 };
 
 // INV (MI_T): outputs oc = 0 X(chi) <- Y0; 1 X(d0 chi) <- Y1; 2 X(d1 chi) <- i k1 Y0.
 // FWD (MF_T): outputs oc = 0 Y_b <- FFT(X0) + i k1 FFT(X2); 1 Y_w0 <- FFT(X1).
 template <int N, bool INV>
-__global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl,
+                                                                          const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = TM<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
   if (ctrl->done) return;
-  extern __shared__ __align__(16) double2 smem[];
-  double2* tw = smem;
-  double2* S = smem + Cfg<N>::TWN;
+  extern __shared__ __align__(16) unsigned char msraw[];
+  unsigned char* reg = msraw + ((1024 - (fz::su32(msraw) & 1023)) & 1023);  // 1 KB-aligned
+  double2* S = (double2*)reg;
+  double2* tw = (double2*)(reg + K::REGION);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int oc = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
   const bool nyq = tile >= N * NCH;
@@ -230,11 +240,48 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
   };
+  constexpr bool TMA = K::TMA_OK && PF_TM_TMA;
+  const bool tma = TMA && !nyq;
+  __shared__ uint64_t mbar;
+  uint32_t par = 0;
+  if (tma && t == 0) fz::mbar_init(&mbar);
+  // one component's tile -> registers (column g) -> the rest of the FFT, via TMA
+  auto tma_fft = [&](int c, bool ik1) {
+    if (t == 0) {
+      fz::mbar_expect(&mbar, (uint32_t)K::TILE);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              fz::su32(reg)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CM), "r"((c * N + i0) * N), "r"(fz::su32(&mbar))
+          : "memory");
+    }
+    __syncthreads();
+    fz::mbar_wait(&mbar, par);
+    par ^= 1u;
+    constexpr int A = C::A, BB = C::B;
+    double2 x[A > BB ? A : BB];
+    if (l < BB) {
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) {
+        const int e = BB * n1 + l;
+        x[n1] = *reinterpret_cast<const double2*>(reg + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
+        if (ik1) x[n1] = cik(__ldg(kap1 + e), x[n1]);
+      }
+    }
+    __syncthreads();  // the tile is read before the padded sequences overwrite it
+    if (INV) fz::fft_seq_x<N, true>(x, S + g * SS, tw, l, true);
+    else fz::fft_seq_x<N, false>(x, S + g * SS, tw, l, true);
+    __syncthreads();
+  };
   double2 v2[K::IPT];
   if (two) {  // i k1 FFT(X2) first, kept in registers
-    stage(2);
-    fft_seq<N, false>(S + g * SS, tw, l, true);
-    __syncthreads();
+    if (tma) {
+      tma_fft(2, false);
+    } else {
+      stage(2);
+      fft_seq<N, false>(S + g * SS, tw, l, true);
+      __syncthreads();
+    }
 #pragma unroll
     for (int j = 0; j < K::IPT; ++j) {
       const int idx = t + T * j;
@@ -243,6 +290,9 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
     }
     __syncthreads();
   }
+  if (tma) {
+    tma_fft(cin, INV && oc == 2);
+  } else {
   stage(cin);
   if (INV && oc == 2) {  // i k1 Y(chi) before the inverse axis-1 transform
     for (int idx = t; idx < N * CM; idx += T) {
@@ -254,6 +304,7 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
   }
   fft_seq<N, INV>(S + g * SS, tw, l, true);
   __syncthreads();
+  }
 #pragma unroll
   for (int j = 0; j < K::IPT; ++j) {
     const int idx = t + T * j;
@@ -510,6 +561,7 @@ struct FusedTPlan {
   double2* g0mem = nullptr;
   cufftHandle plan2d = 0;
   int nb_trs = kSMs;  // persistent RS grid: one wave of resident blocks (occupancy API)
+  CUtensorMap tm_y{}, tm_x{};  // axis-1 TMA maps of Y (2 components) and X (3)
 };
 
 static FusedTPlan* ftp(pf_plan* p) { return reinterpret_cast<FusedTPlan*>(p->tfused); }
@@ -556,6 +608,11 @@ static int tfused_ensure(pf_plan* p) {
     default: fz::pass1_twiddles<256>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+  if (N == 128 || N == 256) {
+    const int cm = N == 128 ? ft::TM<128>::CM : ft::TM<256>::CM;
+    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 2));
+    PF_CK(encode_axis1_map(&f->tm_x, f->b.X, N, cm, 3));
+  }
   size_t ws = 0;
   long long dims2[2] = {N, N};
   PF_CK_FFT(cufftCreate(&f->plan2d));
@@ -657,7 +714,8 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   ft::k_tpk<N><<<ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work>>>(f->b, P, p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(1));
-  ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
+  ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl,
+                                                                                      f->tm_y);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(2));
   ft::k_trs<N><<<f->nb_trs, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work>>>(f->b, P, p->t_u, p->s_solid, p->ctrl);
@@ -666,7 +724,8 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   transport_finalize_launch(p, f->b.part, ft::TPK<N>::TILES, p->g.inv_n);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  ft::k_taxis<N, false><<<2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl);
+  ft::k_taxis<N, false><<<2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl,
+                                                                                       f->tm_x);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(5));
   return PF_OK;

@@ -1,5 +1,7 @@
 // Internal declarations shared by the poreflow_b200 translation units.
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <utility>
 
 #include <cuda_runtime.h>
@@ -191,6 +193,11 @@ void fused_free(pf_plan* p);
 int fused_setup(pf_plan* p);
 int fused_finish(pf_plan* p);
 int enqueue_fused(pf_plan* p, cudaEvent_t* ev);
+// TMA tensor maps of the fused passes (pf_fused.cu): [ncomp N N rows][N/2 complex]
+// with box (cm complex, N rows), 128B swizzle; and [ncomp N (c,i0)][N k1][N/2] with
+// box (cp complex, 1, N), 64B swizzle
+int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm, int ncomp);
+int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp, int ncomp);
 // slab-decomposed fused pipeline (pf_fused.cu, driven by pf_slab_fused_*)
 int fused_slab_supported(int N, int l0, int l1);
 int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, double2* Yyn, double2* Yx,
