@@ -30,6 +30,9 @@
 
 #include "pf_fft.cuh"
 
+#ifndef PF_TPK_TMA
+#define PF_TPK_TMA 1  // PK_T loads its two component pencils with 3D TMA tensor copies (N = 128/256)
+#endif
 #ifndef PF_TM_TMA
 #define PF_TM_TMA 1  // transport axis-1 passes load their tiles with 2D TMA tensor copies (N = 128/256)
 #endif
@@ -83,18 +86,25 @@ struct TPK {
   static constexpr int NCH = C::H / CP;
   static constexpr int TILES = N * NCH + N / CP;
   static constexpr int MPT = CP * N / T;
-  static constexpr size_t BYTES = sizeof(double2) * (C::TWN + NSEQ * C::SS);
+  // TMA path (N = 128 / 256, main tiles): the two components' CP x N pencils land
+  // 64B-swizzled at the start of the (1 KB-aligned) padded sequence region
+  static constexpr bool TMA_OK = (N == 128 || N == 256) && CP * 16 == 64;
+  static constexpr size_t REGION = sizeof(double2) * NSEQ * C::SS;
+  static constexpr size_t BOX = sizeof(double2) * CP * N;
+  static constexpr size_t BYTES = REGION + sizeof(double2) * C::TWN + 1024;
 };
 
 template <int N>
-__global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl) {
+__global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl,
+                                                         const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = TPK<N>;
   constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
   if (ctrl->done) return;
-  extern __shared__ __align__(16) double2 smem[];
-  double2* tw = smem;
-  double2* S = smem + Cfg<N>::TWN;
+  extern __shared__ __align__(16) unsigned char psraw[];
+  unsigned char* reg = psraw + ((1024 - (fz::su32(psraw) & 1023)) & 1023);  // 1 KB-aligned
+  double2* S = (double2*)reg;
+  double2* tw = (double2*)(reg + K::REGION);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const int tile = blockIdx.x;
   const bool nyq = tile >= N * NCH;
@@ -103,12 +113,28 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
   auto yoff = [&](int c, int i0, int q) -> size_t {
     return nyq ? (size_t)(c * N + i0) * N + k1b + q : ((size_t)(c * N + i0) * N + k1) * H + ch * CP + q;
   };
-  for (int idx = t; idx < 2 * N * CP; idx += T) {
-    const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
-    const size_t o = yoff(c, i0, q);
-    cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+  constexpr bool TMA = K::TMA_OK && PF_TPK_TMA;
+  const bool tma = TMA && !nyq;
+  __shared__ uint64_t mbar;
+  if (tma) {
+    if (t == 0) {  // two 3D tensor copies: component c's (CP columns x N rows i0) pencil
+      fz::mbar_init(&mbar);
+      fz::mbar_expect(&mbar, (uint32_t)(2 * K::BOX));
+      for (int c = 0; c < 2; ++c)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(fz::su32(reg + c * K::BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(k1), "r"(c * N), "r"(fz::su32(&mbar))
+            : "memory");
+    }
+  } else {
+    for (int idx = t; idx < 2 * N * CP; idx += T) {
+      const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+      const size_t o = yoff(c, i0, q);
+      cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const bool first = (B.G0 != nullptr) && ctrl->iter == 0;
   const size_t tbase = (size_t)tile * CP * N;
@@ -117,9 +143,28 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
 #pragma unroll
   for (int j = 0; j < K::MPT; ++j) chp[j] = B.CH[tbase + t + T * j];
 #endif
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  fft_seq<N, false>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
+  if (tma) {
+    __syncthreads();  // mbarrier initialised
+    fz::mbar_wait(&mbar, 0);
+    constexpr int A = C::A, BB = C::B;
+    const bool act = g < NSEQ;
+    const int cc = act ? g / CP : 0, q = act ? g % CP : 0;
+    const unsigned char* box = reg + cc * K::BOX;
+    double2 x[A > BB ? A : BB];
+    if (act && l < BB) {
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) {  // row e = i0, column q: 16B chunk XOR-swizzled by (e / 2) mod 4
+        const int e = BB * n1 + l;
+        x[n1] = *reinterpret_cast<const double2*>(box + (size_t)e * 64 + ((q ^ ((e >> 1) & 3)) << 4));
+      }
+    }
+    __syncthreads();  // both boxes read before the padded sequences overwrite them
+    fz::fft_seq_x<N, false>(x, S + (act ? g : 0) * SS, tw, l, act);
+  } else {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    fft_seq<N, false>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
+  }
   __syncthreads();
   const size_t nh = (size_t)K::TILES * CP * N;
   double acc[2] = {0.0, 0.0};
@@ -562,6 +607,7 @@ struct FusedTPlan {
   cufftHandle plan2d = 0;
   int nb_trs = kSMs;  // persistent RS grid: one wave of resident blocks (occupancy API)
   CUtensorMap tm_y{}, tm_x{};  // axis-1 TMA maps of Y (2 components) and X (3)
+  CUtensorMap tm_pk{};         // PK_T pencil map of Y
 };
 
 static FusedTPlan* ftp(pf_plan* p) { return reinterpret_cast<FusedTPlan*>(p->tfused); }
@@ -612,6 +658,7 @@ static int tfused_ensure(pf_plan* p) {
     const int cm = N == 128 ? ft::TM<128>::CM : ft::TM<256>::CM;
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 2));
     PF_CK(encode_axis1_map(&f->tm_x, f->b.X, N, cm, 3));
+    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? ft::TPK<128>::CP : ft::TPK<256>::CP, 2));
   }
   size_t ws = 0;
   long long dims2[2] = {N, N};
@@ -711,7 +758,7 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
     return PF_OK;
   };
   PF_CK(mark(0));
-  ft::k_tpk<N><<<ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work>>>(f->b, P, p->ctrl);
+  ft::k_tpk<N><<<ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work>>>(f->b, P, p->ctrl, f->tm_pk);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(1));
   ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl,
