@@ -87,7 +87,7 @@ def main():
                      f"{', '.join(d['top_stalls'])} |\n")
     traffic = {}
     names = {"k_rs<": "RS_rows_local", "k_rs_compact<": "RS_rows_local", "k_pk<": "PK_axis0_spectral",
-             "k_maxis<256, 1>": "MI_axis1_inverse", "k_maxis<256, 0>": "MF_axis1_forward",
+             "k_maxis<256, 1": "MI_axis1_inverse", "k_maxis<256, 0": "MF_axis1_forward",
              "k_tpk<": "PK_T", "k_trs<": "RS_T", "k_taxis<256, 1>": "MI_T", "k_taxis<256, 0>": "MF_T"}
     for d in fl:
         for key, stage in names.items():
