@@ -780,20 +780,30 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     return nyq ? ((size_t)((r * l0 + i0b + q) * 3 + c)) * l1 + kl
                : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
-  constexpr bool TMA = !SL && K::TMA_OK && PF_M_TMA;
+  constexpr bool TMA = K::TMA_OK && PF_M_TMA;
   if (TMA && !nyq) {
     // one 2D bulk tensor copy of the (N rows x CM columns) tile, 128B-swizzled
     __shared__ uint64_t mbar;
     if (t == 0) {
       mbar_init(&mbar);
       mbar_expect(&mbar, (uint32_t)K::TILE);
-      const int x0 = 2 * ch * CM;                   // doubles
-      const int y0 = (c * N + i0) * N;              // rows of [c][i0][e] (Y or X, same 2D view)
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-              su32(S)),
-          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(y0), "r"(su32(&mbar))
-          : "memory");
+      const int x0 = 2 * ch * CM;  // doubles
+      if (SL && INV) {
+        // x-slab Y [c][r][i0][k1 - r l1][k2]: a 5D box (16 doubles, l1, 1, P, 1) whose
+        // rows come out in k1 = r l1 + kl order
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+            "%6}], [%7];" ::"r"(su32(S)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(0), "r"(i0), "r"(0), "r"(c), "r"(su32(&mbar))
+            : "memory");
+      } else {
+        const int y0 = (c * l0 + i0) * N;  // rows of [c][i0][e] (Y at P = 1, or X)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                su32(S)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(y0), "r"(su32(&mbar))
+            : "memory");
+      }
     }
     for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
     __syncthreads();
@@ -902,7 +912,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   auto yoff = [&](int c, int i0, int q) -> size_t {
     return nyq ? (size_t)(i0 * 3 + c) * l1 + k1b + q : ((size_t)(c * N + i0) * l1 + k1) * H + ch * CP + q;
   };
-  constexpr bool TMA = !SL && K::TMA_OK && PF_PK_TMA;
+  constexpr bool TMA = K::TMA_OK && PF_PK_TMA;
   const bool tma = TMA && !nyq;
   __shared__ uint64_t mbar;
   if (tma) {
@@ -1189,7 +1199,11 @@ static int set_attrs(FusedPlan* f) {
 // 2D tensor map of a [3 N N rows][N/2 complex] array, box = (CM complex, N rows),
 // 128B swizzle (the axis-1 passes' tile); encoded through the runtime's driver
 // entry point so the library does not link libcuda directly.
+static int encode_axis1_rows(CUtensorMap* tm, const double2* base, int N, int cm, int64_t rows);
 int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm, int ncomp) {
+  return encode_axis1_rows(tm, base, N, cm, (int64_t)ncomp * N * N);
+}
+static int encode_axis1_rows(CUtensorMap* tm, const double2* base, int N, int cm, int64_t rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -1202,7 +1216,7 @@ int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm, int nc
     enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
   const int H = N / 2;
-  cuuint64_t gdim[2] = {(cuuint64_t)2 * H, (cuuint64_t)ncomp * N * N};
+  cuuint64_t gdim[2] = {(cuuint64_t)2 * H, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)H * sizeof(double2)};
   cuuint32_t box[2] = {(cuuint32_t)2 * cm, (cuuint32_t)N};
   cuuint32_t es[2] = {1, 1};
@@ -1218,7 +1232,14 @@ int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm, int nc
 
 // 3D tensor map of Y [3 N (c, i0)][N k1][N/2 complex], box = (CP complex, 1, N i0),
 // 64B swizzle (PK's component pencils).
+static int encode_pk_map_gen(CUtensorMap* tm, const double2* base, int N, int cp, int ncomp, int l1);
 int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp, int ncomp) {
+  return encode_pk_map_gen(tm, base, N, cp, ncomp, N);
+}
+static int encode_pk_map_l1(CUtensorMap* tm, const double2* base, int N, int cp, int l1) {
+  return encode_pk_map_gen(tm, base, N, cp, 3, l1);
+}
+static int encode_pk_map_gen(CUtensorMap* tm, const double2* base, int N, int cp, int ncomp, int l1) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -1231,8 +1252,8 @@ int encode_pk_map(CUtensorMap* tm, const double2* base, int N, int cp, int ncomp
     enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
   const int H = N / 2;
-  cuuint64_t gdim[3] = {(cuuint64_t)2 * H, (cuuint64_t)N, (cuuint64_t)ncomp * N};
-  cuuint64_t gstride[2] = {(cuuint64_t)H * sizeof(double2), (cuuint64_t)N * H * sizeof(double2)};
+  cuuint64_t gdim[3] = {(cuuint64_t)2 * H, (cuuint64_t)l1, (cuuint64_t)ncomp * N};
+  cuuint64_t gstride[2] = {(cuuint64_t)H * sizeof(double2), (cuuint64_t)l1 * H * sizeof(double2)};
   cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)N};
   cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, gdim, gstride, box, es,
@@ -1555,6 +1576,36 @@ static bool fslab_shape_ok(int N, int l0, int l1) {
   return l0 % cm == 0 && l1 % cp == 0;
 }
 
+// 5D tensor map of the x-slab Y [3][P][l0][l1][N/2 complex] with box (cm complex,
+// l1, 1, P, 1): an axis-1 tile whose N rows come out in k1 order, 128B swizzle.
+static int encode_yx_map(CUtensorMap* tm, const double2* base, int N, int cm, int l0, int l1) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PF_CK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return PF_ERR_CUDA;
+    }
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const int H = N / 2, P = N / l1;
+  const cuuint64_t rowb = (cuuint64_t)H * sizeof(double2);
+  cuuint64_t gdim[5] = {(cuuint64_t)2 * H, (cuuint64_t)l1, (cuuint64_t)l0, (cuuint64_t)P, 3};
+  cuuint64_t gstride[4] = {rowb, rowb * l1, rowb * l1 * l0, rowb * l1 * l0 * P};
+  cuuint32_t box[5] = {(cuuint32_t)2 * cm, (cuuint32_t)l1, 1, (cuuint32_t)P, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, gdim, gstride, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (5D) failed (%d)", (int)r);
+    return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+
 int fused_slab_supported(int N, int l0, int l1) { return fslab_shape_ok(N, l0, l1) ? 1 : 0; }
 
 int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, double2* Yyn, double2* Yx,
@@ -1622,6 +1673,13 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   PF_CK_CUDA(cudaMalloc(&f->spec, sizeof(double2) * 3 * (size_t)l0 * N * (H + 1)));
   PF_CK_FFT(cufftSetWorkArea(f->plan2d, f->ws));
   PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
+  if (N == 128 || N == 256) {  // TMA maps of this slab's layouts
+    const int cm = N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM;
+    const int cp = N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP;
+    PF_CK(encode_yx_map(&f->tm_y, Yx, N, cm, l0, l1));
+    PF_CK(encode_axis1_rows(&f->tm_xr, f->b.XR, N, cm, 3 * (int64_t)l0 * N));
+    PF_CK(encode_pk_map_l1(&f->tm_pk, Yy, N, cp, l1));
+  }
   switch (N) {
     case 64: PF_CK(set_attrs<64>(f)); break;
     case 128: PF_CK(set_attrs<128>(f)); break;
@@ -1713,7 +1771,7 @@ static int fslab_mf_t(pf_plan* p) {
     fz::k_rsfix<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
   }
   PF_CK_CUDA(cudaGetLastError());
-  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_y);
+  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_xr);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
