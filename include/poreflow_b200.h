@@ -171,6 +171,16 @@ int pf_slab_fused_pk(pf_plan* plan);
 int pf_slab_fused_rs(pf_plan* plan, double* totals9);
 int pf_slab_fused_mf(pf_plan* plan);
 int pf_slab_fused_end(pf_plan* plan, double* Q_tspec);
+/* Component-pipelined form of pf_slab_fused_rs / pf_slab_fused_mf, so the host
+ * can overlap the exchange of component c + 1 with the passes of component c:
+ * pf_slab_fused_rs_part(c) for c = 0, 1, 2 (each after its component and the
+ * Nyquist columns arrived) then pf_slab_fused_totals; after pf_slab_finalize,
+ * pf_slab_fused_mf_part(c, fix = (c == 0)) for c = 0, 1, 2, each component's
+ * exchange issued as soon as its MF is enqueued.  Same results as the
+ * unsplit calls (the residual sums are reduced in a fixed order). */
+int pf_slab_fused_rs_part(pf_plan* plan, int comp);
+int pf_slab_fused_totals(pf_plan* plan, double* totals9);
+int pf_slab_fused_mf_part(pf_plan* plan, int comp, int fix);
 
 /* ------------------------------------------------------------------------
  * Transport — replaces poreflow.transport.solve_transport

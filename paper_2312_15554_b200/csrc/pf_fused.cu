@@ -85,6 +85,8 @@ struct Bufs {
   // plane window of one launch of the x-slab passes (SL kernels): planes
   // [i0a, i0a + nl) of the l0; RS partial rows at [q * pst + poff + block]
   int i0a, nl, pst, poff;
+  // component window of one launch of MI / RS (SL kernels): components [c0, c0 + nc)
+  int c0, nc;
 };
 
 struct State {
@@ -130,7 +132,7 @@ __device__ __forceinline__ void rs_issue(int tile, const Bufs& B, const State& s
   using K = RS2<N>;
   using C = Cfg<N>;
   const int TPC = (SL ? B.nl : N) * N / K::R;  // tiles per component
-  const int c = tile / TPC;
+  const int c = (SL ? B.c0 : 0) + tile / TPC;
   const int64_t row0 = ((int64_t)(tile % TPC) * K::R + (SL ? (int64_t)B.i0a * N : 0));
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   const int64_t x0 = (int64_t)c * n + row0 * N;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   const int TPC = (SL ? B.nl : N) * N / R;
-  const int NT = 3 * TPC;
+  const int NT = (SL ? B.nc : 3) * TPC;  // component window [c0, c0 + nc) (slab)
   pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
   double acc[6] = {0, 0, 0, 0, 0, 0};
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
-    const int c = tile / TPC;
+    const int c = (SL ? B.c0 : 0) + tile / TPC;
     const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     double2* XR = B.XR + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XRn = B.XRn + (size_t)c * (SL ? B.l0 : N) * N;
@@ -356,7 +358,7 @@ __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& 
   using K = RS2<N>;
   using C = Cfg<N>;
   const int TPC = (SL ? B.nl : N) * N / K::R;
-  const int c = tile / TPC;
+  const int c = (SL ? B.c0 : 0) + tile / TPC;
   const int64_t row0 = ((int64_t)(tile % TPC) * K::R + (SL ? (int64_t)B.i0a * N : 0));
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   constexpr int R = K::R;
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   using K = RS2<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   const int TPC = (SL ? B.nl : N) * N / R;
-  const int NT = 3 * TPC;
+  const int NT = (SL ? B.nc : 3) * TPC;  // component window [c0, c0 + nc) (slab)
   constexpr int SPR = N / 32;  // 32-voxel segments per row
   const int CS = cp.cs;
   static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   double acc[6] = {0, 0, 0, 0, 0, 0};
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
-    const int c = tile / TPC;
+    const int c = (SL ? B.c0 : 0) + tile / TPC;
     const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     double2* XR = B.XR + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XRn = B.XRn + (size_t)c * (SL ? B.l0 : N) * N;
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   const int l0 = (SL ? B.l0 : N), l1 = (SL ? B.l1 : N), s1 = (SL ? B.s1 : Cfg<N>::LOGN);
   const int nl = SL ? B.nl : N, i0a = SL ? B.i0a : 0;  // plane window of this launch
   const int TPC = nl * NCH + nl / CM;  // tiles per component over the window
-  const int c = blockIdx.x / TPC, tile = blockIdx.x % TPC;
+  const int c = (SL ? B.c0 : 0) + blockIdx.x / TPC, tile = blockIdx.x % TPC;
   const bool nyq = tile >= nl * NCH;
   const int i0 = nyq ? 0 : i0a + tile / NCH, ch = nyq ? 0 : tile % NCH;  // i0: local plane
   const int i0b = nyq ? i0a + (tile - nl * NCH) * CM : 0;
@@ -1131,6 +1133,7 @@ struct FusedPlan {
   int c_cs = 16;  // staging capacity per tile (Compact::cs)
   int compact = 0;
   int nb_rs = kSMs;              // persistent RS grid of the active path (full or compact)
+  int rs_rows = kSMs;            // RS partial rows of the last slab iteration (nb_rs or 3 nb_rs)
   // slab-decomposed use (fused_slab_*): Y buffers owned by the caller (exchanged
   // between ranks), the pore part of |lam|^2 added to the local totals instead
   int slab = 0;
@@ -1303,6 +1306,8 @@ int fused_ensure(pf_plan* p) {
   f->b.k1off = 0;
   f->b.i0a = 0;
   f->b.nl = N;
+  f->b.c0 = 0;
+  f->b.nc = 3;
   f->b.pst = 0;
   f->b.poff = 0;
   f->b.Yx = f->b.Y;
@@ -1653,6 +1658,8 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   f->b.k1off = k1off;
   f->b.i0a = 0;
   f->b.nl = l0;
+  f->b.c0 = 0;
+  f->b.nc = 3;
   f->b.pst = 0;  // set per launch (nb_rs)
   f->b.poff = 0;
   std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
@@ -1738,13 +1745,29 @@ static int fslab_pk_t(pf_plan* p) {
 }
 
 template <int N>
-static int fslab_rs_t(pf_plan* p, double* totals) {
+static int fslab_totals_t(pf_plan* p, double* totals) {
+  FusedPlan* f = fp_of(p);
+  const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
+  fz::k_fslab_totals<<<1, kFinalizeThreads, 0, p->work>>>(f->b.part_rs, f->rs_rows, f->b.part_pk, pk_tiles,
+                                                         f->lam_pore, totals);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+// MI + RS over the component window [c0, c0 + nc): nc = 3 (one launch each, partial
+// rows [0, nb_rs)) or nc = 1 (one component, so the exchange of the next
+// component overlaps it; partial rows [c0 nb_rs, (c0 + 1) nb_rs) of 3 nb_rs).
+// totals (may be null) = this rank's 9 sums once every component has run.
+template <int N>
+static int fslab_rs_t(pf_plan* p, int c0, int nc, double* totals) {
   FusedPlan* f = fp_of(p);
   fz::State st{p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid};
-  const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
-  const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
-  f->b.pst = f->nb_rs;
-  f->b.poff = 0;
+  const int m_tiles = nc * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
+  f->b.c0 = c0;
+  f->b.nc = nc;
+  f->b.pst = nc == 3 ? f->nb_rs : 3 * f->nb_rs;
+  f->b.poff = nc == 3 ? 0 : c0 * f->nb_rs;
+  f->rs_rows = f->b.pst;
   fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl, f->tm_y);
   PF_CK_CUDA(cudaGetLastError());
   if (f->compact) {
@@ -1754,16 +1777,14 @@ static int fslab_rs_t(pf_plan* p, double* totals) {
     fz::k_rs<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rs<N>(), p->work>>>(f->b, st, p->ctrl);
   }
   PF_CK_CUDA(cudaGetLastError());
-  fz::k_fslab_totals<<<1, kFinalizeThreads, 0, p->work>>>(f->b.part_rs, f->nb_rs, f->b.part_pk, pk_tiles,
-                                                         f->lam_pore, totals);
-  PF_CK_CUDA(cudaGetLastError());
-  return PF_OK;
+  f->b.c0 = 0;
+  f->b.nc = 3;
+  return totals ? fslab_totals_t<N>(p, totals) : PF_OK;
 }
 
 template <int N>
-static int fslab_mf_t(pf_plan* p) {
+static int fslab_rsfix_t(pf_plan* p) {
   FusedPlan* f = fp_of(p);
-  const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
   if (f->compact) {
     fz::k_rsfix_compact<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_u, p->s_solid,
                                                                                       compact_of(f), p->ctrl);
@@ -1771,8 +1792,22 @@ static int fslab_mf_t(pf_plan* p) {
     fz::k_rsfix<N, true><<<f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work>>>(f->b, p->s_ut, p->ctrl);
   }
   PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+// MF over the component window [c0, c0 + nc); `fix` runs the (gated) RSF pass of
+// every component first, so it must be set on the first window of an iteration.
+template <int N>
+static int fslab_mf_t(pf_plan* p, int c0, int nc, bool fix) {
+  FusedPlan* f = fp_of(p);
+  if (fix) PF_CK(fslab_rsfix_t<N>(p));
+  const int m_tiles = nc * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
+  f->b.c0 = c0;
+  f->b.nc = nc;
   fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_xr);
   PF_CK_CUDA(cudaGetLastError());
+  f->b.c0 = 0;
+  f->b.nc = 3;
   return PF_OK;
 }
 
@@ -1784,21 +1819,19 @@ int fused_slab_pk(pf_plan* p) {
   }
 }
 
-int fused_slab_rs(pf_plan* p, double* totals) {
-  switch (fp_of(p)->N) {
-    case 64: return fslab_rs_t<64>(p, totals);
-    case 128: return fslab_rs_t<128>(p, totals);
-    default: return fslab_rs_t<256>(p, totals);
+#define PF_FSLAB_DISPATCH(fn, ...)        \
+  switch (fp_of(p)->N) {                  \
+    case 64: return fn<64>(__VA_ARGS__);  \
+    case 128: return fn<128>(__VA_ARGS__); \
+    default: return fn<256>(__VA_ARGS__); \
   }
-}
 
-int fused_slab_mf(pf_plan* p) {
-  switch (fp_of(p)->N) {
-    case 64: return fslab_mf_t<64>(p);
-    case 128: return fslab_mf_t<128>(p);
-    default: return fslab_mf_t<256>(p);
-  }
-}
+int fused_slab_rs(pf_plan* p, double* totals) { PF_FSLAB_DISPATCH(fslab_rs_t, p, 0, 3, totals) }
+int fused_slab_rs_part(pf_plan* p, int comp) { PF_FSLAB_DISPATCH(fslab_rs_t, p, comp, 1, nullptr) }
+int fused_slab_totals(pf_plan* p, double* totals) { PF_FSLAB_DISPATCH(fslab_totals_t, p, totals) }
+int fused_slab_mf(pf_plan* p) { PF_FSLAB_DISPATCH(fslab_mf_t, p, 0, 3, true) }
+int fused_slab_mf_part(pf_plan* p, int comp, int fix) { PF_FSLAB_DISPATCH(fslab_mf_t, p, comp, 1, fix != 0) }
+#undef PF_FSLAB_DISPATCH
 
 // Q^ back to the slab T layout (unscaled) and the compact multipliers materialised.
 int fused_slab_end(pf_plan* p, double2* Tq) {

@@ -206,6 +206,9 @@ int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R
 int fused_slab_pk(pf_plan* p);
 int fused_slab_rs(pf_plan* p, double* totals);
 int fused_slab_mf(pf_plan* p);
+int fused_slab_rs_part(pf_plan* p, int comp);
+int fused_slab_totals(pf_plan* p, double* totals);
+int fused_slab_mf_part(pf_plan* p, int comp, int fix);
 int fused_slab_end(pf_plan* p, double2* Tq);
 int fused_is_compact(const pf_plan* p);
 // fused transport pipeline (pf_fused_transport.cu)

@@ -436,6 +436,37 @@ int pf_slab_fused_mf(pf_plan* p) {
   return leave(p);
 }
 
+// Component-pipelined variants (slab.py overlaps the exchange of component c + 1
+// with the passes of component c): MI + RS of one component; the rank's 9 sums
+// once all three ran; MF of one component (fix = 1 on the first one of an
+// iteration runs the gated RSF pass of every component first).
+int pf_slab_fused_rs_part(pf_plan* p, int comp) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(comp >= 0 && comp < 3, "comp 0..2");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_rs_part(p, comp));
+  return leave(p);
+}
+
+int pf_slab_fused_totals(pf_plan* p, double* totals) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(totals, "null argument");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_totals(p, totals));
+  return leave(p);
+}
+
+int pf_slab_fused_mf_part(pf_plan* p, int comp, int fix) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(comp >= 0 && comp < 3, "comp 0..2");
+  PF_CK(enter(p));
+  PF_CK(fused_slab_mf_part(p, comp, fix));
+  return leave(p);
+}
+
 int pf_slab_fused_end(pf_plan* p, double* Tq) {
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));

@@ -129,6 +129,15 @@ class DeviceSlabBackend:
     def fused_mf(self):
         N.check(self.lib.pf_slab_fused_mf(self.h))
 
+    def fused_rs_part(self, comp):
+        N.check(self.lib.pf_slab_fused_rs_part(self.h, int(comp)))
+
+    def fused_totals(self, totals):
+        N.check(self.lib.pf_slab_fused_totals(self.h, self._p(totals)))
+
+    def fused_mf_part(self, comp, fix):
+        N.check(self.lib.pf_slab_fused_mf_part(self.h, int(comp), 1 if fix else 0))
+
     def fused_end(self, Q):
         N.check(self.lib.pf_slab_fused_end(self.h, self._p(Q)))
 
@@ -152,15 +161,19 @@ class SlabStokes:
     """
 
     def __init__(self, backend, dims, cfg: StokesConfig, penalties: PenaltyParams | None, solid_local, state,
-                 group=None, poll_every: int = 8, comm=None):
+                 group=None, poll_every: int = 8, comm=None, overlap: bool = True):
         """``comm``: an object with torch.distributed's ``get_world_size`` /
         ``all_to_all_single`` / ``all_reduce`` (default: torch.distributed when
-        initialised); tests inject an in-process loopback to run P ranks on one GPU."""
+        initialised); tests inject an in-process loopback to run P ranks on one GPU.
+        ``overlap``: pipeline every 3-component exchange per component (async
+        all_to_all) so component c's transfer overlaps the local
+        transforms of its neighbours; False = one blocking exchange per transform."""
         import torch.distributed as dist
 
         self.b, self.dims, self.cfg = backend, tuple(int(x) for x in dims), cfg
         self.pen = penalties or PenaltyParams()
         self.solid, self.state, self.group, self.poll = solid_local, state, group, max(1, int(poll_every))
+        self.overlap = bool(overlap)
         if comm is not None:
             self.dist = comm
         else:
@@ -184,15 +197,45 @@ class SlabStokes:
         k = 2 * ncomp * self.b.exch
         self.dist.all_to_all_single(self.recv[:k], self.send[:k], group=self.group)
 
+    def _a2a(self, out, inp):
+        """Asynchronous all_to_all of equal contiguous splits; the returned handle's
+        ``wait()`` orders the caller's stream after it (NCCL) or blocks (gloo)."""
+        return self.dist.all_to_all_single(out, inp, group=self.group, async_op=True)
+
+    def _pipelined(self, ncomp):
+        return self.overlap and self.world > 1 and ncomp > 1
+
     def _to_spectrum(self, real, ncomp, tspec):
-        self.b.forward(real, ncomp, self.send)
-        self._exchange(ncomp)
-        self.b.forward_finish(self.recv, ncomp, tspec)
+        if not self._pipelined(ncomp):
+            self.b.forward(real, ncomp, self.send)
+            self._exchange(ncomp)
+            self.b.forward_finish(self.recv, ncomp, tspec)
+            return
+        # component c's exchange runs while component c + 1's 2D transform and
+        # component c - 1's 1D transform do
+        E, R, T = 2 * self.b.exch, self.b.real, 2 * self.b.tspec
+        works = []
+        for c in range(ncomp):
+            self.b.forward(real[c * R:(c + 1) * R], 1, self.send[c * E:(c + 1) * E])
+            works.append(self._a2a(self.recv[c * E:(c + 1) * E], self.send[c * E:(c + 1) * E]))
+        for c in range(ncomp):
+            works[c].wait()
+            self.b.forward_finish(self.recv[c * E:(c + 1) * E], 1, tspec[c * T:(c + 1) * T])
 
     def _to_real(self, tspec, ncomp, real):
-        self.b.inverse(tspec, ncomp, self.send)
-        self._exchange(ncomp)
-        self.b.inverse_finish(self.recv, ncomp, real)
+        if not self._pipelined(ncomp):
+            self.b.inverse(tspec, ncomp, self.send)
+            self._exchange(ncomp)
+            self.b.inverse_finish(self.recv, ncomp, real)
+            return
+        E, R, T = 2 * self.b.exch, self.b.real, 2 * self.b.tspec
+        works = []
+        for c in range(ncomp):
+            self.b.inverse(tspec[c * T:(c + 1) * T], 1, self.send[c * E:(c + 1) * E])
+            works.append(self._a2a(self.recv[c * E:(c + 1) * E], self.send[c * E:(c + 1) * E]))
+        for c in range(ncomp):
+            works[c].wait()
+            self.b.inverse_finish(self.recv[c * E:(c + 1) * E], 1, real[c * R:(c + 1) * R])
 
     def begin(self):
         """Bind the state and build the spectral copies of the initial state
@@ -263,8 +306,8 @@ class FusedSlabStokes(SlabStokes):
     no packing pass; at P = 1 both layouts coincide and nothing moves."""
 
     def __init__(self, backend, dims, cfg, penalties, solid_local, state, group=None, poll_every: int = 8,
-                 comm=None):
-        super().__init__(backend, dims, cfg, penalties, solid_local, state, group, poll_every, comm)
+                 comm=None, overlap: bool = True):
+        super().__init__(backend, dims, cfg, penalties, solid_local, state, group, poll_every, comm, overlap)
         be = backend
         ym, yn = be.fused_sizes()
         if ym == 0:
@@ -276,6 +319,7 @@ class FusedSlabStokes(SlabStokes):
         else:
             self.Yx, self.Yxn = self.Yy, self.Yyn
         be.fused_bind(self.Yy, self.Yyn, self.Yx, self.Yxn)
+        self._pending = []  # MF-side exchanges still in flight (overlapped mode)
 
     def _swap(self, src, srcn, dst, dstn):
         if self.world == 1:
@@ -297,26 +341,59 @@ class FusedSlabStokes(SlabStokes):
         self.it = 0
         return self
 
+    def _drain(self):
+        for w in self._pending:
+            w.wait()
+        self._pending = []
+
+    def _comp(self, buf, c):
+        per = 2 * self.ym // 3  # one component's main array (doubles)
+        return buf[c * per:(c + 1) * per]
+
     def iterate(self, n_iter: int, poll: bool = True) -> dict:
+        """Overlapped (P > 1, the default): after PK the Nyquist columns and the
+        three components go out as four async all_to_alls and MI + RS of component
+        c starts as soon as its data is in, under the transfer of c + 1; MF of
+        component c is followed at once by its exchange back, under MF of c + 1;
+        PK waits for all of them.  Same arithmetic as the blocking order."""
         be = self.b
         info = {"done": False}
+        ov = self.overlap and self.world > 1
         for _ in range(int(n_iter)):
+            self._drain()
             be.fused_pk()
-            self._swap(self.Yy, self.Yyn, self.Yx, self.Yxn)
-            be.fused_rs(self.totals)
+            if ov:
+                wn = self._a2a(self.Yxn, self.Yyn)
+                ws = [self._a2a(self._comp(self.Yx, c), self._comp(self.Yy, c)) for c in range(3)]
+                wn.wait()
+                for c in range(3):
+                    ws[c].wait()
+                    be.fused_rs_part(c)
+                be.fused_totals(self.totals)
+            else:
+                self._swap(self.Yy, self.Yyn, self.Yx, self.Yxn)
+                be.fused_rs(self.totals)
             if self.world > 1:
                 self.dist.all_reduce(self.totals, group=self.group)
             be.finalize(self.totals)
-            be.fused_mf()
+            if ov:
+                for c in range(3):
+                    be.fused_mf_part(c, c == 0)
+                    self._pending.append(self._a2a(self._comp(self.Yy, c), self._comp(self.Yx, c)))
+                self._pending.append(self._a2a(self.Yyn, self.Yxn))
+            else:
+                be.fused_mf()
             self.it += 1
             if poll and (self.it % self.poll == 0 or self.it == self.cfg.max_iter):
                 info = be.read()
                 if info["done"]:
-                    return info
-            self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
+                    return info  # (an exchange still in flight is drained by end(); Y is dead once done)
+            if not ov:
+                self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
         return info
 
     def end(self) -> ConvergenceReport:
+        self._drain()
         self.b.fused_end(self.Q)  # Q^ back to T layout; u~, a, lam materialised
         rep = super().end()
         rep.meta["pipeline"] = "slab-fused"
@@ -324,7 +401,8 @@ class FusedSlabStokes(SlabStokes):
 
 
 def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalties: PenaltyParams | None = None,
-                      init_local: dict | None = None, group=None, device=None, comm=None, fused: bool | None = None):
+                      init_local: dict | None = None, group=None, device=None, comm=None, fused: bool | None = None,
+                      overlap: bool = True):
     """Device slab solve on this rank: ``solid_local`` is the rank's x-slab of the
     indicator (uint8, (N0/P, N1, N2)); returns (local state dict of CUDA tensors,
     ConvergenceReport — identical on every rank)."""
@@ -356,7 +434,7 @@ def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalt
     if fused is None:
         fused = be.fused_sizes()[0] > 0
     cls = FusedSlabStokes if fused else SlabStokes
-    solver = cls(be, dims, cfg, penalties, solid, st, group, comm=comm)
+    solver = cls(be, dims, cfg, penalties, solid, st, group, comm=comm, overlap=overlap)
     rep = solver.solve()
     t.cuda.synchronize(dev)
     shp3, shp1 = (3, hi - lo, int(dims[1]), int(dims[2])), (hi - lo, int(dims[1]), int(dims[2]))

@@ -39,7 +39,7 @@ class _RankComm:
     def _meet(self):
         self.hub.barrier.wait(timeout=300)
 
-    def all_to_all_single(self, recv, send, group=None):
+    def all_to_all_single(self, recv, send, group=None, async_op=False):
         import torch
 
         h, w = self.hub, self.hub.world
@@ -51,6 +51,7 @@ class _RankComm:
             recv[s * k:(s + 1) * k].copy_(h.slots[s][self.r * k:(self.r + 1) * k])
         torch.cuda.synchronize()
         self._meet()
+        return _Done() if async_op else None
 
     def all_reduce(self, t, group=None):
         import torch
@@ -65,6 +66,13 @@ class _RankComm:
         self._meet()
         t.copy_(tot)
         torch.cuda.synchronize()
+
+
+class _Done:
+    """Handle of an exchange the loopback already completed (async_op=True)."""
+
+    def wait(self):
+        return True
 
 
 def run_ranks(world, fn):

@@ -51,9 +51,9 @@ def test_device_slab_matches_fused_at_64(pf):
     np.testing.assert_allclose(rep.history, rref.history, rtol=1e-6, atol=1e-9 * np.abs(rref.history).max())
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world,overlap", [(2, True), (4, True), (2, False)])
 @pytest.mark.parametrize("case", ["stokes_sphere16_stiff", "stokes_sphere12_adaptive"])
-def test_device_slab_multi_rank_loopback(pf, golden, case, world):
+def test_device_slab_multi_rank_loopback(pf, golden, case, world, overlap):
     """P ranks' device backends on one GPU (tests/slab_loopback.py): every
     rank's slab offsets, zero-mode ownership and packing, against the reference."""
     from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
@@ -70,7 +70,7 @@ def test_device_slab_multi_rank_loopback(pf, golden, case, world):
 
     def rank_fn(r, comm):
         lo, hi = slab_range(n0, world, r)
-        st, rep = solve_stokes_slab(z["solid"][lo:hi], z["solid"].shape, cfg, penalties, comm=comm)
+        st, rep = solve_stokes_slab(z["solid"][lo:hi], z["solid"].shape, cfg, penalties, comm=comm, overlap=overlap)
         return {k: v.cpu().numpy() for k, v in st.items()}, rep
 
     res = run_ranks(world, rank_fn)
@@ -81,10 +81,12 @@ def test_device_slab_multi_rank_loopback(pf, golden, case, world):
         assert rel_l2(full, z[k]) <= 1e-10, k
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_fused_slab_matches_fused_pipeline(pf, world):
+@pytest.mark.parametrize("world,overlap", [(1, True), (2, True), (4, True), (2, False), (4, False)])
+def test_fused_slab_matches_fused_pipeline(pf, world, overlap):
     """The fused slab pipeline (pf_slab_fused_*) over P loopback ranks reproduces
-    the single-GPU fused pipeline: same iterations, fields to round-off."""
+    the single-GPU fused pipeline: same iterations, fields to round-off; both the
+    component-pipelined exchange (pf_slab_fused_rs_part / _mf_part) and the
+    blocking one."""
     from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
     from slab_loopback import run_ranks
 
@@ -95,7 +97,7 @@ def test_fused_slab_matches_fused_pipeline(pf, world):
 
     def rank_fn(r, comm):
         lo, hi = slab_range(64, world, r)
-        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True)
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True, overlap=overlap)
         return {k: v.cpu().numpy() for k, v in st.items()}, rep
 
     res = run_ranks(world, rank_fn)

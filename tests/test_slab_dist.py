@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _run_rank(rank, world, port, case, q):
+def _run_rank(rank, world, port, case, q, overlap=True):
     sys.path.insert(0, HERE)
     sys.path.insert(0, os.path.dirname(HERE))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -51,7 +51,7 @@ def _run_rank(rank, world, port, case, q):
         st = {k: torch.zeros(3 * L, dtype=torch.float64) for k in ("u", "u_tilde", "a", "lam")}
         st["q"] = torch.zeros(L, dtype=torch.float64)
         solid_t = torch.from_numpy(np.ascontiguousarray(solid[lo:hi], dtype=np.uint8)).reshape(-1)
-        rep = S.SlabStokes(be, dims, cfg, penalties, solid_t, st, poll_every=4).solve()
+        rep = S.SlabStokes(be, dims, cfg, penalties, solid_t, st, poll_every=4, overlap=overlap).solve()
         q.put((rank, lo, hi, {k: v.numpy().copy() for k, v in st.items()}, rep.iterations, rep.converged,
                rep.history))
     finally:
@@ -59,11 +59,11 @@ def _run_rank(rank, world, port, case, q):
             dist.destroy_process_group()
 
 
-def _solve(case, world):
+def _solve(case, world, overlap=True):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_run_rank, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run_rank, args=(r, world, port, case, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -84,12 +84,13 @@ def _gather(res, dims):
     return out
 
 
-@pytest.mark.parametrize("case,world", [("stokes_sphere16_stiff", 1), ("stokes_sphere16_stiff", 4),
-                                        ("stokes_random_trunc", 2)])
-def test_slab_driver_reproduces_reference(golden, case, world):
-    """sphere16: stiff, converged (943 it); random_trunc: 10x12x9 (odd N2), adaptive, 40 it."""
+@pytest.mark.parametrize("case,world,overlap", [("stokes_sphere16_stiff", 1, True), ("stokes_sphere16_stiff", 4, True),
+                                                ("stokes_random_trunc", 2, True), ("stokes_random_trunc", 2, False)])
+def test_slab_driver_reproduces_reference(golden, case, world, overlap):
+    """sphere16: stiff, converged (943 it); random_trunc: 10x12x9 (odd N2), adaptive, 40 it.
+    overlap = the component-pipelined async exchanges (default), else blocking."""
     z = golden(case)
-    res = _solve(case, world)
+    res = _solve(case, world, overlap)
     its = {r[4] for r in res}
     assert its == {int(z["iterations"])}, its  # every rank stops at the reference's iteration
     for r in res:
