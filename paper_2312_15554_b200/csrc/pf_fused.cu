@@ -725,10 +725,12 @@ struct PK2 {
   // TMA path (single GPU, N = 128 / 256, main tiles): each component's CP x N
   // pencil lands 64B-swizzled; the three boxes sit at the END of the padded
   // sequence region so the first FFT round's stores never reach the last box
-  static constexpr bool TMA_OK = (N == 128 || N == 256) && CP * 16 == 64;
+  // (CP = 8: 128-byte box rows, SWIZZLE_128B)
+  static constexpr int ROWB = CP * 16;  // box row bytes
+  static constexpr bool TMA_OK = (N == 128 || N == 256) && (ROWB == 64 || ROWB == 128);
   static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
   static constexpr size_t BOX = sizeof(double2) * CP * N;
-  static constexpr size_t BOX_OFF = ((REGION - 3 * BOX) / 512) * 512;
+  static constexpr size_t BOX_OFF = ((REGION - 3 * BOX) / 1024) * 1024;
   static constexpr size_t BYTES = REGION + sizeof(double2) * C::TWN + 1024;
 };
 
@@ -962,9 +964,10 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
       double2 x[A > BB ? A : BB];
       if (act && l < BB) {
 #pragma unroll
-        for (int n1 = 0; n1 < A; ++n1) {  // row e = i0, column q: 16B chunk XOR-swizzled by (e / 2) mod 4
-          const int e = BB * n1 + l;
-          x[n1] = *reinterpret_cast<const double2*>(box + (size_t)e * 64 + ((q ^ ((e >> 1) & 3)) << 4));
+        for (int n1 = 0; n1 < A; ++n1) {  // row e = i0, column q: 16B chunk XOR-swizzled by (e / 2) mod 4 (64B)
+          const int e = BB * n1 + l;       // or by e mod 8 (128B)
+          const int sw = K::ROWB == 64 ? ((e >> 1) & 3) : (e & 7);
+          x[n1] = *reinterpret_cast<const double2*>(box + (size_t)e * K::ROWB + ((q ^ sw) << 4));
         }
       }
       __syncthreads();  // this round's boxes are read before its stores may overwrite them
@@ -1260,8 +1263,8 @@ static int encode_pk_map_gen(CUtensorMap* tm, const double2* base, int N, int cp
   cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)N};
   cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, gdim, gstride, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, cp * 16 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return PF_ERR_CUDA;
