@@ -12,26 +12,40 @@
 namespace pf {
 namespace fz {
 
+// Sequences of N <= 256 points are transformed by one 8/16-lane group with the
+// two-pass scheme below.  Longer ones (N = M * 256, M = 2, 4) are M padded blocks
+// of L = 256: a radix-M stage over the whole sequence (all threads of the block)
+// plus M independent L-point transforms.  Space-domain element e = j + L b sits in
+// block b at position j (sp); spectral index k = M m + r in block r at position m
+// (kp) — the forward transform leaves the spectrum in that order and the inverse
+// takes it, so only the index maps differ from the short case.
 template <int N>
 struct Cfg {
-  static constexpr int A = (N == 64) ? 8 : 16;  // radix of pass 1 (and stride of pass-1 stores)
-  static constexpr int B = N / A;               // radix of pass 2
-  static constexpr int G = A > B ? A : B;       // lanes per FFT group
-  static constexpr int NG = 256 / G;            // groups per 256-thread block
-  static constexpr int SS = N + N / A + 1;      // padded smem sequence stride (complex)
-  static constexpr int H = N / 2;               // stored half-spectrum columns (k2 < N/2)
-  static constexpr int LOGN = N == 64 ? 6 : (N == 128 ? 7 : 8);
-  static constexpr int RSR = NG;                // rows per RS tile
-  static constexpr int CM = NG;                 // k2 columns per MF / MI tile
-  static constexpr int CP = NG / 2;             // k2 columns per PK tile
-  static constexpr int NCHM = H / CM;           // column chunks per i0 (M kernels)
-  static constexpr int NCHP = H / CP;           // column chunks per k1 (PK)
+  static constexpr int M = N > 256 ? N / 256 : 1;  // blocks of a long sequence
+  static constexpr int L = N / M;                  // length of one block transform (<= 256)
+  static constexpr int A = (L == 64) ? 8 : 16;     // radix of pass 1 (and stride of pass-1 stores)
+  static constexpr int B = L / A;                  // radix of pass 2
+  static constexpr int G = A > B ? A : B;          // lanes per FFT group
+  static constexpr int NG = 256 / G;               // groups per 256-thread block
+  static constexpr int SSL = L + L / A + 1;        // padded smem stride of one block (complex)
+  static constexpr int SS = M * SSL;               // padded smem sequence stride (complex)
+  static constexpr int H = N / 2;                  // stored half-spectrum columns (k2 < N/2)
+  static constexpr int LOGN = N == 64 ? 6 : (N == 128 ? 7 : (N == 256 ? 8 : (N == 512 ? 9 : 10)));
+  static constexpr int RSR = NG;                   // rows per RS tile
+  static constexpr int CM = NG;                    // k2 columns per MF / MI tile
+  static constexpr int CP = NG / 2;                // k2 columns per PK tile
+  static constexpr int NCHM = H / CM;              // column chunks per i0 (M kernels)
+  static constexpr int NCHP = H / CP;              // column chunks per k1 (PK)
   static constexpr int M_TILES = N * NCHM + N / CM;
   static constexpr int PK_TILES = N * NCHP + N / CP;
   static constexpr int RS_TILES = N * N / RSR;
   // compact pass-1 twiddle table: rows w^b (b = 1..3) and w^(4a) (a = 1..A/4-1), B lanes each
-  static constexpr int TWN = (3 + A / 4 - 1) * B;
-  static __device__ __forceinline__ int pad(int e) { return e + e / A; }
+  static constexpr int TWL = (3 + A / 4 - 1) * B;
+  // + for long sequences the radix-M stage's w_N^(j r), rows r = 1..M-1 of L entries
+  static constexpr int TWN = TWL + (M - 1) * L;
+  static __device__ __forceinline__ int pad(int e) { return e + e / A; }  // within one block
+  static __device__ __forceinline__ int sp(int e) { return M == 1 ? pad(e) : (e / L) * SSL + pad(e % L); }
+  static __device__ __forceinline__ int kp(int k) { return M == 1 ? pad(k) : (k % M) * SSL + pad(k / M); }
 };
 
 // cos(2 pi m / 16)
@@ -165,16 +179,22 @@ struct Dft<16, INV> {
 template <int N>
 inline void pass1_twiddles(double2* out) {
   using C = Cfg<N>;
+  constexpr int L = C::L;
   int r = 0;
   auto row = [&](int k1) {
     for (int l = 0; l < C::B; ++l) {
-      const double a = 2.0 * M_PI * (double)(l * k1) / (double)N;
+      const double a = 2.0 * M_PI * (double)(l * k1) / (double)L;
       out[r * C::B + l] = make_double2(std::cos(a), -std::sin(a));
     }
     ++r;
   };
   for (int b = 1; b < 4; ++b) row(b);
   for (int a = 1; a < C::A / 4; ++a) row(4 * a);
+  for (int rr = 1; rr < C::M; ++rr)  // radix-M stage: w_N^(j rr)
+    for (int j = 0; j < L; ++j) {
+      const double a = 2.0 * M_PI * (double)(j * rr) / (double)N;
+      out[C::TWL + (rr - 1) * L + j] = make_double2(std::cos(a), -std::sin(a));
+    }
 }
 
 // Remainder of fft_seq once pass 1's inputs are in registers: x[n1] = element
@@ -233,6 +253,58 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
     for (int n1 = 0; n1 < A; ++n1) x[n1] = s[C::pad(B * n1 + l)];
   }
   fft_seq_x<N, INV>(x, s, tw, l, active);
+}
+
+// Radix-M stage of long sequences (Cfg<N>::M > 1; no-op otherwise), all threads
+// of the block: forward = DIF butterfly + twiddle w_N^(j r) (natural order in,
+// blocks ready for their L-point transforms); inverse = conjugate twiddle +
+// inverse butterfly (after the blocks' inverse transforms).  nseq sequences of
+// stride ss (complex) from S; tw = the kernel's staged Cfg<N> table.
+template <int N, bool INV>
+__device__ __forceinline__ void radix_stage(double2* S, int nseq, int ss, const double2* tw, int t, int T) {
+  using C = Cfg<N>;
+  constexpr int M = C::M, L = C::L;
+  if constexpr (M > 1) {
+    const double2* twb = tw + C::TWL;
+    for (int idx = t; idx < nseq * L; idx += T) {
+      const int sq = idx / L, j = idx % L;
+      double2* base = S + (size_t)sq * ss + C::pad(j);
+      double2 a[M];
+#pragma unroll
+      for (int b = 0; b < M; ++b) a[b] = base[b * C::SSL];
+      if (!INV) {
+        Dft<M, false>::run(a);
+#pragma unroll
+        for (int r = 1; r < M; ++r) a[r] = cmul(a[r], twb[(r - 1) * L + j]);
+      } else {
+#pragma unroll
+        for (int r = 1; r < M; ++r) {
+          double2 w = twb[(r - 1) * L + j];
+          w.y = -w.y;
+          a[r] = cmul(a[r], w);
+        }
+        Dft<M, true>::run(a);
+      }
+#pragma unroll
+      for (int b = 0; b < M; ++b) base[b * C::SSL] = a[b];
+    }
+  }
+}
+
+// The block transforms of nseq sequences (stride ss): block (sq, b) = unit
+// u = sq M + b, units dealt to the ngr groups in rounds.  With M = 1 this is
+// exactly fft_seq on sequence g (round 0), g + ngr, ...  Every thread of the
+// block must call it (groups idle in a round still take the __syncwarp's).
+template <int N, bool INV>
+__device__ __forceinline__ void fft_units(double2* S, int nseq, int ss, const double2* tw, int g, int l, int ngr) {
+  using C = Cfg<N>;
+  const int nu = nseq * C::M;
+  for (int u0 = 0; u0 < nu; u0 += ngr) {
+    const int u = u0 + g;
+    const bool act = u < nu;
+    const int uu = act ? u : 0;
+    fft_seq<C::L, INV>(S + (size_t)(uu / C::M) * ss + (uu % C::M) * C::SSL, tw, l, act);
+  }
 }
 
 }  // namespace fz

@@ -190,19 +190,23 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
       double2 xa = sx[(2 * p) * H + k], xb = sx[(2 * p + 1) * H + k];
       if (k == 0) xa.y = xb.y = 0.0;  // C2R keeps the real part of self-conjugate modes
       double2* sp = SI + p * SS;
-      sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
-      if (k > 0) sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+      sp[C::kp(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+      if (k > 0) sp[C::kp(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
     }
-    for (int p = t; p < NP; p += T) SI[p * SS + C::pad(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
+    for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
-    fft_seq<N, true>(SI + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
+    if constexpr (C::M > 1) {
+      __syncthreads();
+      radix_stage<N, true>(SI, NP, SS, tw, t, T);
+    }
     __syncthreads();
     // (2) local projection + multipliers (pure.py:59-68) and six squared norms; a
     // lane takes both rows of a pair at one column (one 16-byte sequence access)
 #pragma unroll 2
     for (int j = 0; j < K::VPT / 2; ++j) {
       const int w = t + T * j, p = w / N, col = w % N;
-      double2* zp = SI + p * SS + C::pad(col);
+      double2* zp = SI + p * SS + C::sp(col);
       const double2 z = *zp;
       double rr[2];
 #pragma unroll
@@ -236,17 +240,21 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     __syncthreads();
     // staged inputs consumed: prefetch the next tile while this one finishes
     if (t == 0 && tile + (int)gridDim.x < NT) rs_issue<N, SL>(tile + gridDim.x, B, st, sst, sx, sxn, sh, &mbar);
-    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    if constexpr (C::M > 1) {
+      radix_stage<N, false>(SF, NP, SS, tw, t, T);
+      __syncthreads();
+    }
+    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     __syncthreads();
     // (3) separate the two real transforms of each row pair, store X-space rows of R
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
-      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      const double2 zk = SF[p * SS + C::kp(k)], zm = SF[p * SS + C::kp((N - k) & (N - 1))];
       XR[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
       XR[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
     for (int p = t; p < NP; p += T) {
-      const double2 z = SF[p * SS + C::pad(H)];
+      const double2 z = SF[p * SS + C::kp(H)];
       XRn[row0 + 2 * p] = make_double2(z.x, 0.0);
       XRn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
@@ -299,20 +307,24 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
     mbar_wait(&mbar, phase);
     for (int v = t; v < V; v += T) {
       const int row = v / N, col = v % N;
-      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::pad(col))[row & 1] = sst[v];
+      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::sp(col))[row & 1] = sst[v];
     }
     __syncthreads();
     if (t == 0 && tile + (int)gridDim.x < NT) issue(tile + gridDim.x);
-    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    if constexpr (C::M > 1) {
+      radix_stage<N, false>(SF, NP, SS, tw, t, T);
+      __syncthreads();
+    }
+    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     __syncthreads();
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
-      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      const double2 zk = SF[p * SS + C::kp(k)], zm = SF[p * SS + C::kp((N - k) & (N - 1))];
       XU[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
       XU[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
     for (int p = t; p < NP; p += T) {
-      const double2 z = SF[p * SS + C::pad(H)];
+      const double2 z = SF[p * SS + C::kp(H)];
       XUn[row0 + 2 * p] = make_double2(z.x, 0.0);
       XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
@@ -460,12 +472,16 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
       double2 xa = sx[(2 * p) * H + k], xb = sx[(2 * p + 1) * H + k];
       if (k == 0) xa.y = xb.y = 0.0;
       double2* sp = SI + p * SS;
-      sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
-      if (k > 0) sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+      sp[C::kp(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+      if (k > 0) sp[C::kp(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
     }
-    for (int p = t; p < NP; p += T) SI[p * SS + C::pad(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
+    for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
-    fft_seq<N, true>(SI + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
+    if constexpr (C::M > 1) {
+      __syncthreads();
+      radix_stage<N, true>(SI, NP, SS, tw, t, T);
+    }
     __syncthreads();
     // (2) local step; pore: u~' = u', a' = 0, lam' = lam (only u' is stored).
     // A lane takes both rows of a pair at one column: one 16-byte access of the
@@ -474,7 +490,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
 #pragma unroll 2
     for (int j = 0; j < K::VPT / 2; ++j) {
       const int w = t + T * j, p = w / N, col = w % N;
-      double2* zp = SI + p * SS + C::pad(col);
+      double2* zp = SI + p * SS + C::sp(col);
       const double2 z = *zp;
       double rr[2];
 #pragma unroll
@@ -511,16 +527,20 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     __syncthreads();
     if (t == 0 && has_next)
       rsc_issue<N, SL>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[phase ^ 1u], ro);
-    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    if constexpr (C::M > 1) {
+      radix_stage<N, false>(SF, NP, SS, tw, t, T);
+      __syncthreads();
+    }
+    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     __syncthreads();
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
-      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      const double2 zk = SF[p * SS + C::kp(k)], zm = SF[p * SS + C::kp((N - k) & (N - 1))];
       XR[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
       XR[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
     for (int p = t; p < NP; p += T) {
-      const double2 z = SF[p * SS + C::pad(H)];
+      const double2 z = SF[p * SS + C::kp(H)];
       XRn[row0 + 2 * p] = make_double2(z.x, 0.0);
       XRn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
@@ -565,21 +585,25 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
       const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
       double val = u[(int64_t)c * n + row0 * N + v];
       if (solid) val = cp.ut[(int64_t)c * cp.ns + o0 + segb + __popc(mask & ((1u << lane) - 1u))];
-      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::pad(col))[row & 1] = val;
+      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::sp(col))[row & 1] = val;
     }
     __syncthreads();
-    fft_seq<N, false>(SF + (g < NP ? g : 0) * SS, tw, l, g < NP);
+    if constexpr (C::M > 1) {
+      radix_stage<N, false>(SF, NP, SS, tw, t, T);
+      __syncthreads();
+    }
+    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     __syncthreads();
     double2* XU = B.XU + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XUn = B.XUn + (size_t)c * (SL ? B.l0 : N) * N;
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
-      const double2 zk = SF[p * SS + C::pad(k)], zm = SF[p * SS + C::pad((N - k) & (N - 1))];
+      const double2 zk = SF[p * SS + C::kp(k)], zm = SF[p * SS + C::kp((N - k) & (N - 1))];
       XU[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
       XU[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
     for (int p = t; p < NP; p += T) {
-      const double2 z = SF[p * SS + C::pad(H)];
+      const double2 z = SF[p * SS + C::kp(H)];
       XUn[row0 + 2 * p] = make_double2(z.x, 0.0);
       XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
@@ -713,7 +737,8 @@ struct PK2 {
 #ifdef PF_PK_CP
   static constexpr int CP = PF_PK_CP;
 #else
-  static constexpr int CP = (NGP % 3 == 0) ? NGP / 3 : NGP / 2;
+  // (a long sequence takes M groups: NGP / M sequences per round)
+  static constexpr int CP = ((NGP / C::M) % 3 == 0) ? NGP / C::M / 3 : NGP / C::M / 2;
 #endif
   static constexpr int NSEQ = 3 * CP;
   static constexpr int NCH = C::H / CP;
@@ -730,7 +755,11 @@ struct PK2 {
   static constexpr bool TMA_OK = (N == 128 || N == 256) && (ROWB == 64 || ROWB == 128);
   static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
   static constexpr size_t BOX = sizeof(double2) * CP * N;
-  static constexpr size_t BOX_OFF = ((REGION - 3 * BOX) / 1024) * 1024;
+  static constexpr size_t BOX_AL = ROWB == 128 ? 1024 : 512;  // swizzle-atom alignment of a box
+  static constexpr size_t BOX_OFF = ((REGION - 3 * BOX) / BOX_AL) * BOX_AL;
+  // the last box must lie beyond what the first FFT round stores (NGP sequences)
+  static_assert(!TMA_OK || NSEQ <= NGP || BOX_OFF + (NSEQ / CP - 1) * BOX >= sizeof(double2) * NGP * SS,
+                "PK TMA boxes overlap the first round's sequences");
   static constexpr size_t BYTES = REGION + sizeof(double2) * C::TWN + 1024;
 };
 
@@ -738,12 +767,12 @@ template <int N>
 struct M2 {
   using C = Cfg<N>;
   static constexpr int T = 128;
-  static constexpr int NGM = T / C::G;        // groups = sequences per tile
-  static constexpr int CM = NGM;              // columns per tile
+  static constexpr int NGM = T / C::G;        // groups = block transforms per tile
+  static constexpr int CM = NGM / C::M;       // columns (sequences) per tile
   static constexpr int NCH = C::H / CM;
   static constexpr int TPC = N * NCH + N / CM;  // tiles per component
   static constexpr int TILES = 3 * TPC;
-  static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
+  static constexpr size_t SEQ = sizeof(double2) * CM * C::SS;
   // TMA path (single GPU, N = 128 / 256, main tiles): the CM x N tile lands
   // 128B-swizzled in a 1 KB-aligned region that the padded sequences then reuse
   static constexpr bool TMA_OK = (N == 128 || N == 256) && CM * 16 == 128;
@@ -842,10 +871,10 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
     if (INV) {
       const size_t o = yoff_of(e, q);
-      cp16(S + q * SS + C::pad(e), nyq ? B.Yxn + o : B.Yx + o);
+      cp16(S + q * SS + C::kp(e), nyq ? B.Yxn + o : B.Yx + o);
     } else {
       const size_t o = off_of(e, q);
-      cp16(S + q * SS + C::pad(e), nyq ? B.XRn + o : B.XR + o);
+      cp16(S + q * SS + C::sp(e), nyq ? B.XRn + o : B.XR + o);
     }
   }
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
@@ -858,18 +887,30 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
         const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
         const size_t o = off_of(e, q);
         const double2 vu = nyq ? B.XUn[o] : B.XU[o];
-        double2* p = S + q * SS + C::pad(e);
+        double2* p = S + q * SS + C::sp(e);
         *p = make_double2(p->x + db * vu.x, p->y + db * vu.y);
       }
       __syncthreads();
     }
   }
-  fft_seq<N, INV>(S + g * SS, tw, l, true);
+  if constexpr (C::M > 1) {
+    if (!INV) {
+      radix_stage<N, false>(S, CM, SS, tw, t, T);
+      __syncthreads();
+    }
+    fft_units<N, INV>(S, CM, SS, tw, g, l, K::NGM);
+    if (INV) {
+      __syncthreads();
+      radix_stage<N, true>(S, CM, SS, tw, t, T);
+    }
+  } else {
+    fft_seq<N, INV>(S + g * SS, tw, l, true);
+  }
   __syncthreads();
   }
   for (int idx = t; idx < N * CM; idx += T) {
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
-    const double2 v = S[q * SS + C::pad(e)];
+    const double2 v = S[q * SS + (INV ? C::sp(e) : C::kp(e))];
     if (!INV) {
       const size_t o = yoff_of(e, q);
       if (nyq) B.Yxn[o] = v; else B.Yx[o] = v;
@@ -934,7 +975,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
     for (int idx = t; idx < 3 * N * CP; idx += T) {
       const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
       const size_t o = yoff(c, i0, q);
-      cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+      cp16(S + (c * CP + q) * SS + C::sp(i0), nyq ? B.Yn + o : B.Y + o);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
@@ -976,11 +1017,11 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   } else {
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
-      const int sq = g + r * K::NGP;
-      fft_seq<N, false>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
+    if constexpr (C::M > 1) {
+      radix_stage<N, false>(S, NSEQ, SS, tw, t, T);
+      __syncthreads();
     }
+    fft_units<N, false>(S, NSEQ, SS, tw, g, l, K::NGP);
   }
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
@@ -1009,7 +1050,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
     double2 r[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double2 rc = S[(c * CP + q) * SS + C::pad(k0)];
+      const double2 rc = S[(c * CP + q) * SS + C::kp(k0)];
       r[c] = make_double2(kc[c] * qq.y + rc.x, -(kc[c] * qq.x) + rc.y);  // -i k q + R^
       if (zero) r[c].x = r[c].x + P.dn * P.g[c];                          // n g_p at k = 0
     }
@@ -1029,7 +1070,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
       double2 u = csub(r[c], cscale(kc[c], corr));
       u = make_double2(u.x * invA, u.y * invA);
       dv = cadd(dv, cik(kc[c], u));
-      S[(c * CP + q) * SS + C::pad(k0)] = make_double2(u.x * P.inv_n, u.y * P.inv_n);
+      S[(c * CP + q) * SS + C::kp(k0)] = make_double2(u.x * P.inv_n, u.y * P.inv_n);
     }
     double2 qn = csub(qq, cscale(beta, dv));
     if (zero) qn = make_double2(0.0, 0.0);
@@ -1041,16 +1082,16 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
     B.D[tbase + m] = dv;
   }
   __syncthreads();
-#pragma unroll
-  for (int r = 0; r < (NSEQ + K::NGP - 1) / K::NGP; ++r) {
-    const int sq = g + r * K::NGP;
-    fft_seq<N, true>(S + (sq < NSEQ ? sq : 0) * SS, tw, l, sq < NSEQ);
+  fft_units<N, true>(S, NSEQ, SS, tw, g, l, K::NGP);
+  if constexpr (C::M > 1) {
+    __syncthreads();
+    radix_stage<N, true>(S, NSEQ, SS, tw, t, T);
   }
   __syncthreads();
   for (int idx = t; idx < 3 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
     const size_t o = yoff(c, i0, q);
-    const double2 v = S[(c * CP + q) * SS + C::pad(i0)];
+    const double2 v = S[(c * CP + q) * SS + C::sp(i0)];
     if (nyq) B.Yn[o] = v; else B.Y[o] = v;
   }
   block_sum<3>(acc);
@@ -1154,7 +1195,7 @@ bool fused_supported(const pf_plan* p) {
   if (p->g.d != 3) return false;
   const int N = p->g.n[0];
   if (p->g.n[1] != N || p->g.n[2] != N) return false;
-  return N == 64 || N == 128 || N == 256;
+  return N == 64 || N == 128 || N == 256 || N == 512;
 }
 
 template <int N>
@@ -1282,7 +1323,7 @@ int fused_ensure(pf_plan* p) {
   // X: 6 comps (XU 3, XR 3); Y: 3; Q, D: 1 each
   const size_t elems = 11 * (main1 + nyq1) + N;
   const int nb_rs = kRsMaxBlocks;
-  const int nb_pk = (N == 64) ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : fz::PK2<256>::TILES);
+  const int nb_pk = (N == 64) ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : (N == 256 ? fz::PK2<256>::TILES : fz::PK2<512>::TILES));
   const size_t part = 6 * (size_t)nb_rs + 3 * (size_t)nb_pk;
   f->bytes = elems * sizeof(double2) + part * sizeof(double);
   PF_CK_CUDA(cudaMalloc(&f->mem, f->bytes));
@@ -1317,11 +1358,12 @@ int fused_ensure(pf_plan* p) {
   f->b.Yxn = f->b.Yn;
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
-  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : fz::Cfg<512>::TWN)));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
-    default: fz::pass1_twiddles<256>(tw.data()); break;
+    case 256: fz::pass1_twiddles<256>(tw.data()); break;
+    default: fz::pass1_twiddles<512>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   if (N == 128 || N == 256) {
@@ -1354,7 +1396,8 @@ int fused_ensure(pf_plan* p) {
   switch (N) {
     case 64: PF_CK(set_attrs<64>(f)); break;
     case 128: PF_CK(set_attrs<128>(f)); break;
-    default: PF_CK(set_attrs<256>(f)); break;
+    case 256: PF_CK(set_attrs<256>(f)); break;
+    default: PF_CK(set_attrs<512>(f)); break;
   }
   p->fused = f;
   p->scratch_bytes += f->bytes;
@@ -1383,7 +1426,8 @@ static int to_tilemajor(int N, const double2* src, double2* dst, double scale, b
   switch (N) {
     case 64: fz::k_tilemajor<64><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
     case 128: fz::k_tilemajor<128><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
-    default: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
+    case 256: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
+    default: fz::k_tilemajor<512><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
@@ -1473,7 +1517,8 @@ int fused_setup(pf_plan* p) {
   switch (N) {
     case 64: fz::k_split_yx<64><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
     case 128: fz::k_split_yx<128><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
-    default: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+    case 256: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+    default: fz::k_split_yx<512><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   (void)NN;
@@ -1481,7 +1526,8 @@ int fused_setup(pf_plan* p) {
   switch (N) {
     case 64: return compact_setup_t<64>(p, f);
     case 128: return compact_setup_t<128>(p, f);
-    default: return compact_setup_t<256>(p, f);
+    case 256: return compact_setup_t<256>(p, f);
+    default: return compact_setup_t<512>(p, f);
   }
 }
 
@@ -1498,7 +1544,8 @@ int fused_finish(pf_plan* p) {
     switch (N) {
       case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
       case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
-      default: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      case 256: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      default: fz::k_compact_move<512><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
     }
     PF_CK_CUDA(cudaGetLastError());
   }
@@ -1566,7 +1613,8 @@ int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {
   switch (fp_of(p)->N) {
     case 64: return enqueue_fused_t<64>(p, ev);
     case 128: return enqueue_fused_t<128>(p, ev);
-    default: return enqueue_fused_t<256>(p, ev);
+    case 256: return enqueue_fused_t<256>(p, ev);
+    default: return enqueue_fused_t<512>(p, ev);
   }
 }
 
@@ -1577,10 +1625,10 @@ int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {
 // k1off) of Q^, D^; Y lives in the two exchange-native layouts of Bufs, whose
 // buffers the caller owns and all-to-alls between PK and the axis-1 passes.
 static bool fslab_shape_ok(int N, int l0, int l1) {
-  if (N != 64 && N != 128 && N != 256) return false;
+  if (N != 64 && N != 128 && N != 256 && N != 512) return false;
   if (l0 <= 0 || l1 <= 0 || (l1 & (l1 - 1)) || N % l0 || N % l1) return false;
-  const int cm = N == 64 ? fz::M2<64>::CM : (N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM);
-  const int cp = N == 64 ? fz::PK2<64>::CP : (N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP);
+  const int cm = N == 64 ? fz::M2<64>::CM : (N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : fz::M2<512>::CM));
+  const int cp = N == 64 ? fz::PK2<64>::CP : (N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : fz::PK2<512>::CP));
   return l0 % cm == 0 && l1 % cp == 0;
 }
 
@@ -1630,7 +1678,7 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   const size_t H = N / 2;
   const size_t xm = (size_t)l0 * N * H, xn = (size_t)l0 * N;  // X per component
   const size_t qd = (size_t)l1 * N * H + (size_t)l1 * N;      // Q^ / D^ (tile-major, y-slab)
-  const int pk_max = N == 64 ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : fz::PK2<256>::TILES);
+  const int pk_max = N == 64 ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : (N == 256 ? fz::PK2<256>::TILES : fz::PK2<512>::TILES));
   const size_t elems = 6 * (xm + xn) + 2 * qd + N;
   const size_t part = 6 * (size_t)kRsMaxBlocks + 3 * (size_t)pk_max;
   f->bytes = elems * sizeof(double2) + part * sizeof(double);
@@ -1665,11 +1713,12 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   f->b.nc = 3;
   f->b.pst = 0;  // set per launch (nb_rs)
   f->b.poff = 0;
-  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : fz::Cfg<512>::TWN)));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
-    default: fz::pass1_twiddles<256>(tw.data()); break;
+    case 256: fz::pass1_twiddles<256>(tw.data()); break;
+    default: fz::pass1_twiddles<512>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   // axes-(1, 2) transform of this slab's R at setup
@@ -1693,7 +1742,8 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   switch (N) {
     case 64: PF_CK(set_attrs<64>(f)); break;
     case 128: PF_CK(set_attrs<128>(f)); break;
-    default: PF_CK(set_attrs<256>(f)); break;
+    case 256: PF_CK(set_attrs<256>(f)); break;
+    default: PF_CK(set_attrs<512>(f)); break;
   }
   p->scratch_bytes += f->bytes + ws + sizeof(double2) * 3 * (size_t)l0 * N * (H + 1);
   return PF_OK;
@@ -1712,13 +1762,15 @@ int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R
   switch (N) {
     case 64: fz::k_split_yx<64><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
     case 128: fz::k_split_yx<128><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
-    default: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+    case 256: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+    default: fz::k_split_yx<512><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   switch (N) {
     case 64: PF_CK(compact_setup_t<64>(p, f)); break;
     case 128: PF_CK(compact_setup_t<128>(p, f)); break;
-    default: PF_CK(compact_setup_t<256>(p, f)); break;
+    case 256: PF_CK(compact_setup_t<256>(p, f)); break;
+    default: PF_CK(compact_setup_t<512>(p, f)); break;
   }
   f->lam_pore = p->sc.lam_pore_sq;  // local: enters the totals before the all-reduce
   p->sc.lam_pore_sq = 0.0;
@@ -1818,7 +1870,8 @@ int fused_slab_pk(pf_plan* p) {
   switch (fp_of(p)->N) {
     case 64: return fslab_pk_t<64>(p);
     case 128: return fslab_pk_t<128>(p);
-    default: return fslab_pk_t<256>(p);
+    case 256: return fslab_pk_t<256>(p);
+    default: return fslab_pk_t<512>(p);
   }
 }
 
@@ -1826,7 +1879,8 @@ int fused_slab_pk(pf_plan* p) {
   switch (fp_of(p)->N) {                  \
     case 64: return fn<64>(__VA_ARGS__);  \
     case 128: return fn<128>(__VA_ARGS__); \
-    default: return fn<256>(__VA_ARGS__); \
+    case 256: return fn<256>(__VA_ARGS__); \
+    default: return fn<512>(__VA_ARGS__); \
   }
 
 int fused_slab_rs(pf_plan* p, double* totals) { PF_FSLAB_DISPATCH(fslab_rs_t, p, 0, 3, totals) }
@@ -1847,7 +1901,8 @@ int fused_slab_end(pf_plan* p, double2* Tq) {
     switch (N) {
       case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
       case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
-      default: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      case 256: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      default: fz::k_compact_move<512><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
     }
     PF_CK_CUDA(cudaGetLastError());
   }

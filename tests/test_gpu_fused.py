@@ -171,3 +171,27 @@ def torch_pore(ind, like):
     import torch
 
     return torch.from_numpy(ind.values == 0).to(like.device)
+
+
+@pytest.mark.parametrize("compact", [True, False])
+def test_fused_long_sequences_512_match_cufft_pipeline(pf, compact):
+    """N = 512: every axis transform is two 256-point block transforms plus a
+    radix-2 stage (pf_fft.cuh radix_stage / fft_units).  A truncated adaptive
+    solve on the fused pipeline agrees with the cuFFT pipeline (iterations,
+    fields to round-off, history)."""
+    import torch
+
+    ind = pf.random_packing_geometry(512, seed=2)
+    cfg = pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=(0.3, 1.0, -0.5), max_iter=4)
+    a, ra = pf.solve_stokes_device(ind, cfg, pipeline="fused", compact=compact)
+    assert ra.meta["pipeline"] == ("fused-compact" if compact else "fused")
+    ah = {k: getattr(a, k).cpu().numpy() for k in ("u", "u_tilde", "q", "a", "lam")}
+    del a
+    torch.cuda.empty_cache()
+    b, rb = pf.solve_stokes_device(ind, cfg, pipeline="cufft")
+    assert rb.meta["pipeline"] == "cufft" and ra.iterations == rb.iterations == 4
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(ah[k], getattr(b, k).cpu().numpy()) <= FIELD_TOL, k
+    _hist_close(ra.history, rb.history)
+    del b
+    torch.cuda.empty_cache()
