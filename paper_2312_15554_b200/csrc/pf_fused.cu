@@ -775,7 +775,9 @@ struct M2 {
   static constexpr size_t SEQ = sizeof(double2) * CM * C::SS;
   // TMA path (single GPU, N = 128 / 256, main tiles): the CM x N tile lands
   // 128B-swizzled in a 1 KB-aligned region that the padded sequences then reuse
-  static constexpr bool TMA_OK = (N == 128 || N == 256) && CM * 16 == 128;
+  // (N = 512: 64-byte rows, two 256-row boxes, single GPU only)
+  static constexpr bool TMA_OK = ((N == 128 || N == 256) && CM * 16 == 128) || (N == 512 && CM * 16 == 64);
+  static constexpr int ROWB = CM * 16;
   static constexpr size_t TILE = sizeof(double2) * CM * N;
   static constexpr size_t REGION = SEQ > TILE ? SEQ : TILE;
   static constexpr size_t BYTES_INV = sizeof(double2) * C::TWN + REGION + 1024;
@@ -814,14 +816,25 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
                : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
   constexpr bool TMA = K::TMA_OK && PF_M_TMA;
-  if (TMA && !nyq) {
+  if (TMA && !nyq && (C::M == 1 || !SL)) {
     // one 2D bulk tensor copy of the (N rows x CM columns) tile, 128B-swizzled
+    // (long sequences: M copies of 256 rows, 64B-swizzled)
     __shared__ uint64_t mbar;
     if (t == 0) {
       mbar_init(&mbar);
       mbar_expect(&mbar, (uint32_t)K::TILE);
       const int x0 = 2 * ch * CM;  // doubles
-      if (SL && INV) {
+      if constexpr (C::M > 1) {
+#pragma unroll
+        for (int b = 0; b < C::M; ++b) {
+          const int y0 = (c * l0 + i0) * N + b * C::L;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+              "[%4];" ::"r"(su32(reg + b * C::L * K::ROWB)),
+              "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(y0), "r"(su32(&mbar))
+              : "memory");
+        }
+      } else if (SL && INV) {
         // x-slab Y [c][r][i0][k1 - r l1][k2]: a 5D box (16 doubles, l1, 1, P, 1) whose
         // rows come out in k1 = r l1 + kl order
         asm volatile(
@@ -842,8 +855,61 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     __syncthreads();
     mbar_wait(&mbar, 0);
     constexpr int A = C::A, BB = C::B;
-    double2 x[A > BB ? A : BB];
     const unsigned char* tile = reg;
+    // 16-byte chunk q of tile row e (64B swizzle: chunk ^ (e / 2) mod 4; 128B: ^ e mod 8)
+    auto at = [&](int e, int q) -> double2 {
+      const int sw = K::ROWB == 64 ? ((e >> 1) & 3) : (e & 7);
+      return *reinterpret_cast<const double2*>(tile + (size_t)e * K::ROWB + ((q ^ sw) << 4));
+    };
+    if constexpr (C::M > 1) {
+      if (INV) {
+        // block transform unit g = (column q, block r): its elements are rows e = M p + r
+        const int q = g / C::M, r = g % C::M;
+        double2 x[A > BB ? A : BB];
+        if (l < BB) {
+#pragma unroll
+          for (int n1 = 0; n1 < A; ++n1) x[n1] = at(C::M * (BB * n1 + l) + r, q);
+        }
+        __syncthreads();  // the tile is read
+        fft_seq_x<C::L, true>(x, S + q * SS + r * C::SSL, tw, l, true);
+        __syncthreads();
+        radix_stage<N, true>(S, CM, SS, tw, t, T);
+      } else {
+        // forward: the radix-M stage straight from the tile into registers, then
+        // into the padded sequences once every thread has read its rows
+        constexpr int IT = CM * C::L / T;
+        static_assert(CM * C::L % T == 0, "radix items per thread");
+        double2 a[IT][C::M];
+        const double db = ctrl->db;
+        const double2* twb = tw + C::TWL;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int idx = t + T * it, q = idx % CM, j = idx / CM;
+#pragma unroll
+          for (int b = 0; b < C::M; ++b) {
+            a[it][b] = at(j + C::L * b, q);
+            if (db != 0.0) {  // rare: b changed this iteration; XU holds X(u~') (k_rsfix)
+              const double2 vu = B.XU[off_of(j + C::L * b, q)];
+              a[it][b] = make_double2(a[it][b].x + db * vu.x, a[it][b].y + db * vu.y);
+            }
+          }
+          Dft<C::M, false>::run(a[it]);
+#pragma unroll
+          for (int r = 1; r < C::M; ++r) a[it][r] = cmul(a[it][r], twb[(r - 1) * C::L + j]);
+        }
+        __syncthreads();  // the tile is read
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int idx = t + T * it, q = idx % CM, j = idx / CM;
+#pragma unroll
+          for (int b = 0; b < C::M; ++b) S[q * SS + b * C::SSL + C::pad(j)] = a[it][b];
+        }
+        __syncthreads();
+        fft_units<N, false>(S, CM, SS, tw, g, l, K::NGM);
+      }
+      __syncthreads();
+    } else {
+    double2 x[A > BB ? A : BB];
     if (l < BB) {
 #pragma unroll
       for (int n1 = 0; n1 < A; ++n1) {
@@ -864,6 +930,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     __syncthreads();  // the tile is read: the padded sequences may now overwrite it
     fft_seq_x<N, INV>(x, S + g * SS, tw, l, true);
     __syncthreads();
+    }
   } else {
   // element mapping: main tiles walk (e, q) with q fastest (contiguous columns);
   // Nyquist tiles walk (q, e) with e fastest (contiguous rows).
@@ -1265,11 +1332,11 @@ static int encode_axis1_rows(CUtensorMap* tm, const double2* base, int N, int cm
   const int H = N / 2;
   cuuint64_t gdim[2] = {(cuuint64_t)2 * H, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)H * sizeof(double2)};
-  cuuint32_t box[2] = {(cuuint32_t)2 * cm, (cuuint32_t)N};
+  cuuint32_t box[2] = {(cuuint32_t)2 * cm, (cuuint32_t)(N > 256 ? 256 : N)};  // (box rows <= 256)
   cuuint32_t es[2] = {1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, gdim, gstride, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, cm * 16 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return PF_ERR_CUDA;
@@ -1371,6 +1438,9 @@ int fused_ensure(pf_plan* p) {
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
     PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP, 3));
+  } else if (N == 512) {  // axis-1 passes only (two 256-row boxes per tile)
+    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, fz::M2<512>::CM, 3));
+    PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, fz::M2<512>::CM, 3));
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
