@@ -116,6 +116,11 @@ template <int R, bool INV>
 struct Dft;
 
 template <bool INV>
+struct Dft<1, INV> {
+  static __device__ __forceinline__ void run(double2*) {}
+};
+
+template <bool INV>
 struct Dft<2, INV> {
   static __device__ __forceinline__ void run(double2* x) {
     const double2 a = x[0], b = x[1];

@@ -59,6 +59,18 @@
 #ifndef PF_PK_THREADS
 #define PF_PK_THREADS 128
 #endif
+#ifndef PF_PK512_T  // PK at N = 512: threads, columns per tile, min blocks per SM (measured:
+#define PF_PK512_T 192  // 3.85 ms vs 4.06 at 128 threads / 2 columns / 3 blocks)
+#endif
+#ifndef PF_PK512_CP
+#define PF_PK512_CP 4
+#endif
+#ifndef PF_PK512_MINB
+#define PF_PK512_MINB 2
+#endif
+#ifndef PF_RS512_T  // RS threads at N = 512 (one row pair per tile: 2 block transforms of 16 lanes)
+#define PF_RS512_T 64  // (measured 3.93 ms vs 4.38 at 32 and 4.48 at 128)
+#endif
 
 namespace pf {
 namespace fz {
@@ -108,7 +120,7 @@ struct RS2 {
   // threads per block: one FFT group per row pair (every thread FFT-active) for
   // N <= 128; for N = 256 one group per row (measured: 128^3 RS 0.071 vs 0.088 ms,
   // 256^3 0.483 vs 0.512 ms the other way round)
-  static constexpr int T = R * C::G / (PF_RS_HALFT(N) ? 2 : 1);
+  static constexpr int T = N == 512 ? PF_RS512_T : R * C::G / (PF_RS_HALFT(N) ? 2 : 1);
   static constexpr int V = R * N;               // voxels per tile
   static constexpr int VPT = V / T;             // voxels per thread
   static constexpr int NP = R / 2;              // inverse sequences (two rows each)
@@ -731,14 +743,15 @@ __global__ void __launch_bounds__(kThreads) k_pore_a_lam(int64_t n, const uint8_
 template <int N>
 struct PK2 {
   using C = Cfg<N>;
-  static constexpr int T = PF_PK_THREADS;
+  static constexpr int T = N == 512 ? PF_PK512_T : PF_PK_THREADS;
+  static constexpr int MINB = N == 512 ? PF_PK512_MINB : PF_PK_MINB;
   static constexpr int NGP = T / C::G;
   // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
 #ifdef PF_PK_CP
   static constexpr int CP = PF_PK_CP;
 #else
   // (a long sequence takes M groups: NGP / M sequences per round)
-  static constexpr int CP = ((NGP / C::M) % 3 == 0) ? NGP / C::M / 3 : NGP / C::M / 2;
+  static constexpr int CP = N == 512 ? PF_PK512_CP : (((NGP / C::M) % 3 == 0) ? NGP / C::M / 3 : NGP / C::M / 2);
 #endif
   static constexpr int NSEQ = 3 * CP;
   static constexpr int NCH = C::H / CP;
@@ -752,14 +765,19 @@ struct PK2 {
   // sequence region so the first FFT round's stores never reach the last box
   // (CP = 8: 128-byte box rows, SWIZZLE_128B)
   static constexpr int ROWB = CP * 16;  // box row bytes
-  static constexpr bool TMA_OK = (N == 128 || N == 256) && (ROWB == 64 || ROWB == 128);
+  static constexpr bool TMA_OK = ((N == 128 || N == 256) && (ROWB == 64 || ROWB == 128)) || (N == 512 && ROWB == 64);
   static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
   static constexpr size_t BOX = sizeof(double2) * CP * N;
   static constexpr size_t BOX_AL = ROWB == 128 ? 1024 : 512;  // swizzle-atom alignment of a box
   static constexpr size_t BOX_OFF = ((REGION - 3 * BOX) / BOX_AL) * BOX_AL;
   // the last box must lie beyond what the first FFT round stores (NGP sequences)
-  static_assert(!TMA_OK || NSEQ <= NGP || BOX_OFF + (NSEQ / CP - 1) * BOX >= sizeof(double2) * NGP * SS,
+  static_assert(!TMA_OK || C::M > 1 || NSEQ <= NGP || BOX_OFF + (NSEQ / CP - 1) * BOX >= sizeof(double2) * NGP * SS,
                 "PK TMA boxes overlap the first round's sequences");
+  // long sequences: component c's sequences, written after its boxes are read,
+  // must not reach the boxes of component c + 1
+  static_assert(!TMA_OK || C::M == 1 || (sizeof(double2) * CP * SS <= BOX_OFF + BOX &&
+                                         sizeof(double2) * 2 * CP * SS <= BOX_OFF + 2 * BOX),
+                "PK TMA boxes overlap the sequences of the previous component");
   static constexpr size_t BYTES = REGION + sizeof(double2) * C::TWN + 1024;
 };
 
@@ -1002,7 +1020,7 @@ struct SpecArgs {
 // registers before the forward FFTs.
 
 template <int N, bool SL>
-__global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl,
+__global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl,
                                                               const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = PK2<N>;
@@ -1025,12 +1043,22 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
     return nyq ? (size_t)(i0 * 3 + c) * l1 + k1b + q : ((size_t)(c * N + i0) * l1 + k1) * H + ch * CP + q;
   };
   constexpr bool TMA = K::TMA_OK && PF_PK_TMA;
-  const bool tma = TMA && !nyq;
+  const bool tma = TMA && !nyq && (C::M == 1 || !SL);
   __shared__ uint64_t mbar;
   if (tma) {
     if (t == 0) {  // three 3D tensor copies: component c's (CP columns x N rows i0) pencil
       mbar_init(&mbar);
       mbar_expect(&mbar, (uint32_t)(3 * K::BOX));
+      if constexpr (C::M > 1) {  // (long sequences: M copies of 256 rows per component)
+        for (int c = 0; c < 3; ++c)
+          for (int b = 0; b < C::M; ++b)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4}], [%5];" ::"r"(su32(reg + K::BOX_OFF + c * K::BOX + b * C::L * K::ROWB)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(k1), "r"(c * N + b * C::L),
+                "r"(su32(&mbar))
+                : "memory");
+      } else
       for (int c = 0; c < 3; ++c)
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -1059,7 +1087,44 @@ __global__ void __launch_bounds__(PK2<N>::T, PF_PK_MINB) k_pk(Bufs B, SpecArgs P
   }
 #endif
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
-  if (tma) {
+  if (tma && C::M > 1) {
+    __syncthreads();  // mbarrier initialised
+    mbar_wait(&mbar, 0);
+    // radix-M stage straight from the boxes, one component at a time: component
+    // c's boxes into registers, then its sequences (which reach no later box)
+    constexpr int IT = (CP * C::L + T - 1) / T;
+    const double2* twb = tw + C::TWL;
+    for (int c = 0; c < 3; ++c) {
+      const unsigned char* box = reg + K::BOX_OFF + c * K::BOX;
+      double2 a[IT][C::M];
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int idx = t + T * it, q = idx % CP, j = idx / CP;
+        if (idx < CP * C::L) {
+#pragma unroll
+          for (int b = 0; b < C::M; ++b) {
+            const int e = j + C::L * b;
+            const int sw = K::ROWB == 64 ? ((e >> 1) & 3) : (e & 7);
+            a[it][b] = *reinterpret_cast<const double2*>(box + (size_t)e * K::ROWB + ((q ^ sw) << 4));
+          }
+          Dft<C::M, false>::run(a[it]);
+#pragma unroll
+          for (int r = 1; r < C::M; ++r) a[it][r] = cmul(a[it][r], twb[(r - 1) * C::L + j]);
+        }
+      }
+      __syncthreads();  // component c's boxes are read
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int idx = t + T * it, q = idx % CP, j = idx / CP;
+        if (idx < CP * C::L) {
+#pragma unroll
+          for (int b = 0; b < C::M; ++b) S[(c * CP + q) * SS + b * C::SSL + C::pad(j)] = a[it][b];
+        }
+      }
+    }
+    __syncthreads();
+    fft_units<N, false>(S, NSEQ, SS, tw, g, l, K::NGP);
+  } else if (tma) {
     __syncthreads();  // mbarrier initialised
     mbar_wait(&mbar, 0);
     constexpr int A = C::A, BB = C::B;
@@ -1368,7 +1433,7 @@ static int encode_pk_map_gen(CUtensorMap* tm, const double2* base, int N, int cp
   const int H = N / 2;
   cuuint64_t gdim[3] = {(cuuint64_t)2 * H, (cuuint64_t)l1, (cuuint64_t)ncomp * N};
   cuuint64_t gstride[2] = {(cuuint64_t)H * sizeof(double2), (cuuint64_t)l1 * H * sizeof(double2)};
-  cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)N};
+  cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)(N > 256 ? 256 : N)};  // (box rows <= 256)
   cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, gdim, gstride, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, cp * 16 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -1438,9 +1503,10 @@ int fused_ensure(pf_plan* p) {
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
     PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP, 3));
-  } else if (N == 512) {  // axis-1 passes only (two 256-row boxes per tile)
+  } else if (N == 512) {  // two 256-row boxes per tile / component pencil
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, fz::M2<512>::CM, 3));
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, fz::M2<512>::CM, 3));
+    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, fz::PK2<512>::CP, 3));
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
