@@ -138,3 +138,32 @@ def test_fused_slab_full_solve_matches_reference(pf, golden):
     assert rep.iterations == int(z["iterations"][0]) and rep.converged
     assert np.abs(u.ravel()[z["sample"]] - z["u_sample"][0]).max() <= 1e-10 * z["u_max"][0]
     assert abs(np.linalg.norm(u) - z["u_norm"][0]) <= 1e-10 * z["u_norm"][0]
+
+
+def test_fused_slab_512_two_ranks_matches_fused_pipeline(pf):
+    """Long-sequence fused passes (N = 512) on the slab layouts: two loopback
+    ranks (256 x-planes each, overlapped per-component exchanges) against the
+    single-GPU fused pipeline, truncated solve."""
+    import torch
+
+    from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
+    from slab_loopback import run_ranks
+
+    ind = pf.random_packing_geometry(512, seed=4)
+    cfg = pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=(1.0, 0.0, 0.0), max_iter=3)
+    ref, rref = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    u_ref = ref.u.cpu().numpy()
+    del ref
+    torch.cuda.empty_cache()
+    vals = np.asarray(ind.values)
+
+    def rank_fn(r, comm):
+        lo, hi = slab_range(512, 2, r)
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True)
+        return st["u"].cpu().numpy(), rep
+
+    res = run_ranks(2, rank_fn)
+    for _, rep in res:
+        assert rep.meta["pipeline"] == "slab-fused" and rep.iterations == rref.iterations == 3
+    u = np.concatenate([x for x, _ in res], axis=1)
+    assert rel_l2(u, u_ref) <= 1e-10
