@@ -57,7 +57,7 @@ int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode
 int pf_plan_destroy(pf_plan* plan);
 int pf_plan_set_stream(pf_plan* plan, void* stream);
 /* Enable (default) or disable the fused power-of-two Stokes pipeline
- * (cubic grids N = 64, 128, 256, 512; transport up to 256); disabled or unsupported grids use the
+ * (cubic grids N = 64, 128, 256, 512); disabled or unsupported grids use the
  * general cuFFT pipeline.  Both compute the same iteration. */
 int pf_plan_set_fused(pf_plan* plan, int enable);
 /* Enable (default) or disable solid-only storage of u~, a, lam on the fused

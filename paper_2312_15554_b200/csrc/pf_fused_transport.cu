@@ -81,7 +81,7 @@ struct TPK {
   using C = Cfg<N>;
   static constexpr int T = 128;
   static constexpr int NGP = T / C::G;
-  static constexpr int CP = NGP / 2;
+  static constexpr int CP = NGP / C::M / 2;  // (a long sequence takes M groups)
   static constexpr int NSEQ = 2 * CP;
   static constexpr int NCH = C::H / CP;
   static constexpr int TILES = N * NCH + N / CP;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
     for (int idx = t; idx < 2 * N * CP; idx += T) {
       const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
       const size_t o = yoff(c, i0, q);
-      cp16(S + (c * CP + q) * SS + C::pad(i0), nyq ? B.Yn + o : B.Y + o);
+      cp16(S + (c * CP + q) * SS + C::sp(i0), nyq ? B.Yn + o : B.Y + o);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
@@ -163,7 +163,11 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
   } else {
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    fft_seq<N, false>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
+    if constexpr (C::M > 1) {
+      fz::radix_stage<N, false>(S, NSEQ, SS, tw, t, T);
+      __syncthreads();
+    }
+    fz::fft_units<N, false>(S, NSEQ, SS, tw, g, l, K::NGP);
   }
   __syncthreads();
   const size_t nh = (size_t)K::TILES * CP * N;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
       bk = bk + P.b0v[c] * kc[c];
       ksq = ksq + kc[c] * kc[c];
     }
-    const double2 fb = S[q * SS + C::pad(k0)], fw0 = S[(CP + q) * SS + C::pad(k0)];
+    const double2 fb = S[q * SS + C::kp(k0)], fw0 = S[(CP + q) * SS + C::kp(k0)];
     const double2 f = cadd(fb, cik(kc[0], fw0));  // F^ = S^ + i k.W^   (pure.py:104-105)
     const bool zero = (k0 | kk1 | k2) == 0;
     const double2 chi = zero ? make_double2(0.0, 0.0) : cdiv_np(f, make_double2(P.a0 * L, bk));
@@ -207,17 +211,21 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
       acc[1] += w * s2;
     }
     B.CH[tbase + m] = chi;
-    S[q * SS + C::pad(k0)] = make_double2(chi.x * P.inv_n, chi.y * P.inv_n);
+    S[q * SS + C::kp(k0)] = make_double2(chi.x * P.inv_n, chi.y * P.inv_n);
     const double2 g0 = cik(kc[0], chi);
-    S[(CP + q) * SS + C::pad(k0)] = make_double2(g0.x * P.inv_n, g0.y * P.inv_n);
+    S[(CP + q) * SS + C::kp(k0)] = make_double2(g0.x * P.inv_n, g0.y * P.inv_n);
   }
   __syncthreads();
-  fft_seq<N, true>(S + (g < NSEQ ? g : 0) * SS, tw, l, g < NSEQ);
+  fz::fft_units<N, true>(S, NSEQ, SS, tw, g, l, K::NGP);
+  if constexpr (C::M > 1) {
+    __syncthreads();
+    fz::radix_stage<N, true>(S, NSEQ, SS, tw, t, T);
+  }
   __syncthreads();
   for (int idx = t; idx < 2 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
     const size_t o = yoff(c, i0, q);
-    const double2 v = S[(c * CP + q) * SS + C::pad(i0)];
+    const double2 v = S[(c * CP + q) * SS + C::sp(i0)];
     if (nyq) B.Yn[o] = v; else B.Y[o] = v;
   }
   block_sum<2>(acc);
@@ -233,10 +241,10 @@ struct TM {
   using C = Cfg<N>;
   static constexpr int T = 128;
   static constexpr int NGM = T / C::G;
-  static constexpr int CM = NGM;
+  static constexpr int CM = NGM / C::M;
   static constexpr int NCH = C::H / CM;
   static constexpr int TPC = N * NCH + N / CM;  // tiles per output component
-  static constexpr size_t SEQ = sizeof(double2) * NGM * C::SS;
+  static constexpr size_t SEQ = sizeof(double2) * CM * C::SS;
   // one sequence set: Y_b = FFT(X0) + i k1 FFT(X2) runs its two transforms one
   // after the other, stashing i k1 FFT(X2) in registers (IPT items per thread)
   // TMA path (N = 128 / 256, main tiles): the CM x N tile lands 128B-swizzled in a
@@ -278,8 +286,8 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
     for (int idx = t; idx < N * CM; idx += T) {
       const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
       const size_t o = off_of(c, e, q);
-      if (INV) cp16(S + q * SS + C::pad(e), nyq ? B.Yn + o : B.Y + o);
-      else cp16(S + q * SS + C::pad(e), nyq ? B.Xn + o : B.X + o);
+      if (INV) cp16(S + q * SS + C::kp(e), nyq ? B.Yn + o : B.Y + o);
+      else cp16(S + q * SS + C::sp(e), nyq ? B.Xn + o : B.X + o);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -324,14 +332,18 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
       tma_fft(2, false);
     } else {
       stage(2);
-      fft_seq<N, false>(S + g * SS, tw, l, true);
+      if constexpr (C::M > 1) {
+        fz::radix_stage<N, false>(S, CM, SS, tw, t, T);
+        __syncthreads();
+      }
+      fz::fft_units<N, false>(S, CM, SS, tw, g, l, K::NGM);
       __syncthreads();
     }
 #pragma unroll
     for (int j = 0; j < K::IPT; ++j) {
       const int idx = t + T * j;
       const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
-      v2[j] = cik(__ldg(kap1 + e), S[q * SS + C::pad(e)]);
+      v2[j] = cik(__ldg(kap1 + e), S[q * SS + C::kp(e)]);
     }
     __syncthreads();
   }
@@ -342,19 +354,31 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
   if (INV && oc == 2) {  // i k1 Y(chi) before the inverse axis-1 transform
     for (int idx = t; idx < N * CM; idx += T) {
       const int q = idx / N, e = idx % N;
-      double2* p = S + q * SS + C::pad(e);
+      double2* p = S + q * SS + C::kp(e);
       *p = cik(__ldg(kap1 + e), *p);
     }
     __syncthreads();
   }
-  fft_seq<N, INV>(S + g * SS, tw, l, true);
+  if constexpr (C::M > 1) {
+    if (!INV) {
+      fz::radix_stage<N, false>(S, CM, SS, tw, t, T);
+      __syncthreads();
+    }
+    fz::fft_units<N, INV>(S, CM, SS, tw, g, l, K::NGM);
+    if (INV) {
+      __syncthreads();
+      fz::radix_stage<N, true>(S, CM, SS, tw, t, T);
+    }
+  } else {
+    fft_seq<N, INV>(S + g * SS, tw, l, true);
+  }
   __syncthreads();
   }
 #pragma unroll
   for (int j = 0; j < K::IPT; ++j) {
     const int idx = t + T * j;
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
-    double2 v = S[q * SS + C::pad(e)];
+    double2 v = S[q * SS + (INV ? C::sp(e) : C::kp(e))];
     if (two) v = cadd(v, v2[j]);
     const size_t o = off_of(oc, e, q);
     if (INV) {
@@ -369,10 +393,10 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
 template <int N>
 struct TRS {
   using C = Cfg<N>;
-  static constexpr int R = 512 / N;          // rows per tile
+  static constexpr int R = N > 256 ? 2 : 512 / N;  // rows per tile
   static constexpr int NSF = 2 * R;          // forward sequences: (w0 + i w1), (s + i w2) per row
   static constexpr int NSI = R + R / 2;      // inverse: (d0 + i d1) per row, (d2, d2) per row pair
-  static constexpr int T = NSF * C::G;       // one group per forward sequence
+  static constexpr int T = NSF * C::M * C::G;  // one group per forward block transform
   static constexpr int V = R * N;
   static constexpr int VPT = V / T;
   static constexpr size_t TW = sizeof(double2) * C::TWN;
@@ -453,14 +477,18 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       }
       double2* sp = SIq + sq * SS;
       if (k == 0 || k == H) {
-        sp[C::pad(k)] = make_double2(xa.x, xb.x);  // C2R keeps the real part of self-conjugate modes
+        sp[C::kp(k)] = make_double2(xa.x, xb.x);  // C2R keeps the real part of self-conjugate modes
       } else {
-        sp[C::pad(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
-        sp[C::pad(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+        sp[C::kp(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+        sp[C::kp(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
       }
     }
     __syncthreads();
-    fft_seq<N, true>(SIq + (g < K::NSI ? g : 0) * SS, tw, l, g < K::NSI);
+    fz::fft_units<N, true>(SIq, K::NSI, SS, tw, g, l, T / C::G);
+    if constexpr (C::M > 1) {
+      __syncthreads();
+      fz::radix_stage<N, true>(SIq, K::NSI, SS, tw, t, T);
+    }
     __syncthreads();
     // (2) polarization (pure.py:71-87) with A, B, F from H and u (transport.py:112-121);
     // gradients to registers first: the forward sequences overwrite the inverse ones
@@ -468,10 +496,10 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
 #pragma unroll
     for (int j = 0; j < K::VPT; ++j) {
       const int v = t + T * j, row = v / N, col = v % N;
-      const double2 z01 = SIq[row * SS + C::pad(col)];
+      const double2 z01 = SIq[row * SS + C::sp(col)];
       gv[j][0] = z01.x;
       gv[j][1] = z01.y;
-      gv[j][2] = reinterpret_cast<const double*>(SIq + (R + (row >> 1)) * SS + C::pad(col))[row & 1];
+      gv[j][2] = reinterpret_cast<const double*>(SIq + (R + (row >> 1)) * SS + C::sp(col))[row & 1];
     }
     __syncthreads();
 #pragma unroll
@@ -490,12 +518,16 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
         w[c] = contrast * tg;
         s = s - (pep * su[c * V + v] - P.b0v[c]) * tg;
       }
-      SFq[(2 * row) * SS + C::pad(col)] = make_double2(w[0], w[1]);
-      SFq[(2 * row + 1) * SS + C::pad(col)] = make_double2(s, w[2]);
+      SFq[(2 * row) * SS + C::sp(col)] = make_double2(w[0], w[1]);
+      SFq[(2 * row + 1) * SS + C::sp(col)] = make_double2(s, w[2]);
     }
     __syncthreads();
     if (t == 0 && tile + (int)gridDim.x < NT) trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbar);
-    fft_seq<N, false>(SFq + g * SS, tw, l, true);
+    if constexpr (C::M > 1) {
+      fz::radix_stage<N, false>(SFq, K::NSF, SS, tw, t, T);
+      __syncthreads();
+    }
+    fz::fft_units<N, false>(SFq, K::NSF, SS, tw, g, l, T / C::G);
     __syncthreads();
     // (3) separate; X_a = X(s) + i k2 X(w2); store X comps 0 (X_a), 1 (X(w0)), 2 (X(w1))
     const int64_t NN = (int64_t)N * N;
@@ -503,8 +535,8 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       const int r = idx / (H + 1), k = idx % (H + 1);
       const double2* s1 = SFq + (2 * r) * SS;
       const double2* s2 = SFq + (2 * r + 1) * SS;
-      const double2 a1 = s1[C::pad(k)], m1 = s1[C::pad((N - k) & (N - 1))];
-      const double2 a2 = s2[C::pad(k)], m2 = s2[C::pad((N - k) & (N - 1))];
+      const double2 a1 = s1[C::kp(k)], m1 = s1[C::kp((N - k) & (N - 1))];
+      const double2 a2 = s2[C::kp(k)], m2 = s2[C::kp((N - k) & (N - 1))];
       const double2 xw0 = make_double2(0.5 * (a1.x + m1.x), 0.5 * (a1.y - m1.y));
       const double2 xw1 = make_double2(0.5 * (a1.y + m1.y), -0.5 * (a1.x - m1.x));
       const double2 xs = make_double2(0.5 * (a2.x + m2.x), 0.5 * (a2.y - m2.y));
@@ -630,7 +662,7 @@ static int tfused_ensure(pf_plan* p) {
   FusedTPlan* f = new FusedTPlan();
   f->N = N;
   const size_t H = N / 2, NN = (size_t)N * N, nh = NN * (H + 1);
-  const int nb_pk = (N == 64) ? ft::TPK<64>::TILES : (N == 128 ? ft::TPK<128>::TILES : ft::TPK<256>::TILES);
+  const int nb_pk = (N == 64) ? ft::TPK<64>::TILES : (N == 128 ? ft::TPK<128>::TILES : (N == 256 ? ft::TPK<256>::TILES : ft::TPK<512>::TILES));
   const size_t elems = 3 * NN * H + 3 * NN + 2 * NN * H + 2 * NN + nh + N;
   const size_t bytes = elems * sizeof(double2) + 2 * (size_t)nb_pk * sizeof(double);
   PF_CK_CUDA(cudaMalloc(&f->mem, bytes));
@@ -647,11 +679,12 @@ static int tfused_ensure(pf_plan* p) {
   f->b.Yn = take(2 * NN);
   f->b.tw = take(N);
   f->b.part = (double*)m;
-  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : fz::Cfg<256>::TWN));
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : fz::Cfg<512>::TWN)));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
-    default: fz::pass1_twiddles<256>(tw.data()); break;
+    case 256: fz::pass1_twiddles<256>(tw.data()); break;
+    default: fz::pass1_twiddles<512>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   if (N == 128 || N == 256) {
@@ -678,7 +711,8 @@ static int tfused_ensure(pf_plan* p) {
   switch (N) {
     case 64: PF_CK(tset_attrs<64>(f)); break;
     case 128: PF_CK(tset_attrs<128>(f)); break;
-    default: PF_CK(tset_attrs<256>(f)); break;
+    case 256: PF_CK(tset_attrs<256>(f)); break;
+    default: PF_CK(tset_attrs<512>(f)); break;
   }
   p->tfused = f;
   p->scratch_bytes += bytes;
@@ -783,7 +817,8 @@ int tfused_setup(pf_plan* p, bool warm) {
   switch (ftp(p)->N) {
     case 64: return tsetup_t<64>(p, warm);
     case 128: return tsetup_t<128>(p, warm);
-    default: return tsetup_t<256>(p, warm);
+    case 256: return tsetup_t<256>(p, warm);
+    default: return tsetup_t<512>(p, warm);
   }
 }
 
@@ -791,7 +826,8 @@ int tfused_finish(pf_plan* p) {
   switch (ftp(p)->N) {
     case 64: return tfinish_t<64>(p);
     case 128: return tfinish_t<128>(p);
-    default: return tfinish_t<256>(p);
+    case 256: return tfinish_t<256>(p);
+    default: return tfinish_t<512>(p);
   }
 }
 
@@ -799,7 +835,8 @@ int tfused_enqueue(pf_plan* p, cudaEvent_t* ev) {
   switch (ftp(p)->N) {
     case 64: return tenqueue_t<64>(p, ev);
     case 128: return tenqueue_t<128>(p, ev);
-    default: return tenqueue_t<256>(p, ev);
+    case 256: return tenqueue_t<256>(p, ev);
+    default: return tenqueue_t<512>(p, ev);
   }
 }
 

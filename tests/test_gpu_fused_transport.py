@@ -93,3 +93,32 @@ def test_fused_transport_warm_start(pf, flow64):
     assert rep.meta["pipeline"] == "fused" and rep.iterations == it
     assert rel_l2(st.chi, chi) <= FIELD_TOL and rel_l2(st.grad_chi, gchi) <= FIELD_TOL
     _hist_close(rep.history, hist)
+
+
+def test_fused_transport_512_matches_cufft_pipeline(pf):
+    """Long sequences (N = 512, two 256-point blocks + radix-2 stage) in the
+    transport passes: truncated solve under a synthetic flow against the cuFFT
+    transport pipeline (iterations, chi and grad chi to round-off, history)."""
+    import torch
+
+    n = 512
+    ind = pf.random_packing_geometry(n, seed=6)
+    dev = torch.device("cuda", 0)
+    x = torch.arange(n, dtype=torch.float64, device=dev) / n
+    u = torch.zeros((3, n, n, n), dtype=torch.float64, device=dev)
+    u[0] = 1.0 + 0.2 * torch.sin(2 * np.pi * x)[None, :, None]
+    u[1] = 0.1 * torch.cos(2 * np.pi * x)[:, None, None]
+    u *= torch.as_tensor(np.asarray(ind.values) == 0, device=dev)
+    cfg = pf.TransportConfig(pe=10.0, a0=0.55, eps=1e-12, composition_gradient=(1.0, 0.0, 0.0), max_iter=4)
+    a, ra = pf.solve_transport_device(ind, u, cfg, pipeline="fused")
+    assert ra.meta["pipeline"] == "fused"
+    chi, gchi = a.chi.cpu().numpy(), a.grad_chi.cpu().numpy()
+    del a
+    torch.cuda.empty_cache()
+    b, rb = pf.solve_transport_device(ind, u, cfg, pipeline="cufft")
+    assert rb.meta["pipeline"] == "cufft" and ra.iterations == rb.iterations == 4
+    assert rel_l2(chi, b.chi.cpu().numpy()) <= FIELD_TOL
+    assert rel_l2(gchi, b.grad_chi.cpu().numpy()) <= FIELD_TOL
+    _hist_close(ra.history, rb.history)
+    del b
+    torch.cuda.empty_cache()
