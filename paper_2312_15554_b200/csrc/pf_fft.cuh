@@ -41,8 +41,8 @@ struct Cfg {
   static constexpr int RS_TILES = N * N / RSR;
   // compact pass-1 twiddle table: rows w^b (b = 1..3) and w^(4a) (a = 1..A/4-1), B lanes each
   static constexpr int TWL = (3 + A / 4 - 1) * B;
-  // + for long sequences the radix-M stage's w_N^(j r), rows r = 1..M-1 of L entries
-  static constexpr int TWN = TWL + (M - 1) * L;
+  // + for long sequences the radix-M stage's w_N^j (L entries; w_N^(j r) = its r-th power)
+  static constexpr int TWN = TWL + (M > 1 ? L : 0);
   static __device__ __forceinline__ int pad(int e) { return e + e / A; }  // within one block
   static __device__ __forceinline__ int sp(int e) { return M == 1 ? pad(e) : (e / L) * SSL + pad(e % L); }
   static __device__ __forceinline__ int kp(int k) { return M == 1 ? pad(k) : (k % M) * SSL + pad(k / M); }
@@ -195,10 +195,10 @@ inline void pass1_twiddles(double2* out) {
   };
   for (int b = 1; b < 4; ++b) row(b);
   for (int a = 1; a < C::A / 4; ++a) row(4 * a);
-  for (int rr = 1; rr < C::M; ++rr)  // radix-M stage: w_N^(j rr)
+  if (C::M > 1)  // radix-M stage: w_N^j
     for (int j = 0; j < L; ++j) {
-      const double a = 2.0 * M_PI * (double)(j * rr) / (double)N;
-      out[C::TWL + (rr - 1) * L + j] = make_double2(std::cos(a), -std::sin(a));
+      const double a = 2.0 * M_PI * (double)j / (double)N;
+      out[C::TWL + j] = make_double2(std::cos(a), -std::sin(a));
     }
 }
 
@@ -260,6 +260,23 @@ __device__ __forceinline__ void fft_seq(double2* s, const double2* __restrict__ 
   fft_seq_x<N, INV>(x, s, tw, l, active);
 }
 
+// a[r] *= w_N^(j r) (conjugated for the inverse), r = 1..M-1; w_N^j from the
+// table, its powers by complex multiplication (<= 2 ulp)
+template <int N, bool INV>
+__device__ __forceinline__ void radix_twiddle(double2* a, const double2* __restrict__ tw, int j) {
+  using C = Cfg<N>;
+  if constexpr (C::M > 1) {
+    double2 w1 = tw[C::TWL + j];
+    if (INV) w1.y = -w1.y;
+    double2 w = w1;
+#pragma unroll
+    for (int r = 1; r < C::M; ++r) {
+      a[r] = cmul(a[r], w);
+      if (r + 1 < C::M) w = cmul(w, w1);
+    }
+  }
+}
+
 // Radix-M stage of long sequences (Cfg<N>::M > 1; no-op otherwise), all threads
 // of the block: forward = DIF butterfly + twiddle w_N^(j r) (natural order in,
 // blocks ready for their L-point transforms); inverse = conjugate twiddle +
@@ -270,26 +287,15 @@ __device__ __forceinline__ void radix_stage(double2* S, int nseq, int ss, const 
   using C = Cfg<N>;
   constexpr int M = C::M, L = C::L;
   if constexpr (M > 1) {
-    const double2* twb = tw + C::TWL;
     for (int idx = t; idx < nseq * L; idx += T) {
       const int sq = idx / L, j = idx % L;
       double2* base = S + (size_t)sq * ss + C::pad(j);
       double2 a[M];
 #pragma unroll
       for (int b = 0; b < M; ++b) a[b] = base[b * C::SSL];
-      if (!INV) {
-        Dft<M, false>::run(a);
-#pragma unroll
-        for (int r = 1; r < M; ++r) a[r] = cmul(a[r], twb[(r - 1) * L + j]);
-      } else {
-#pragma unroll
-        for (int r = 1; r < M; ++r) {
-          double2 w = twb[(r - 1) * L + j];
-          w.y = -w.y;
-          a[r] = cmul(a[r], w);
-        }
-        Dft<M, true>::run(a);
-      }
+      if (!INV) Dft<M, false>::run(a);
+      radix_twiddle<N, INV>(a, tw, j);
+      if (INV) Dft<M, true>::run(a);
 #pragma unroll
       for (int b = 0; b < M; ++b) base[b * C::SSL] = a[b];
     }

@@ -116,11 +116,11 @@ struct State {
 template <int N>
 struct RS2 {
   using C = Cfg<N>;
-  static constexpr int R = 1024 / N;            // rows per tile (1024 voxels)
+  static constexpr int R = N > 512 ? 2 : 1024 / N;  // rows per tile (1024 voxels; one row pair at N = 1024)
   // threads per block: one FFT group per row pair (every thread FFT-active) for
   // N <= 128; for N = 256 one group per row (measured: 128^3 RS 0.071 vs 0.088 ms,
   // 256^3 0.483 vs 0.512 ms the other way round)
-  static constexpr int T = N == 512 ? PF_RS512_T : R * C::G / (PF_RS_HALFT(N) ? 2 : 1);
+  static constexpr int T = N == 1024 ? 64 : (N == 512 ? PF_RS512_T : R * C::G / (PF_RS_HALFT(N) ? 2 : 1));
   static constexpr int V = R * N;               // voxels per tile
   static constexpr int VPT = V / T;             // voxels per thread
   static constexpr int NP = R / 2;              // inverse sequences (two rows each)
@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   const int NT = (SL ? B.nc : 3) * TPC;  // component window [c0, c0 + nc) (slab)
   constexpr int SPR = N / 32;  // 32-voxel segments per row
   const int CS = cp.cs;
-  static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
+  static_assert(T % 32 == 0, "segment bases are per warp");
+  if (V != 1024) return;  // segment bases assume 32 segments of 32 voxels per tile (never launched otherwise)
   pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -575,7 +576,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
   constexpr int SPR = N / 32;
-  static_assert(V == 1024 && T % 32 == 0, "segment bases assume 32 segments of 32 voxels per tile");
+  static_assert(T % 32 == 0, "segment bases are per warp");
+  if (V != 1024) return;  // segment bases assume 32 segments of 32 voxels per tile (never launched otherwise)
   pdl_wait();
   if (ctrl->done || ctrl->db == 0.0) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -899,7 +901,6 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
         static_assert(CM * C::L % T == 0, "radix items per thread");
         double2 a[IT][C::M];
         const double db = ctrl->db;
-        const double2* twb = tw + C::TWL;
 #pragma unroll
         for (int it = 0; it < IT; ++it) {
           const int idx = t + T * it, q = idx % CM, j = idx / CM;
@@ -912,8 +913,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
             }
           }
           Dft<C::M, false>::run(a[it]);
-#pragma unroll
-          for (int r = 1; r < C::M; ++r) a[it][r] = cmul(a[it][r], twb[(r - 1) * C::L + j]);
+          radix_twiddle<N, false>(a[it], tw, j);
         }
         __syncthreads();  // the tile is read
 #pragma unroll
@@ -1093,7 +1093,6 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
     // radix-M stage straight from the boxes, one component at a time: component
     // c's boxes into registers, then its sequences (which reach no later box)
     constexpr int IT = (CP * C::L + T - 1) / T;
-    const double2* twb = tw + C::TWL;
     for (int c = 0; c < 3; ++c) {
       const unsigned char* box = reg + K::BOX_OFF + c * K::BOX;
       double2 a[IT][C::M];
@@ -1108,8 +1107,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
             a[it][b] = *reinterpret_cast<const double2*>(box + (size_t)e * K::ROWB + ((q ^ sw) << 4));
           }
           Dft<C::M, false>::run(a[it]);
-#pragma unroll
-          for (int r = 1; r < C::M; ++r) a[it][r] = cmul(a[it][r], twb[(r - 1) * C::L + j]);
+          radix_twiddle<N, false>(a[it], tw, j);
         }
       }
       __syncthreads();  // component c's boxes are read
@@ -1327,7 +1325,7 @@ bool fused_supported(const pf_plan* p) {
   if (p->g.d != 3) return false;
   const int N = p->g.n[0];
   if (p->g.n[1] != N || p->g.n[2] != N) return false;
-  return N == 64 || N == 128 || N == 256 || N == 512;
+  return N == 64 || N == 128 || N == 256 || N == 512 || N == 1024;
 }
 
 template <int N>
@@ -1455,7 +1453,7 @@ int fused_ensure(pf_plan* p) {
   // X: 6 comps (XU 3, XR 3); Y: 3; Q, D: 1 each
   const size_t elems = 11 * (main1 + nyq1) + N;
   const int nb_rs = kRsMaxBlocks;
-  const int nb_pk = (N == 64) ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : (N == 256 ? fz::PK2<256>::TILES : fz::PK2<512>::TILES));
+  const int nb_pk = (N == 64) ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : (N == 256 ? fz::PK2<256>::TILES : (N == 512 ? fz::PK2<512>::TILES : fz::PK2<1024>::TILES)));
   const size_t part = 6 * (size_t)nb_rs + 3 * (size_t)nb_pk;
   f->bytes = elems * sizeof(double2) + part * sizeof(double);
   PF_CK_CUDA(cudaMalloc(&f->mem, f->bytes));
@@ -1490,12 +1488,13 @@ int fused_ensure(pf_plan* p) {
   f->b.Yxn = f->b.Yn;
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
-  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : fz::Cfg<512>::TWN)));
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : (N == 512 ? fz::Cfg<512>::TWN : fz::Cfg<1024>::TWN))));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
     case 256: fz::pass1_twiddles<256>(tw.data()); break;
-    default: fz::pass1_twiddles<512>(tw.data()); break;
+    case 512: fz::pass1_twiddles<512>(tw.data()); break;
+    default: fz::pass1_twiddles<1024>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   if (N == 128 || N == 256) {
@@ -1533,7 +1532,8 @@ int fused_ensure(pf_plan* p) {
     case 64: PF_CK(set_attrs<64>(f)); break;
     case 128: PF_CK(set_attrs<128>(f)); break;
     case 256: PF_CK(set_attrs<256>(f)); break;
-    default: PF_CK(set_attrs<512>(f)); break;
+    case 512: PF_CK(set_attrs<512>(f)); break;
+    default: PF_CK(set_attrs<1024>(f)); break;
   }
   p->fused = f;
   p->scratch_bytes += f->bytes;
@@ -1563,7 +1563,8 @@ static int to_tilemajor(int N, const double2* src, double2* dst, double scale, b
     case 64: fz::k_tilemajor<64><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
     case 128: fz::k_tilemajor<128><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
     case 256: fz::k_tilemajor<256><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
-    default: fz::k_tilemajor<512><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
+    case 512: fz::k_tilemajor<512><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
+    default: fz::k_tilemajor<1024><<<nb, kThreads, 0, s>>>(src, dst, scale, to_tm, l1); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
@@ -1591,7 +1592,8 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
   PF_CK(reduce_rows_to(p, p->partials, 2, nb, out));
   PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->work));
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
-  f->compact = (p->compact_enable && p->h_small[0] == 0.0) ? 1 : 0;
+  // (solid-only storage needs 1024-voxel RS tiles: N <= 512)
+  f->compact = (p->compact_enable && p->h_small[0] == 0.0 && fz::RS2<N>::V == 1024) ? 1 : 0;
   f->nb_rs = f->compact ? f->nb_compact : f->nb_full;
   p->sc.lam_pore_sq = f->compact ? p->h_small[1] : 0.0;
   if (!f->compact) return PF_OK;
@@ -1654,7 +1656,8 @@ int fused_setup(pf_plan* p) {
     case 64: fz::k_split_yx<64><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
     case 128: fz::k_split_yx<128><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
     case 256: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
-    default: fz::k_split_yx<512><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+    case 512: fz::k_split_yx<512><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
+    default: fz::k_split_yx<1024><<<grid, kThreads, 0, p->work>>>(p->specA, f->b); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   (void)NN;
@@ -1663,7 +1666,8 @@ int fused_setup(pf_plan* p) {
     case 64: return compact_setup_t<64>(p, f);
     case 128: return compact_setup_t<128>(p, f);
     case 256: return compact_setup_t<256>(p, f);
-    default: return compact_setup_t<512>(p, f);
+    case 512: return compact_setup_t<512>(p, f);
+    default: return compact_setup_t<1024>(p, f);
   }
 }
 
@@ -1681,7 +1685,8 @@ int fused_finish(pf_plan* p) {
       case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
       case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
       case 256: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
-      default: fz::k_compact_move<512><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      case 512: fz::k_compact_move<512><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      default: fz::k_compact_move<1024><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
     }
     PF_CK_CUDA(cudaGetLastError());
   }
@@ -1750,7 +1755,8 @@ int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {
     case 64: return enqueue_fused_t<64>(p, ev);
     case 128: return enqueue_fused_t<128>(p, ev);
     case 256: return enqueue_fused_t<256>(p, ev);
-    default: return enqueue_fused_t<512>(p, ev);
+    case 512: return enqueue_fused_t<512>(p, ev);
+    default: return enqueue_fused_t<1024>(p, ev);
   }
 }
 
@@ -1761,10 +1767,10 @@ int enqueue_fused(pf_plan* p, cudaEvent_t* ev) {
 // k1off) of Q^, D^; Y lives in the two exchange-native layouts of Bufs, whose
 // buffers the caller owns and all-to-alls between PK and the axis-1 passes.
 static bool fslab_shape_ok(int N, int l0, int l1) {
-  if (N != 64 && N != 128 && N != 256 && N != 512) return false;
+  if (N != 64 && N != 128 && N != 256 && N != 512 && N != 1024) return false;
   if (l0 <= 0 || l1 <= 0 || (l1 & (l1 - 1)) || N % l0 || N % l1) return false;
-  const int cm = N == 64 ? fz::M2<64>::CM : (N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : fz::M2<512>::CM));
-  const int cp = N == 64 ? fz::PK2<64>::CP : (N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : fz::PK2<512>::CP));
+  const int cm = N == 64 ? fz::M2<64>::CM : (N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : (N == 512 ? fz::M2<512>::CM : fz::M2<1024>::CM)));
+  const int cp = N == 64 ? fz::PK2<64>::CP : (N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : (N == 512 ? fz::PK2<512>::CP : fz::PK2<1024>::CP)));
   return l0 % cm == 0 && l1 % cp == 0;
 }
 
@@ -1814,7 +1820,7 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   const size_t H = N / 2;
   const size_t xm = (size_t)l0 * N * H, xn = (size_t)l0 * N;  // X per component
   const size_t qd = (size_t)l1 * N * H + (size_t)l1 * N;      // Q^ / D^ (tile-major, y-slab)
-  const int pk_max = N == 64 ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : (N == 256 ? fz::PK2<256>::TILES : fz::PK2<512>::TILES));
+  const int pk_max = N == 64 ? fz::PK2<64>::TILES : (N == 128 ? fz::PK2<128>::TILES : (N == 256 ? fz::PK2<256>::TILES : (N == 512 ? fz::PK2<512>::TILES : fz::PK2<1024>::TILES)));
   const size_t elems = 6 * (xm + xn) + 2 * qd + N;
   const size_t part = 6 * (size_t)kRsMaxBlocks + 3 * (size_t)pk_max;
   f->bytes = elems * sizeof(double2) + part * sizeof(double);
@@ -1849,12 +1855,13 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   f->b.nc = 3;
   f->b.pst = 0;  // set per launch (nb_rs)
   f->b.poff = 0;
-  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : fz::Cfg<512>::TWN)));
+  std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : (N == 512 ? fz::Cfg<512>::TWN : fz::Cfg<1024>::TWN))));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
     case 128: fz::pass1_twiddles<128>(tw.data()); break;
     case 256: fz::pass1_twiddles<256>(tw.data()); break;
-    default: fz::pass1_twiddles<512>(tw.data()); break;
+    case 512: fz::pass1_twiddles<512>(tw.data()); break;
+    default: fz::pass1_twiddles<1024>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   // axes-(1, 2) transform of this slab's R at setup
@@ -1879,7 +1886,8 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
     case 64: PF_CK(set_attrs<64>(f)); break;
     case 128: PF_CK(set_attrs<128>(f)); break;
     case 256: PF_CK(set_attrs<256>(f)); break;
-    default: PF_CK(set_attrs<512>(f)); break;
+    case 512: PF_CK(set_attrs<512>(f)); break;
+    default: PF_CK(set_attrs<1024>(f)); break;
   }
   p->scratch_bytes += f->bytes + ws + sizeof(double2) * 3 * (size_t)l0 * N * (H + 1);
   return PF_OK;
@@ -1899,14 +1907,16 @@ int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R
     case 64: fz::k_split_yx<64><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
     case 128: fz::k_split_yx<128><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
     case 256: fz::k_split_yx<256><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
-    default: fz::k_split_yx<512><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+    case 512: fz::k_split_yx<512><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
+    default: fz::k_split_yx<1024><<<grid, kThreads, 0, p->work>>>(f->spec, f->b); break;
   }
   PF_CK_CUDA(cudaGetLastError());
   switch (N) {
     case 64: PF_CK(compact_setup_t<64>(p, f)); break;
     case 128: PF_CK(compact_setup_t<128>(p, f)); break;
     case 256: PF_CK(compact_setup_t<256>(p, f)); break;
-    default: PF_CK(compact_setup_t<512>(p, f)); break;
+    case 512: PF_CK(compact_setup_t<512>(p, f)); break;
+    default: PF_CK(compact_setup_t<1024>(p, f)); break;
   }
   f->lam_pore = p->sc.lam_pore_sq;  // local: enters the totals before the all-reduce
   p->sc.lam_pore_sq = 0.0;
@@ -2007,7 +2017,8 @@ int fused_slab_pk(pf_plan* p) {
     case 64: return fslab_pk_t<64>(p);
     case 128: return fslab_pk_t<128>(p);
     case 256: return fslab_pk_t<256>(p);
-    default: return fslab_pk_t<512>(p);
+    case 512: return fslab_pk_t<512>(p);
+    default: return fslab_pk_t<1024>(p);
   }
 }
 
@@ -2016,7 +2027,8 @@ int fused_slab_pk(pf_plan* p) {
     case 64: return fn<64>(__VA_ARGS__);  \
     case 128: return fn<128>(__VA_ARGS__); \
     case 256: return fn<256>(__VA_ARGS__); \
-    default: return fn<512>(__VA_ARGS__); \
+    case 512: return fn<512>(__VA_ARGS__); \
+    default: return fn<1024>(__VA_ARGS__); \
   }
 
 int fused_slab_rs(pf_plan* p, double* totals) { PF_FSLAB_DISPATCH(fslab_rs_t, p, 0, 3, totals) }
@@ -2038,7 +2050,8 @@ int fused_slab_end(pf_plan* p, double2* Tq) {
       case 64: fz::k_compact_move<64><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
       case 128: fz::k_compact_move<128><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
       case 256: fz::k_compact_move<256><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
-      default: fz::k_compact_move<512><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      case 512: fz::k_compact_move<512><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
+      default: fz::k_compact_move<1024><<<nb, kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut, p->s_a, p->s_lam, p->s_u, 1, rows); break;
     }
     PF_CK_CUDA(cudaGetLastError());
   }

@@ -350,7 +350,7 @@ int pf_transport_begin(pf_plan* p, const pf_transport_params* P, const uint8_t* 
   if (res) *res = p->t_res;
   k_ctrl_init_t<<<1, 1, 0, p->work>>>(p->ctrl);
   PF_CK_CUDA(cudaGetLastError());
-  p->t_pipeline = (p->fused_enable && fused_supported(p)) ? 1 : 0;
+  p->t_pipeline = (p->fused_enable && fused_supported(p) && p->g.n[0] <= 512) ? 1 : 0;  // fused transport: N <= 512
   if (p->t_pipeline == 1) return tfused_setup(p, true);
   const int64_t n = p->g.nr;
   switch (d) {

@@ -99,3 +99,34 @@ def run_ranks(world, fn):
         if e is not None:
             raise e
     return out
+
+
+class SoloComm:
+    """Rank ``rank`` of a ``world``-rank slab decomposition run ALONE: the other
+    ranks' exchange blocks arrive as zeros and contribute nothing to the
+    all-reduce.  Both device slab pipelines then compute the same well-defined
+    map (the iteration with the other ranks' fields held at zero), so comparing
+    them validates the per-rank kernels of a decomposition whose full cell does
+    not fit one GPU (1024^3), and the rank's compute time is the per-GPU share
+    of that decomposition.  Test / measurement infrastructure only."""
+
+    def __init__(self, world, rank=0):
+        self.world, self.r = world, rank
+
+    def get_world_size(self, group=None):
+        return self.world
+
+    def get_rank(self, group=None):
+        return self.r
+
+    def is_initialized(self):
+        return True
+
+    def all_to_all_single(self, recv, send, group=None, async_op=False):
+        k = send.numel() // self.world
+        recv.zero_()
+        recv[self.r * k:(self.r + 1) * k].copy_(send[self.r * k:(self.r + 1) * k])
+        return _Done() if async_op else None
+
+    def all_reduce(self, t, group=None):
+        return None

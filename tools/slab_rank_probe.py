@@ -1,0 +1,65 @@
+"""Per-rank compute of a slab-decomposed cell whose full size does not fit one
+GPU (BASELINE cfg 5, 1024^3): rank 0 of P run alone with the other ranks'
+exchange blocks zero (tests/slab_loopback.py SoloComm), fused and cuFFT slab
+pipelines, CUDA-event time per iteration.  Exchanges are local copies here, so
+this is the rank's compute share; DESIGN.md §6 adds the NVLink exchange.
+
+    python tools/slab_rank_probe.py [N] [P] [iters]
+"""
+
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2312_15554_b200 as pf  # noqa: E402
+from paper_2312_15554_b200 import slab as S  # noqa: E402
+from slab_loopback import SoloComm  # noqa: E402
+
+
+def run(n, world, iters, fused):
+    dev = torch.device("cuda", 0)
+    ind = pf.random_packing_geometry(n, seed=0)
+    lo, hi = S.slab_range(n, world, 0)
+    solid_np = np.ascontiguousarray(ind.values[lo:hi])
+    del ind
+    cfg = pf.StokesConfig.with_tolerance(1e-12, pressure_gradient=(1.0, 0.0, 0.0), max_iter=iters + 4)
+    be = S.DeviceSlabBackend((n, n, n), world, 0, "central", dev)
+    be.bind()
+    L = (hi - lo) * n * n
+    st = {k: torch.zeros(3 * L, dtype=torch.float64, device=dev) for k in ("u", "u_tilde", "a", "lam")}
+    st["q"] = torch.zeros(L, dtype=torch.float64, device=dev)
+    solid = torch.as_tensor(solid_np).reshape(-1).to(dev)
+    cls = S.FusedSlabStokes if fused else S.SlabStokes
+    sol = cls(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st, comm=SoloComm(world))
+    sol.begin()
+    sol.iterate(2, poll=False)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    sol.iterate(iters, poll=False)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / iters
+    sol.end()
+    be.close()
+    del sol, st, solid
+    torch.cuda.empty_cache()
+    return ms
+
+
+if __name__ == "__main__":
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+    world = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    iters = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+    res = {}
+    for fused in (True, False):
+        ms = run(n, world, iters if fused else max(2, iters // 2), fused)
+        res["fused" if fused else "cufft"] = {"ms_per_iter": ms, "rank_voxel_iters_per_s": n ** 3 / world / (ms / 1e3)}
+    print(json.dumps({"grid": n, "ranks": world, "rank": 0, "pipelines": res}))
