@@ -57,7 +57,7 @@ int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode
 int pf_plan_destroy(pf_plan* plan);
 int pf_plan_set_stream(pf_plan* plan, void* stream);
 /* Enable (default) or disable the fused power-of-two Stokes pipeline
- * (cubic grids N = 64, 128, 256, 512); disabled or unsupported grids use the
+ * (cubic grids N = 64 ... 1024; transport up to 512); disabled or unsupported grids use the
  * general cuFFT pipeline.  Both compute the same iteration. */
 int pf_plan_set_fused(pf_plan* plan, int enable);
 /* Enable (default) or disable solid-only storage of u~, a, lam on the fused
@@ -151,7 +151,7 @@ int pf_slab_form_r(pf_plan* plan, double* R, int gated);
 int pf_slab_scale(pf_plan* plan, const double* src, double* dst, int64_t count, double scale);
 int pf_slab_read(pf_plan* plan, pf_stokes_result* result);
 
-/* Fused slab pipeline (cubic N in {64, 128, 256, 512}, P a power of two, slabs of
+/* Fused slab pipeline (cubic N in {64, 128, 256, 512, 1024}, P a power of two, slabs of
  * whole tiles; pf_slab_fused_sizes reports 0 when unsupported).  Per iteration:
  * pf_slab_fused_pk (axis 0 + Green's operator on the y-slab Y) -> exchange
  * Y y-slab -> x-slab -> pf_slab_fused_rs (axis-1 inverse, rows + local step,
