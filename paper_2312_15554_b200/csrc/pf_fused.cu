@@ -75,6 +75,14 @@
 namespace pf {
 namespace fz {
 
+// 16-byte chunk XOR of TMA row e for box rows of RB bytes (SWIZZLE_128B/64B/32B;
+// 16-byte rows are not swizzled): the chunk index is XORed with address bits
+// [7, 7 + log2(RB / 16)) of the row start, i.e. with (e * RB) >> 7.
+template <int RB>
+__device__ __forceinline__ int swz16(int e) {
+  return RB == 128 ? (e & 7) : (RB == 64 ? ((e >> 1) & 3) : (RB == 32 ? ((e >> 2) & 1) : 0));
+}
+
 struct Bufs {
   double2 *XU, *XUn;  // X-space (after axis 2): u' (MI -> RS); X(u~') when b changed (RS-fix -> MF)
   double2 *XR, *XRn;  // X-space R = b u~' - a' (RS -> MF)   [3][N*N][H], [3][N*N]
@@ -97,6 +105,8 @@ struct Bufs {
   // plane window of one launch of the x-slab passes (SL kernels): planes
   // [i0a, i0a + nl) of the l0; RS partial rows at [q * pst + poff + block]
   int i0a, nl, pst, poff;
+  // the host encoded the TMA tensor maps of this layout (else the passes stage with LDGSTS)
+  int tma;
   // component window of one launch of MI / RS (SL kernels): components [c0, c0 + nc)
   int c0, nc;
 };
@@ -767,7 +777,8 @@ struct PK2 {
   // sequence region so the first FFT round's stores never reach the last box
   // (CP = 8: 128-byte box rows, SWIZZLE_128B)
   static constexpr int ROWB = CP * 16;  // box row bytes
-  static constexpr bool TMA_OK = ((N == 128 || N == 256) && (ROWB == 64 || ROWB == 128)) || (N == 512 && ROWB == 64);
+  static constexpr bool TMA_OK = ((N == 128 || N == 256) && (ROWB == 64 || ROWB == 128)) || (N == 512 && ROWB == 64) ||
+                                 (N == 1024 && ROWB == 16);
   static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
   static constexpr size_t BOX = sizeof(double2) * CP * N;
   static constexpr size_t BOX_AL = ROWB == 128 ? 1024 : 512;  // swizzle-atom alignment of a box
@@ -796,7 +807,8 @@ struct M2 {
   // TMA path (single GPU, N = 128 / 256, main tiles): the CM x N tile lands
   // 128B-swizzled in a 1 KB-aligned region that the padded sequences then reuse
   // (N = 512: 64-byte rows, two 256-row boxes, single GPU only)
-  static constexpr bool TMA_OK = ((N == 128 || N == 256) && CM * 16 == 128) || (N == 512 && CM * 16 == 64);
+  static constexpr bool TMA_OK = ((N == 128 || N == 256) && CM * 16 == 128) || (N == 512 && CM * 16 == 64) ||
+                                 (N == 1024 && CM * 16 == 32);
   static constexpr int ROWB = CM * 16;
   static constexpr size_t TILE = sizeof(double2) * CM * N;
   static constexpr size_t REGION = SEQ > TILE ? SEQ : TILE;
@@ -836,7 +848,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
                : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
   constexpr bool TMA = K::TMA_OK && PF_M_TMA;
-  if (TMA && !nyq && (C::M == 1 || !SL)) {
+  if (TMA && !nyq && B.tma) {
     // one 2D bulk tensor copy of the (N rows x CM columns) tile, 128B-swizzled
     // (long sequences: M copies of 256 rows, 64B-swizzled)
     __shared__ uint64_t mbar;
@@ -844,7 +856,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
       mbar_init(&mbar);
       mbar_expect(&mbar, (uint32_t)K::TILE);
       const int x0 = 2 * ch * CM;  // doubles
-      if constexpr (C::M > 1) {
+      if (C::M > 1 && !(SL && INV)) {
 #pragma unroll
         for (int b = 0; b < C::M; ++b) {
           const int y0 = (c * l0 + i0) * N + b * C::L;
@@ -878,7 +890,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     const unsigned char* tile = reg;
     // 16-byte chunk q of tile row e (64B swizzle: chunk ^ (e / 2) mod 4; 128B: ^ e mod 8)
     auto at = [&](int e, int q) -> double2 {
-      const int sw = K::ROWB == 64 ? ((e >> 1) & 3) : (e & 7);
+      const int sw = swz16<K::ROWB>(e);
       return *reinterpret_cast<const double2*>(tile + (size_t)e * K::ROWB + ((q ^ sw) << 4));
     };
     if constexpr (C::M > 1) {
@@ -1043,7 +1055,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
     return nyq ? (size_t)(i0 * 3 + c) * l1 + k1b + q : ((size_t)(c * N + i0) * l1 + k1) * H + ch * CP + q;
   };
   constexpr bool TMA = K::TMA_OK && PF_PK_TMA;
-  const bool tma = TMA && !nyq && (C::M == 1 || !SL);
+  const bool tma = TMA && !nyq && B.tma;
   __shared__ uint64_t mbar;
   if (tma) {
     if (t == 0) {  // three 3D tensor copies: component c's (CP columns x N rows i0) pencil
@@ -1103,7 +1115,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
 #pragma unroll
           for (int b = 0; b < C::M; ++b) {
             const int e = j + C::L * b;
-            const int sw = K::ROWB == 64 ? ((e >> 1) & 3) : (e & 7);
+            const int sw = swz16<K::ROWB>(e);
             a[it][b] = *reinterpret_cast<const double2*>(box + (size_t)e * K::ROWB + ((q ^ sw) << 4));
           }
           Dft<C::M, false>::run(a[it]);
@@ -1137,7 +1149,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
 #pragma unroll
         for (int n1 = 0; n1 < A; ++n1) {  // row e = i0, column q: 16B chunk XOR-swizzled by (e / 2) mod 4 (64B)
           const int e = BB * n1 + l;       // or by e mod 8 (128B)
-          const int sw = K::ROWB == 64 ? ((e >> 1) & 3) : (e & 7);
+          const int sw = swz16<K::ROWB>(e);
           x[n1] = *reinterpret_cast<const double2*>(box + (size_t)e * K::ROWB + ((q ^ sw) << 4));
         }
       }
@@ -1376,6 +1388,12 @@ static int set_attrs(FusedPlan* f) {
 // 2D tensor map of a [3 N N rows][N/2 complex] array, box = (CM complex, N rows),
 // 128B swizzle (the axis-1 passes' tile); encoded through the runtime's driver
 // entry point so the library does not link libcuda directly.
+static CUtensorMapSwizzle swizzle_for(int row_bytes) {
+  return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                             : (row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
+}
+
 static int encode_axis1_rows(CUtensorMap* tm, const double2* base, int N, int cm, int64_t rows);
 int encode_axis1_map(CUtensorMap* tm, const double2* base, int N, int cm, int ncomp) {
   return encode_axis1_rows(tm, base, N, cm, (int64_t)ncomp * N * N);
@@ -1398,7 +1416,7 @@ static int encode_axis1_rows(CUtensorMap* tm, const double2* base, int N, int cm
   cuuint32_t box[2] = {(cuuint32_t)2 * cm, (cuuint32_t)(N > 256 ? 256 : N)};  // (box rows <= 256)
   cuuint32_t es[2] = {1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, gdim, gstride, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, cm * 16 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cm * 16),
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -1434,7 +1452,7 @@ static int encode_pk_map_gen(CUtensorMap* tm, const double2* base, int N, int cp
   cuuint32_t box[3] = {(cuuint32_t)2 * cp, 1, (cuuint32_t)(N > 256 ? 256 : N)};  // (box rows <= 256)
   cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, gdim, gstride, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, cp * 16 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cp * 16),
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -1497,15 +1515,14 @@ int fused_ensure(pf_plan* p) {
     default: fz::pass1_twiddles<1024>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
-  if (N == 128 || N == 256) {
-    const int cm = N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM;
+  f->b.tma = 0;
+  if (N >= 128) {  // TMA maps (N > 256: M boxes of 256 rows per tile / component pencil)
+    const int cm = N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : (N == 512 ? fz::M2<512>::CM : fz::M2<1024>::CM));
+    const int cp = N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : (N == 512 ? fz::PK2<512>::CP : fz::PK2<1024>::CP));
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
-    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP, 3));
-  } else if (N == 512) {  // two 256-row boxes per tile / component pencil
-    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, fz::M2<512>::CM, 3));
-    PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, fz::M2<512>::CM, 3));
-    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, fz::PK2<512>::CP, 3));
+    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, cp, 3));
+    f->b.tma = 1;
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
@@ -1795,7 +1812,7 @@ static int encode_yx_map(CUtensorMap* tm, const double2* base, int N, int cm, in
   cuuint32_t box[5] = {(cuuint32_t)2 * cm, (cuuint32_t)l1, 1, (cuuint32_t)P, 1};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, gdim, gstride, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cm * 16), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (5D) failed (%d)", (int)r);
@@ -1875,12 +1892,14 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
   PF_CK_CUDA(cudaMalloc(&f->spec, sizeof(double2) * 3 * (size_t)l0 * N * (H + 1)));
   PF_CK_FFT(cufftSetWorkArea(f->plan2d, f->ws));
   PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
-  if (N == 128 || N == 256) {  // TMA maps of this slab's layouts
-    const int cm = N == 128 ? fz::M2<128>::CM : fz::M2<256>::CM;
-    const int cp = N == 128 ? fz::PK2<128>::CP : fz::PK2<256>::CP;
+  f->b.tma = 0;
+  if (N >= 128 && l1 <= 256 && N / l1 <= 256) {  // TMA maps of this slab's layouts (box dims <= 256)
+    const int cm = N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : (N == 512 ? fz::M2<512>::CM : fz::M2<1024>::CM));
+    const int cp = N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : (N == 512 ? fz::PK2<512>::CP : fz::PK2<1024>::CP));
     PF_CK(encode_yx_map(&f->tm_y, Yx, N, cm, l0, l1));
     PF_CK(encode_axis1_rows(&f->tm_xr, f->b.XR, N, cm, 3 * (int64_t)l0 * N));
     PF_CK(encode_pk_map_l1(&f->tm_pk, Yy, N, cp, l1));
+    f->b.tma = 1;
   }
   switch (N) {
     case 64: PF_CK(set_attrs<64>(f)); break;
