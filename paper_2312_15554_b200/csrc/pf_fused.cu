@@ -68,6 +68,18 @@
 #ifndef PF_PK512_MINB
 #define PF_PK512_MINB 2
 #endif
+#ifndef PF_PK1024_T  // PK at N = 1024
+#define PF_PK1024_T 128
+#endif
+#ifndef PF_PK1024_CP
+#define PF_PK1024_CP 1
+#endif
+#ifndef PF_PK1024_MINB
+#define PF_PK1024_MINB 3
+#endif
+#ifndef PF_RS1024_T
+#define PF_RS1024_T 64
+#endif
 #ifndef PF_RS512_T  // RS threads at N = 512 (one row pair per tile: 2 block transforms of 16 lanes)
 #define PF_RS512_T 64  // (measured 3.93 ms vs 4.38 at 32 and 4.48 at 128)
 #endif
@@ -130,7 +142,7 @@ struct RS2 {
   // threads per block: one FFT group per row pair (every thread FFT-active) for
   // N <= 128; for N = 256 one group per row (measured: 128^3 RS 0.071 vs 0.088 ms,
   // 256^3 0.483 vs 0.512 ms the other way round)
-  static constexpr int T = N == 1024 ? 64 : (N == 512 ? PF_RS512_T : R * C::G / (PF_RS_HALFT(N) ? 2 : 1));
+  static constexpr int T = N == 1024 ? PF_RS1024_T : (N == 512 ? PF_RS512_T : R * C::G / (PF_RS_HALFT(N) ? 2 : 1));
   static constexpr int V = R * N;               // voxels per tile
   static constexpr int VPT = V / T;             // voxels per thread
   static constexpr int NP = R / 2;              // inverse sequences (two rows each)
@@ -755,15 +767,15 @@ __global__ void __launch_bounds__(kThreads) k_pore_a_lam(int64_t n, const uint8_
 template <int N>
 struct PK2 {
   using C = Cfg<N>;
-  static constexpr int T = N == 512 ? PF_PK512_T : PF_PK_THREADS;
-  static constexpr int MINB = N == 512 ? PF_PK512_MINB : PF_PK_MINB;
+  static constexpr int T = N == 512 ? PF_PK512_T : (N == 1024 ? PF_PK1024_T : PF_PK_THREADS);
+  static constexpr int MINB = N == 512 ? PF_PK512_MINB : (N == 1024 ? PF_PK1024_MINB : PF_PK_MINB);
   static constexpr int NGP = T / C::G;
   // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
 #ifdef PF_PK_CP
   static constexpr int CP = PF_PK_CP;
 #else
   // (a long sequence takes M groups: NGP / M sequences per round)
-  static constexpr int CP = N == 512 ? PF_PK512_CP : (((NGP / C::M) % 3 == 0) ? NGP / C::M / 3 : NGP / C::M / 2);
+  static constexpr int CP = N == 512 ? PF_PK512_CP : (N == 1024 ? PF_PK1024_CP : (((NGP / C::M) % 3 == 0) ? NGP / C::M / 3 : NGP / C::M / 2));
 #endif
   static constexpr int NSEQ = 3 * CP;
   static constexpr int NCH = C::H / CP;
@@ -778,7 +790,7 @@ struct PK2 {
   // (CP = 8: 128-byte box rows, SWIZZLE_128B)
   static constexpr int ROWB = CP * 16;  // box row bytes
   static constexpr bool TMA_OK = ((N == 128 || N == 256) && (ROWB == 64 || ROWB == 128)) || (N == 512 && ROWB == 64) ||
-                                 (N == 1024 && ROWB == 16);
+                                 (N == 1024 && (ROWB == 16 || ROWB == 32));
   static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
   static constexpr size_t BOX = sizeof(double2) * CP * N;
   static constexpr size_t BOX_AL = ROWB == 128 ? 1024 : 512;  // swizzle-atom alignment of a box

@@ -4,7 +4,7 @@ exchange blocks zero (tests/slab_loopback.py SoloComm), fused and cuFFT slab
 pipelines, CUDA-event time per iteration.  Exchanges are local copies here, so
 this is the rank's compute share; DESIGN.md §6 adds the NVLink exchange.
 
-    python tools/slab_rank_probe.py [N] [P] [iters]
+    python tools/slab_rank_probe.py [N] [P] [iters] [fused|both]
 """
 
 import json
@@ -58,8 +58,9 @@ if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
     world = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     iters = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+    which = sys.argv[4] if len(sys.argv) > 4 else "both"
     res = {}
-    for fused in (True, False):
+    for fused in ((True,) if which == "fused" else (True, False)):
         ms = run(n, world, iters if fused else max(2, iters // 2), fused)
         res["fused" if fused else "cufft"] = {"ms_per_iter": ms, "rank_voxel_iters_per_s": n ** 3 / world / (ms / 1e3)}
     print(json.dumps({"grid": n, "ranks": world, "rank": 0, "pipelines": res}))
