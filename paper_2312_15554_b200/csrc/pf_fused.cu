@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   constexpr int SPR = N / 32;  // 32-voxel segments per row
   const int CS = cp.cs;
   static_assert(T % 32 == 0, "segment bases are per warp");
-  if (V != 1024) return;  // segment bases assume 32 segments of 32 voxels per tile (never launched otherwise)
+  // segment bases: groups of 32 segments of 32 voxels (V = 1024: one; 2048 at N = 1024: two)
+  constexpr int SG = V / 1024;
+  if (V != 1024 && V != 2048) return;  // (never launched otherwise)
   pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -500,7 +502,9 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     if (t == 0 && has_next) offs(tile + gridDim.x);  // next tile's row offsets, loaded early
     mbar_wait(&mbar, phase);
     const uint32_t o0 = ros[phase][0];
-    const int sb = seg_base<N>(sh + lane * 32, ros[phase][lane / SPR] - o0, lane);
+    int sb[2 > SG ? 2 : SG];
+#pragma unroll
+    for (int q = 0; q < SG; ++q) sb[q] = seg_base<N>(sh + q * 1024 + lane * 32, ros[phase][(q * 1024 + lane * 32) / N] - o0, lane);
     // (1) inverse: two rows per complex FFT (Hermitian extension of each half spectrum)
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
         const double s4 = u1 - su[v];
         acc[4] += s4 * s4;
         double t1 = u1, a1 = 0.0;
-        const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
+        const int segb = __shfl_sync(0xffffffffu, (SG == 1 || (v >> 10) == 0) ? sb[0] : sb[1], (v >> 5) & 31);
         if (solid) {
           const int ci = segb + __popc(mask & ((1u << lane) - 1u));
           const double t0 = sc[ci], a0 = sc[CS + ci], l0 = sc[2 * CS + ci];
@@ -599,7 +603,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   const int NT = 3 * TPC;
   constexpr int SPR = N / 32;
   static_assert(T % 32 == 0, "segment bases are per warp");
-  if (V != 1024) return;  // segment bases assume 32 segments of 32 voxels per tile (never launched otherwise)
+  constexpr int SG = V / 1024;  // segment-base groups (see k_rs_compact)
+  if (V != 1024 && V != 2048) return;  // (never launched otherwise)
   pdl_wait();
   if (ctrl->done || ctrl->db == 0.0) return;
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -612,13 +617,16 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
     const int c = tile / TPC;
     const int64_t row0 = ((int64_t)(tile % TPC) * R + (SL ? (int64_t)B.i0a * N : 0));
     const uint32_t o0 = cp.off[row0];
-    const int sb = seg_base<N>(Hs + row0 * N + lane * 32, cp.off[row0 + lane / SPR] - o0, lane);
+    int sb[2 > SG ? 2 : SG];
+#pragma unroll
+    for (int q = 0; q < SG; ++q)
+      sb[q] = seg_base<N>(Hs + row0 * N + q * 1024 + lane * 32, cp.off[row0 + (q * 1024 + lane * 32) / N] - o0, lane);
     __syncthreads();
     for (int j = 0; j < K::VPT; ++j) {
       const int v = t + T * j, row = v / N, col = v % N;
       const bool solid = Hs[row0 * N + v] != 0;
       const unsigned mask = __ballot_sync(0xffffffffu, solid);
-      const int segb = __shfl_sync(0xffffffffu, sb, v >> 5);
+      const int segb = __shfl_sync(0xffffffffu, (SG == 1 || (v >> 10) == 0) ? sb[0] : sb[1], (v >> 5) & 31);
       double val = u[(int64_t)c * n + row0 * N + v];
       if (solid) val = cp.ut[(int64_t)c * cp.ns + o0 + segb + __popc(mask & ((1u << lane) - 1u))];
       reinterpret_cast<double*>(SF + (row >> 1) * SS + C::sp(col))[row & 1] = val;
@@ -1621,8 +1629,8 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
   PF_CK(reduce_rows_to(p, p->partials, 2, nb, out));
   PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->work));
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
-  // (solid-only storage needs 1024-voxel RS tiles: N <= 512)
-  f->compact = (p->compact_enable && p->h_small[0] == 0.0 && fz::RS2<N>::V == 1024) ? 1 : 0;
+  // (solid-only storage: RS tiles of 1024 or 2048 voxels)
+  f->compact = (p->compact_enable && p->h_small[0] == 0.0 && fz::RS2<N>::V <= 2048) ? 1 : 0;
   f->nb_rs = f->compact ? f->nb_compact : f->nb_full;
   p->sc.lam_pore_sq = f->compact ? p->h_small[1] : 0.0;
   if (!f->compact) return PF_OK;
