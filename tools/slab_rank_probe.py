@@ -23,13 +23,39 @@ from paper_2312_15554_b200 import slab as S  # noqa: E402
 from slab_loopback import SoloComm  # noqa: E402
 
 
-def run(n, world, iters, fused):
+def stage_times(sol, be, iters):
+    """CUDA-event time of each fused-slab call (blocking exchange order)."""
+    names = ("fused_pk", "fused_rs", "finalize", "fused_mf")
+    ev = {k: [] for k in names}
+    orig = {k: getattr(be, k) for k in names}
+
+    def wrap(k):
+        def f(*a, **kw):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = orig[k](*a, **kw)
+            e1.record()
+            ev[k].append((e0, e1))
+            return r
+        return f
+
+    for k in names:
+        setattr(be, k, wrap(k))
+    sol.overlap = False
+    sol.iterate(iters, poll=False)
+    torch.cuda.synchronize()
+    for k in names:
+        setattr(be, k, orig[k])
+    return {k: sum(a.elapsed_time(b) for a, b in v) / max(1, len(v)) for k, v in ev.items()}
+
+
+def run(n, world, iters, fused, stages=False):
     dev = torch.device("cuda", 0)
     ind = pf.random_packing_geometry(n, seed=0)
     lo, hi = S.slab_range(n, world, 0)
     solid_np = np.ascontiguousarray(ind.values[lo:hi])
     del ind
-    cfg = pf.StokesConfig.with_tolerance(1e-12, pressure_gradient=(1.0, 0.0, 0.0), max_iter=iters + 4)
+    cfg = pf.StokesConfig.with_tolerance(1e-12, pressure_gradient=(1.0, 0.0, 0.0), max_iter=iters + 8)
     be = S.DeviceSlabBackend((n, n, n), world, 0, "central", dev)
     be.bind()
     L = (hi - lo) * n * n
@@ -47,11 +73,12 @@ def run(n, world, iters, fused):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / iters
+    st_ms = stage_times(sol, be, 3) if (stages and fused) else None
     sol.end()
     be.close()
     del sol, st, solid
     torch.cuda.empty_cache()
-    return ms
+    return (ms, st_ms) if stages else ms
 
 
 if __name__ == "__main__":
@@ -61,6 +88,9 @@ if __name__ == "__main__":
     which = sys.argv[4] if len(sys.argv) > 4 else "both"
     res = {}
     for fused in ((True,) if which == "fused" else (True, False)):
-        ms = run(n, world, iters if fused else max(2, iters // 2), fused)
+        out = run(n, world, iters if fused else max(2, iters // 2), fused, stages=fused)
+        ms, st = out if fused else (out, None)
         res["fused" if fused else "cufft"] = {"ms_per_iter": ms, "rank_voxel_iters_per_s": n ** 3 / world / (ms / 1e3)}
+        if st:
+            res["fused"]["stage_ms"] = st
     print(json.dumps({"grid": n, "ranks": world, "rank": 0, "pipelines": res}))
