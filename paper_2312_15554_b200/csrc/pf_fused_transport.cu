@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
   using C = Cfg<N>;
   using K = TPK<N>;
   constexpr int H = C::H, SS = C::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(16) unsigned char psraw[];
   unsigned char* reg = psraw + ((1024 - (fz::su32(psraw) & 1023)) & 1023);  // 1 KB-aligned
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
   using C = Cfg<N>;
   using K = TM<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(16) unsigned char msraw[];
   unsigned char* reg = msraw + ((1024 - (fz::su32(msraw) & 1023)) & 1023);  // 1 KB-aligned
@@ -439,6 +441,7 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
   using K = TRS<N>;
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V;
   constexpr int NT = N * N / R;
+  pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
   __shared__ uint64_t mbar;
@@ -792,22 +795,21 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
     return PF_OK;
   };
   PF_CK(mark(0));
-  ft::k_tpk<N><<<ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work>>>(f->b, P, p->ctrl, f->tm_pk);
-  PF_CK_CUDA(cudaGetLastError());
+  // programmatic dependent launches: every pass waits (pdl_wait) before its first access
+  PF_CK_CUDA(launch_k(ft::k_tpk<N>, ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work, f->b, P,
+                      (const Ctrl*)p->ctrl, f->tm_pk));
   PF_CK(mark(1));
-  ft::k_taxis<N, true><<<3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl,
-                                                                                      f->tm_y);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(launch_k(ft::k_taxis<N, true>, 3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
+                      (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_y));
   PF_CK(mark(2));
-  ft::k_trs<N><<<f->nb_trs, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work>>>(f->b, P, p->t_u, p->s_solid, p->ctrl);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(launch_k(ft::k_trs<N>, f->nb_trs, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work, f->b, P,
+                      (const double*)p->t_u, (const uint8_t*)p->s_solid, (const Ctrl*)p->ctrl));
   PF_CK(mark(3));
   transport_finalize_launch(p, f->b.part, ft::TPK<N>::TILES, p->g.inv_n);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  ft::k_taxis<N, false><<<2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work>>>(f->b, p->kap[1], p->ctrl,
-                                                                                       f->tm_x);
-  PF_CK_CUDA(cudaGetLastError());
+  PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
+                      (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_x));
   PF_CK(mark(5));
   return PF_OK;
 }

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_transport_finalize(Ctrl* _
                                                                          double* __restrict__ hist, const double t1,
                                                                          const double t2, const int64_t max_iter,
                                                                          const double scale) {
+  pdl_wait();
   if (ctrl->done) return;
   double S[2];
   reduce_partials<2>(part, nb, S);
@@ -281,8 +282,8 @@ int transport_polarize(pf_plan* p, const double* grad, double* out) {
 
 void transport_finalize_launch(pf_plan* p, const double* part, int nb, double scale) {
   const TransportConst& C = p->tc;
-  k_transport_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, part, nb, p->t_hist, C.eps_tol1, C.eps_tol2,
-                                                            C.max_iter, scale);
+  launch_k(k_transport_finalize, 1, kFinalizeThreads, 0, p->work, p->ctrl, part, nb, p->t_hist, C.eps_tol1,
+           C.eps_tol2, C.max_iter, scale);
 }
 
 static int enqueue_transport(pf_plan* p) {
