@@ -352,19 +352,39 @@ def run_transport_workload(args):
     pen = pf.PenaltyParams(alpha=100.0, beta=100.0, b=100.0, adaptive=False)
     st, _ = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-4, pressure_gradient=(1.0, 0.0, 0.0),
                                                                        max_iter=200), pen)
-    cfg = pf.TransportConfig(pe=10.0, a0=0.55, eps=1e-12, composition_gradient=(1.0, 0.0, 0.0), max_iter=10**6)
     z = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev)  # noqa: E731
-    state = pf.DeviceTransportState(z(n, n, n), z(3, n, n, n))
-    solver = pf.TransportSolver(ind, st.u, cfg, state, dev, history_rows=args.warmup + args.steps + 4)
-    solver.begin()
-    solver.iterate(args.warmup, poll=False)
+    C = max(1, args.tcells)
+    solvers, streams = [], [torch.cuda.Stream(dev) for _ in range(C)]
+    for k in range(C):  # cfg 2's load cases: composition gradients e_1, e_2, e_3 under one flow
+        g = [0.0, 0.0, 0.0]
+        g[k % 3] = 1.0
+        cfg = pf.TransportConfig(pe=10.0, a0=0.55, eps=1e-12, composition_gradient=tuple(g), max_iter=10**6)
+        with torch.cuda.stream(streams[k]):
+            state = pf.DeviceTransportState(z(n, n, n), z(3, n, n, n))
+            s = pf.TransportSolver(ind, st.u, cfg, state, dev, history_rows=args.warmup + args.steps + 4,
+                                   plan_slot=k)
+            s.begin()
+            s.iterate(args.warmup, poll=False)
+        solvers.append(s)
     torch.cuda.synchronize()
+    main = torch.cuda.current_stream(dev)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    solver.iterate(args.steps, poll=False)
+    for st_k in streams:
+        st_k.wait_stream(main)
+    done = 0
+    while done < args.steps:
+        k = min(8, args.steps - done)
+        for j, s in enumerate(solvers):
+            with torch.cuda.stream(streams[j]):
+                s.iterate(k, poll=False)
+        done += k
+    for st_k in streams:
+        main.wait_stream(st_k)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
+    solver = solvers[0]
     import ctypes
 
     from paper_2312_15554_b200 import _native as N
@@ -373,12 +393,17 @@ def run_transport_workload(args):
     N.check(N.load().pf_transport_profile(solver.plan.handle, 3, sm))
     res = solver.end()
     assert res.iterations == args.warmup + args.steps + 3 and not res.diverged and not res.converged
+    for j, s in enumerate(solvers[1:], 1):
+        with torch.cuda.stream(streams[j]):
+            r = s.end()
+        assert r.iterations == args.warmup + args.steps and not r.diverged
     peak, _ = peak_hbm()
-    value = n ** 3 * args.steps / (ms / 1e3)
+    value = C * n ** 3 * args.steps / (ms / 1e3)
     print(json.dumps({"metric": "transport voxel-iters/s (secondary)", "value": value, "unit": UNIT,
                       "ms_per_step": ms / args.steps, "steps": args.steps, "warmup": args.warmup,
                       "pipeline": solver.pipeline, "dtype": "f64",
-                      "config": {"workload": f"transport_sphere_{n}^3", "pe": 10.0, "a0": 0.55},
+                      "config": {"workload": f"transport_sphere_{n}^3", "pe": 10.0, "a0": 0.55,
+                                 "concurrent_solves": C},
                       "roofline_201B": {"alg_bytes_per_voxel_iter": 201, "achieved_GB_s": 201 * value / 1e9,
                                         "frac": 201 * value / 1e9 / peak},
                       "stages_ms": dict(zip(("PK_T", "MI_T", "RS_T", "finalize", "MF_T"), list(sm)))}),
@@ -541,6 +566,8 @@ def main():
                     help="stokes = the headline metric; transport / ensemble = secondary lines")
     ap.add_argument("--cells", type=int, default=8, help="cells per GPU for --workload ensemble")
     ap.add_argument("--slab-cufft", action="store_true", help="--workload slab: the cuFFT slab pipeline")
+    ap.add_argument("--tcells", type=int, default=1,
+                    help="--workload transport: concurrent solves (cfg 2's load cases e_1..e_3), own plan + stream each")
     args = ap.parse_args()
     if args.workload == "transport":
         return run_transport_workload(args)
