@@ -521,8 +521,11 @@ def run_slab_workload(args):
     st["q"] = torch.zeros(L, dtype=torch.float64, device=dev)
     solid = torch.as_tensor(np.ascontiguousarray(ind.values[lo:hi])).reshape(-1).to(dev)
     fused = be.fused_sizes()[0] > 0 and not args.slab_cufft
-    cls = S.FusedSlabStokes if fused else S.SlabStokes
-    sol = cls(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st)
+    if fused:
+        comm = S.SymmetricMemoryExchange() if (args.exchange == "p2p" and world > 1) else None
+        sol = S.FusedSlabStokes(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st, comm=comm, exchange=args.exchange)
+    else:
+        sol = S.SlabStokes(be, (n, n, n), cfg, pf.PenaltyParams(), solid, st)
     sol.begin()
     sol.iterate(args.warmup, poll=False)
     torch.cuda.synchronize()
@@ -545,7 +548,9 @@ def run_slab_workload(args):
         print(json.dumps({"metric": "Stokes ALM voxel-iters/s, one slab-decomposed cell (secondary, cfg 5)",
                           "value": value, "unit": UNIT, "n_gpus": world, "ms_per_step": ms / args.steps,
                           "steps": args.steps, "warmup": args.warmup, "scaling": "strong", "dtype": "f64",
-                          "pipeline": ("slab-fused (fused passes, Y all_to_all between PK and the axis-1 passes)"
+                          "pipeline": (("slab-fused (fused passes; PK / MF store into the owners' Y over P2P)"
+                                        if args.exchange == "p2p" else
+                                        "slab-fused (fused passes, per-component Y all_to_all overlapped)")
                                        if fused else "slab (cuFFT local transforms + all_to_all)"),
                           "config": {"workload": f"slab_random_packing_{n}^3", "ranks": world}}), flush=True)
     if world > 1:
@@ -566,6 +571,8 @@ def main():
                     help="stokes = the headline metric; transport / ensemble = secondary lines")
     ap.add_argument("--cells", type=int, default=8, help="cells per GPU for --workload ensemble")
     ap.add_argument("--slab-cufft", action="store_true", help="--workload slab: the cuFFT slab pipeline")
+    ap.add_argument("--exchange", default="a2a", choices=("a2a", "p2p"),
+                    help="--workload slab: all_to_all exchange or the transpose fused into the passes over P2P")
     ap.add_argument("--tcells", type=int, default=1,
                     help="--workload transport: concurrent solves (cfg 2's load cases e_1..e_3), own plan + stream each")
     args = ap.parse_args()

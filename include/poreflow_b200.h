@@ -181,6 +181,15 @@ int pf_slab_fused_end(pf_plan* plan, double* Q_tspec);
 int pf_slab_fused_rs_part(pf_plan* plan, int comp);
 int pf_slab_fused_totals(pf_plan* plan, double* totals9);
 int pf_slab_fused_mf_part(pf_plan* plan, int comp, int fix);
+/* Peer-memory exchange (the transpose fused into the passes' stores): device
+ * addresses, valid in this process (P2P-mapped, e.g. torch symmetric memory), of
+ * every rank's Y buffers — y-slab main / Nyquist, x-slab main / Nyquist, one per
+ * rank, npeers = P.  PK then stores its output straight into the x-slab owners'
+ * Yx and MF into the y-slab owners' Yy; the caller replaces each all_to_all by a
+ * cross-rank barrier (all ranks' stores visible) before the consuming pass.
+ * npeers = 0 restores the all_to_all exchange. */
+int pf_slab_fused_set_peers(pf_plan* plan, const uint64_t* yy, const uint64_t* yy_nyq, const uint64_t* yx,
+                            const uint64_t* yx_nyq, int npeers);
 
 /* ------------------------------------------------------------------------
  * Transport — replaces poreflow.transport.solve_transport

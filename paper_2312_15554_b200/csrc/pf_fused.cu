@@ -95,6 +95,12 @@ __device__ __forceinline__ int swz16(int e) {
   return RB == 128 ? (e & 7) : (RB == 64 ? ((e >> 1) & 3) : (RB == 32 ? ((e >> 2) & 1) : 0));
 }
 
+constexpr int kMaxRanks = 16;
+struct Peers {
+  double2 *yy[kMaxRanks], *yyn[kMaxRanks];  // y-slab Y of each rank
+  double2 *yx[kMaxRanks], *yxn[kMaxRanks];  // x-slab Y of each rank
+};
+
 struct Bufs {
   double2 *XU, *XUn;  // X-space (after axis 2): u' (MI -> RS); X(u~') when b changed (RS-fix -> MF)
   double2 *XR, *XRn;  // X-space R = b u~' - a' (RS -> MF)   [3][N*N][H], [3][N*N]
@@ -119,6 +125,10 @@ struct Bufs {
   int i0a, nl, pst, poff;
   // the host encoded the TMA tensor maps of this layout (else the passes stage with LDGSTS)
   int tma;
+  // peer-memory exchange (slab, P2P-mapped Y buffers of every rank; null = exchange by
+  // all_to_all): PK stores straight into the x-slab owners' Yx, MF into the y-slab
+  // owners' Yy, so the transpose rides on the passes' own stores over NVLink
+  const struct Peers* peers;
   // component window of one launch of MI / RS (SL kernels): components [c0, c0 + nc)
   int c0, nc;
 };
@@ -1029,8 +1039,15 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
     const int q = nyq ? idx / N : idx % CM, e = nyq ? idx % N : idx / CM;
     const double2 v = S[q * SS + (INV ? C::sp(e) : C::kp(e))];
     if (!INV) {
-      const size_t o = yoff_of(e, q);
-      if (nyq) B.Yxn[o] = v; else B.Yx[o] = v;
+      if (SL && B.peers) {  // to the owner of k1: its y-slab Y [c][i0][k1 - k1off][k2], Yn [i0][c][k1 - k1off]
+        const int r = e >> s1, kl = e & (l1 - 1);
+        const int i0g = (B.k1off >> s1) * l0 + (nyq ? i0b + q : i0);
+        if (nyq) B.peers->yyn[r][(size_t)(i0g * 3 + c) * l1 + kl] = v;
+        else B.peers->yy[r][((size_t)(c * N + i0g) * l1 + kl) * H + ch * CM + q] = v;
+      } else {
+        const size_t o = yoff_of(e, q);
+        if (nyq) B.Yxn[o] = v; else B.Yx[o] = v;
+      }
     } else {
       const size_t o = off_of(e, q);
       if (nyq) B.XUn[o] = v; else B.XU[o] = v;
@@ -1254,7 +1271,14 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
     const size_t o = yoff(c, i0, q);
     const double2 v = S[(c * CP + q) * SS + C::sp(i0)];
-    if (nyq) B.Yn[o] = v; else B.Y[o] = v;
+    if (SL && B.peers) {  // to the owner of i0: its x-slab Y [c][r][i0l][k1 - r l1][k2], Yn [r][i0l][c][k1 - r l1]
+      const int l0 = B.l0, me = B.k1off >> B.s1, r = i0 / l0, i0l = i0 - r * l0, P = N >> B.s1;
+      const int kl = nyq ? k1b + q : k1;
+      if (nyq) B.peers->yxn[r][((size_t)(me * l0 + i0l) * 3 + c) * l1 + kl] = v;
+      else B.peers->yx[r][(((size_t)(c * P + me) * l0 + i0l) * l1 + kl) * H + ch * CP + q] = v;
+    } else {
+      if (nyq) B.Yn[o] = v; else B.Y[o] = v;
+    }
   }
   block_sum<3>(acc);
   if (t == 0)
@@ -1349,6 +1373,7 @@ struct FusedPlan {
   void* ws = nullptr;        // cuFFT work area of plan2d
   double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
   int nb_full = kSMs, nb_compact = kSMs;
+  fz::Peers* peers = nullptr;  // device copy of the peer pointer table (P2P exchange)
 };
 
 static FusedPlan* fp_of(pf_plan* p) { return reinterpret_cast<FusedPlan*>(p->fused); }
@@ -1587,6 +1612,7 @@ void fused_free(pf_plan* p) {
   cudaFree(f->c_data);
   cudaFree(f->ws);
   cudaFree(f->spec);
+  cudaFree(f->peers);
   delete f;
   p->fused = nullptr;
 }
@@ -2076,6 +2102,33 @@ int fused_slab_totals(pf_plan* p, double* totals) { PF_FSLAB_DISPATCH(fslab_tota
 int fused_slab_mf(pf_plan* p) { PF_FSLAB_DISPATCH(fslab_mf_t, p, 0, 3, true) }
 int fused_slab_mf_part(pf_plan* p, int comp, int fix) { PF_FSLAB_DISPATCH(fslab_mf_t, p, comp, 1, fix != 0) }
 #undef PF_FSLAB_DISPATCH
+
+// Peer-memory exchange: device addresses of every rank's Y buffers (P2P-mapped
+// into this process), or npeers = 0 to go back to the all_to_all exchange.
+int fused_slab_set_peers(pf_plan* p, const uint64_t* yy, const uint64_t* yyn, const uint64_t* yx,
+                         const uint64_t* yxn, int npeers) {
+  FusedPlan* f = fp_of(p);
+  if (npeers == 0) {
+    f->b.peers = nullptr;
+    return PF_OK;
+  }
+  const int P = f->N / f->b.l1;
+  if (npeers != P || P > fz::kMaxRanks) {
+    set_error("peer table needs one entry per rank (%d ranks, at most %d)", P, fz::kMaxRanks);
+    return PF_ERR_ARG;
+  }
+  fz::Peers h{};
+  for (int r = 0; r < P; ++r) {
+    h.yy[r] = reinterpret_cast<double2*>(yy[r]);
+    h.yyn[r] = reinterpret_cast<double2*>(yyn[r]);
+    h.yx[r] = reinterpret_cast<double2*>(yx[r]);
+    h.yxn[r] = reinterpret_cast<double2*>(yxn[r]);
+  }
+  if (!f->peers) PF_CK_CUDA(cudaMalloc(&f->peers, sizeof(fz::Peers)));
+  PF_CK_CUDA(cudaMemcpy(f->peers, &h, sizeof(h), cudaMemcpyHostToDevice));
+  f->b.peers = f->peers;
+  return PF_OK;
+}
 
 // Q^ back to the slab T layout (unscaled) and the compact multipliers materialised.
 int fused_slab_end(pf_plan* p, double2* Tq) {

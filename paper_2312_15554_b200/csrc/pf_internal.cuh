@@ -209,6 +209,8 @@ int fused_slab_mf(pf_plan* p);
 int fused_slab_rs_part(pf_plan* p, int comp);
 int fused_slab_totals(pf_plan* p, double* totals);
 int fused_slab_mf_part(pf_plan* p, int comp, int fix);
+int fused_slab_set_peers(pf_plan* p, const uint64_t* yy, const uint64_t* yyn, const uint64_t* yx,
+                         const uint64_t* yxn, int npeers);
 int fused_slab_end(pf_plan* p, double2* Tq);
 int fused_is_compact(const pf_plan* p);
 // fused transport pipeline (pf_fused_transport.cu)

@@ -467,6 +467,14 @@ int pf_slab_fused_mf_part(pf_plan* p, int comp, int fix) {
   return leave(p);
 }
 
+int pf_slab_fused_set_peers(pf_plan* p, const uint64_t* yy, const uint64_t* yyn, const uint64_t* yx,
+                            const uint64_t* yxn, int npeers) {
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_ARG(npeers == 0 || (yy && yyn && yx && yxn), "null argument");
+  return fused_slab_set_peers(p, yy, yyn, yx, yxn, npeers);
+}
+
 int pf_slab_fused_end(pf_plan* p, double* Tq) {
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));

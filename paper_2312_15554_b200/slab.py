@@ -138,6 +138,12 @@ class DeviceSlabBackend:
     def fused_mf_part(self, comp, fix):
         N.check(self.lib.pf_slab_fused_mf_part(self.h, int(comp), 1 if fix else 0))
 
+    def fused_set_peers(self, yy, yyn, yx, yxn):
+        """Peer-memory exchange: lists (rank order) of every rank's Y buffer
+        addresses, mapped in this process; empty lists restore all_to_all."""
+        arr = lambda v: (ctypes.c_uint64 * max(1, len(v)))(*[int(x) for x in v])  # noqa: E731
+        N.check(self.lib.pf_slab_fused_set_peers(self.h, arr(yy), arr(yyn), arr(yx), arr(yxn), len(yy)))
+
     def fused_end(self, Q):
         N.check(self.lib.pf_slab_fused_end(self.h, self._p(Q)))
 
@@ -306,19 +312,36 @@ class FusedSlabStokes(SlabStokes):
     no packing pass; at P = 1 both layouts coincide and nothing moves."""
 
     def __init__(self, backend, dims, cfg, penalties, solid_local, state, group=None, poll_every: int = 8,
-                 comm=None, overlap: bool = True):
+                 comm=None, overlap: bool = True, exchange: str = "a2a"):
+        """``exchange``: "a2a" — all_to_all of the Y buffers between the passes
+        (per component and overlapped when ``overlap``); "p2p" — the transpose
+        fused into the passes: the Y buffers are P2P-mapped on every rank
+        (``comm.p2p_alloc`` / ``p2p_ptrs``; torch symmetric memory on a GPU box,
+        see ``SymmetricMemoryExchange``), PK and MF store their output straight
+        into the owning ranks' buffers over NVLink, and a cross-rank barrier
+        (``comm.p2p_barrier``) replaces each exchange."""
         super().__init__(backend, dims, cfg, penalties, solid_local, state, group, poll_every, comm, overlap)
         be = backend
         ym, yn = be.fused_sizes()
         if ym == 0:
             raise ValueError("fused slab pipeline unsupported for this grid / rank count")
+        if exchange not in ("a2a", "p2p"):
+            raise ValueError("exchange must be 'a2a' or 'p2p'")
         self.ym, self.yn = ym, yn
-        self.Yy, self.Yyn = be.alloc_complex(ym), be.alloc_complex(yn)
-        if self.world > 1:
-            self.Yx, self.Yxn = be.alloc_complex(ym), be.alloc_complex(yn)
+        self.p2p = exchange == "p2p" and self.world > 1
+        if self.p2p:
+            alloc = lambda k: self.dist.p2p_alloc(2 * k, backend.dev)  # noqa: E731
+            self.Yy, self.Yyn, self.Yx, self.Yxn = alloc(ym), alloc(yn), alloc(ym), alloc(yn)
         else:
-            self.Yx, self.Yxn = self.Yy, self.Yyn
+            self.Yy, self.Yyn = be.alloc_complex(ym), be.alloc_complex(yn)
+            if self.world > 1:
+                self.Yx, self.Yxn = be.alloc_complex(ym), be.alloc_complex(yn)
+            else:
+                self.Yx, self.Yxn = self.Yy, self.Yyn
         be.fused_bind(self.Yy, self.Yyn, self.Yx, self.Yxn)
+        if self.p2p:
+            ptrs = [self.dist.p2p_ptrs(t) for t in (self.Yy, self.Yyn, self.Yx, self.Yxn)]
+            be.fused_set_peers(*ptrs)
         self._pending = []  # MF-side exchanges still in flight (overlapped mode)
 
     def _swap(self, src, srcn, dst, dstn):
@@ -358,6 +381,8 @@ class FusedSlabStokes(SlabStokes):
         PK waits for all of them.  Same arithmetic as the blocking order."""
         be = self.b
         info = {"done": False}
+        if self.p2p:
+            return self._iterate_p2p(n_iter, poll)
         ov = self.overlap and self.world > 1
         for _ in range(int(n_iter)):
             self._drain()
@@ -392,17 +417,77 @@ class FusedSlabStokes(SlabStokes):
                 self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
         return info
 
+    def _iterate_p2p(self, n_iter: int, poll: bool) -> dict:
+        """PK stores into the x-slab owners' Yx, MF into the y-slab owners' Yy;
+        each barrier orders every rank's stores before the consuming pass (and,
+        transitively, every rank's reads of a buffer before the next stores into it)."""
+        be, d = self.b, self.dist
+        info = {"done": False}
+        for _ in range(int(n_iter)):
+            be.fused_pk()
+            d.p2p_barrier()
+            be.fused_rs(self.totals)
+            d.all_reduce(self.totals, group=self.group)
+            be.finalize(self.totals)
+            be.fused_mf()
+            d.p2p_barrier()
+            self.it += 1
+            if poll and (self.it % self.poll == 0 or self.it == self.cfg.max_iter):
+                info = be.read()
+                if info["done"]:
+                    return info
+        return info
+
     def end(self) -> ConvergenceReport:
         self._drain()
         self.b.fused_end(self.Q)  # Q^ back to T layout; u~, a, lam materialised
         rep = super().end()
         rep.meta["pipeline"] = "slab-fused"
+        rep.meta["exchange"] = "p2p" if self.p2p else ("a2a-overlapped" if self.overlap else "a2a")
         return rep
+
+
+class SymmetricMemoryExchange:
+    """torch.distributed with the peer-memory calls of the p2p exchange: Y buffers
+    from torch symmetric memory (P2P-mapped into every rank over NVLink), their
+    peer addresses from the rendezvous, and its device-side barrier (stream
+    ordered, signal pads).  all_to_all_single / all_reduce go to the process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.dist, self.symm, self.group = dist, symm_mem, group or dist.group.WORLD
+        self.handles = {}
+
+    def get_world_size(self, group=None):
+        return self.dist.get_world_size(self.group)
+
+    def get_rank(self, group=None):
+        return self.dist.get_rank(self.group)
+
+    def all_to_all_single(self, out, inp, group=None, async_op=False):
+        return self.dist.all_to_all_single(out, inp, group=self.group, async_op=async_op)
+
+    def all_reduce(self, t, group=None):
+        return self.dist.all_reduce(t, group=self.group)
+
+    def p2p_alloc(self, numel, device):
+        t = torch()
+        buf = self.symm.empty(numel, dtype=t.float64, device=device)
+        self.handles[buf.data_ptr()] = self.symm.rendezvous(buf, self.group.group_name)
+        return buf
+
+    def p2p_ptrs(self, buf):
+        return list(self.handles[buf.data_ptr()].buffer_ptrs)
+
+    def p2p_barrier(self):
+        next(iter(self.handles.values())).barrier(channel=0)
 
 
 def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalties: PenaltyParams | None = None,
                       init_local: dict | None = None, group=None, device=None, comm=None, fused: bool | None = None,
-                      overlap: bool = True):
+                      overlap: bool = True, exchange: str = "a2a"):
     """Device slab solve on this rank: ``solid_local`` is the rank's x-slab of the
     indicator (uint8, (N0/P, N1, N2)); returns (local state dict of CUDA tensors,
     ConvergenceReport — identical on every rank)."""
@@ -434,7 +519,10 @@ def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalt
     if fused is None:
         fused = be.fused_sizes()[0] > 0
     cls = FusedSlabStokes if fused else SlabStokes
-    solver = cls(be, dims, cfg, penalties, solid, st, group, comm=comm, overlap=overlap)
+    kw = {"exchange": exchange} if fused else {}
+    if fused and exchange == "p2p" and comm is None and world > 1:
+        comm = SymmetricMemoryExchange(group)
+    solver = cls(be, dims, cfg, penalties, solid, st, group, comm=comm, overlap=overlap, **kw)
     rep = solver.solve()
     t.cuda.synchronize(dev)
     shp3, shp1 = (3, hi - lo, int(dims[1]), int(dims[2])), (hi - lo, int(dims[1]), int(dims[2]))

@@ -53,6 +53,27 @@ class _RankComm:
         self._meet()
         return _Done() if async_op else None
 
+    # peer-memory exchange: every rank's buffers live on the one GPU, so their
+    # plain device addresses serve as the P2P-mapped peer addresses
+    def p2p_alloc(self, numel, device):
+        import torch
+
+        return torch.empty(numel, dtype=torch.float64, device=device)
+
+    def p2p_ptrs(self, buf):
+        h = self.hub
+        h.slots[self.r] = buf.data_ptr()
+        self._meet()
+        ptrs = list(h.slots)
+        self._meet()
+        return ptrs
+
+    def p2p_barrier(self):
+        import torch
+
+        torch.cuda.synchronize()
+        self._meet()
+
     def all_reduce(self, t, group=None):
         import torch
 

@@ -81,12 +81,15 @@ def test_device_slab_multi_rank_loopback(pf, golden, case, world, overlap):
         assert rel_l2(full, z[k]) <= 1e-10, k
 
 
-@pytest.mark.parametrize("world,overlap", [(1, True), (2, True), (4, True), (2, False), (4, False)])
-def test_fused_slab_matches_fused_pipeline(pf, world, overlap):
+@pytest.mark.parametrize("world,overlap,exchange", [(1, True, "a2a"), (2, True, "a2a"), (4, True, "a2a"),
+                                                    (2, False, "a2a"), (4, False, "a2a"), (2, False, "p2p"),
+                                                    (4, False, "p2p")])
+def test_fused_slab_matches_fused_pipeline(pf, world, overlap, exchange):
     """The fused slab pipeline (pf_slab_fused_*) over P loopback ranks reproduces
     the single-GPU fused pipeline: same iterations, fields to round-off; both the
     component-pipelined exchange (pf_slab_fused_rs_part / _mf_part) and the
-    blocking one."""
+    blocking one, and the peer-memory exchange (PK / MF store straight into the
+    owning ranks' Y buffers; here every rank's buffers share the one GPU)."""
     from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
     from slab_loopback import run_ranks
 
@@ -97,7 +100,8 @@ def test_fused_slab_matches_fused_pipeline(pf, world, overlap):
 
     def rank_fn(r, comm):
         lo, hi = slab_range(64, world, r)
-        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True, overlap=overlap)
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True, overlap=overlap,
+                                    exchange=exchange)
         return {k: v.cpu().numpy() for k, v in st.items()}, rep
 
     res = run_ranks(world, rank_fn)
@@ -140,7 +144,8 @@ def test_fused_slab_full_solve_matches_reference(pf, golden):
     assert abs(np.linalg.norm(u) - z["u_norm"][0]) <= 1e-10 * z["u_norm"][0]
 
 
-def test_fused_slab_512_two_ranks_matches_fused_pipeline(pf):
+@pytest.mark.parametrize("exchange", ["a2a", "p2p"])
+def test_fused_slab_512_two_ranks_matches_fused_pipeline(pf, exchange):
     """Long-sequence fused passes (N = 512) on the slab layouts: two loopback
     ranks (256 x-planes each, overlapped per-component exchanges) against the
     single-GPU fused pipeline, truncated solve."""
@@ -159,12 +164,13 @@ def test_fused_slab_512_two_ranks_matches_fused_pipeline(pf):
 
     def rank_fn(r, comm):
         lo, hi = slab_range(512, 2, r)
-        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True)
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True, exchange=exchange)
         return st["u"].cpu().numpy(), rep
 
     res = run_ranks(2, rank_fn)
     for _, rep in res:
         assert rep.meta["pipeline"] == "slab-fused" and rep.iterations == rref.iterations == 3
+        assert rep.meta["exchange"] == ("p2p" if exchange == "p2p" else "a2a-overlapped")
     u = np.concatenate([x for x, _ in res], axis=1)
     assert rel_l2(u, u_ref) <= 1e-10
 
