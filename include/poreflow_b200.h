@@ -272,6 +272,11 @@ int pf_k_transport_mode_update(int ndim, const int64_t* dims, const double* w_ha
                                const double* lap, double a0, const double* b0_vec_host,
                                double* chi_hat, double* grad_hat, void* stream);
 
+/* Bit-packed indicator (1 bit per voxel, numpy.packbits order — the
+ * first voxel in the most significant bit of byte 0) -> uint8 0/1 per voxel, on
+ * the device: ceil(n / 8) bytes cross PCIe instead of n. */
+int pf_unpack_bits(const uint8_t* bits, uint8_t* out, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

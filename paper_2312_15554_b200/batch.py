@@ -18,6 +18,7 @@ from __future__ import annotations
 from typing import Sequence
 
 from .device import require_cuda, solid_on_device, to_device, torch
+from .grid import all_solid
 from .stokes import DeviceAdmmState, PenaltyParams, StokesConfig, StokesSolver, _fast_path
 from .transport import DeviceTransportState, TransportConfig, TransportSolver, _check_velocity
 
@@ -65,7 +66,7 @@ def solve_stokes_many_device(indicators: Sequence, cfgs: Sequence[StokesConfig],
             raise ValueError("pressure_gradient dimension does not match the grid")
         if pen.b <= 0.0:
             raise ValueError("coupling penalty b must be positive for the zero mode")
-        if ind.values.all():
+        if all_solid(ind):
             out[k] = (DeviceAdmmState.zeros(grid, dev), _fast_path(grid, cfg, pen))
             continue
         st = t.cuda.Stream(dev)

@@ -140,6 +140,23 @@ __global__ void k_tmu(KGeom g, KTabs T, const double2* wh, const double2* sh, co
   }
 }
 
+// numpy.packbits order (first voxel in the most significant bit of byte 0) ->
+// one uint8 0/1 per voxel; one byte in, eight out (one 8-byte store) per thread.
+__global__ void k_unpack_bits(const uint8_t* __restrict__ bits, uint8_t* __restrict__ out, int64_t n) {
+  const int64_t nbytes = (n + 7) / 8;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned v = bits[b];
+    unsigned long long w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w |= (unsigned long long)((v >> (7 - k)) & 1u) << (8 * k);
+    if (8 * b + 8 <= n && ((reinterpret_cast<uintptr_t>(out) & 7) == 0)) {
+      reinterpret_cast<unsigned long long*>(out)[b] = w;
+    } else {
+      for (int k = 0; k < 8 && 8 * b + k < n; ++k) out[8 * b + k] = (uint8_t)((w >> (8 * k)) & 0xffu);
+    }
+  }
+}
+
 static int finish(cudaStream_t s) {
   (void)s;
   PF_CK_CUDA(cudaGetLastError());
@@ -242,6 +259,15 @@ int pf_k_transport_mode_update(int ndim, const int64_t* dims, const double* w_ha
     case 2: k_tmu<2><<<nb, kThreads, 0, s>>>(g, T, W, S, lap, a0, b0[0], b0[1], b0[2], C, G); break;
     default: k_tmu<3><<<nb, kThreads, 0, s>>>(g, T, W, S, lap, a0, b0[0], b0[1], b0[2], C, G); break;
   }
+  return finish(s);
+}
+
+int pf_unpack_bits(const uint8_t* bits, uint8_t* out, int64_t n, void* stream) {
+  PF_ARG(n >= 0, "negative count");
+  if (n == 0) return PF_OK;
+  PF_ARG(bits && out, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  k_unpack_bits<<<blocks_for((n + 7) / 8), kThreads, 0, s>>>(bits, out, n);
   return finish(s);
 }
 

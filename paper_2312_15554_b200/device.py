@@ -138,8 +138,22 @@ def solid_on_device(indicator, device):
         return to_device(np.asarray(indicator.values, dtype=np.uint8), device, torch().uint8)
     key = device.index
     if key not in cache:
-        cache[key] = to_device(indicator.values, device, torch().uint8)
+        bits = getattr(indicator, "bits", None)
+        cache[key] = (_unpack_on_device(bits, indicator.grid.n_pts, device).reshape(indicator.grid.dims)
+                      if bits is not None else to_device(indicator.values, device, torch().uint8))
     return cache[key]
+
+
+def _unpack_on_device(bits, n: int, device):
+    """Packed indicator bytes -> device uint8 0/1 per voxel (pf_unpack_bits)."""
+    t = torch()
+    dbits = to_device(np.asarray(bits, dtype=np.uint8), device, t.uint8)
+    out = t.empty(n, dtype=t.uint8, device=device)
+    with t.cuda.device(device):
+        stream = t.cuda.current_stream(device).cuda_stream
+        N.check(N.load().pf_unpack_bits(ctypes.c_void_p(dbits.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                        int(n), ctypes.c_void_p(stream)))
+    return out
 
 
 _STAGE_BYTES = 16 << 20

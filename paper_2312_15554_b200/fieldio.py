@@ -28,7 +28,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .grid import IndicatorField, UnitCellGrid
+from .grid import IndicatorField, PackedIndicator, UnitCellGrid
 from .report import ConvergenceReport
 
 _FMT = "%.17g"
@@ -195,6 +195,25 @@ def load_indicator_raw(path, dims, dtype=np.uint8, threshold: float = 0.5) -> In
         raise ValueError(f"raw file holds {vals.size} values, dims {dims} need {int(np.prod(dims))}: {path}")
     values = (vals.reshape(dims) >= threshold).astype(np.uint8)
     return IndicatorField(UnitCellGrid(dims), values)
+
+
+def load_indicator_bits(path, dims) -> PackedIndicator:
+    """Bit-packed voxel file (numpy.packbits order, C order, ceil(prod(dims) / 8)
+    bytes): stays packed on the host; the device solvers unpack it on the GPU."""
+    path = Path(path)
+    if not path.exists():
+        raise FileNotFoundError(path)
+    return PackedIndicator(UnitCellGrid(tuple(int(n) for n in dims)), np.fromfile(path, dtype=np.uint8))
+
+
+def save_indicator_bits(indicator, path) -> Path:
+    """Write an indicator as a bit-packed voxel file (see ``load_indicator_bits``)."""
+    path = Path(path)
+    bits = getattr(indicator, "bits", None)
+    if bits is None:
+        bits = np.packbits(np.asarray(indicator.values, dtype=np.uint8).ravel())
+    np.asarray(bits, dtype=np.uint8).tofile(path)
+    return path
 
 
 def write_indicator(indicator: IndicatorField, path) -> Path:

@@ -98,6 +98,62 @@ class IndicatorField:
         return self.values.astype(np.float64)
 
 
+class PackedIndicator:
+    """Bit-packed solid indicator: 1 bit per voxel in numpy.packbits
+    order (the first voxel, C order, in the most significant bit of byte 0).
+    Accepted wherever an ``IndicatorField`` is: the device solvers copy the
+    ceil(n / 8) bytes to the GPU and unpack them there (``pf_unpack_bits``);
+    ``values`` unpacks on the host only for host consumers (cached)."""
+
+    def __init__(self, grid: UnitCellGrid, bits):
+        bits = np.ascontiguousarray(np.asarray(bits, dtype=np.uint8).ravel())
+        n = grid.n_pts
+        if bits.size != (n + 7) // 8:
+            raise ValueError(f"packed indicator needs {(n + 7) // 8} bytes for grid {grid.dims}, got {bits.size}")
+        if n % 8 and int(bits[-1]) & ((1 << (8 - n % 8)) - 1):
+            raise ValueError("padding bits of the last byte must be zero")
+        bits.setflags(write=False)
+        self.grid, self.bits = grid, bits
+        self._values = None
+        self._device_cache: dict = {}
+
+    @classmethod
+    def from_indicator(cls, indicator: IndicatorField) -> "PackedIndicator":
+        return cls(indicator.grid, np.packbits(np.asarray(indicator.values, dtype=np.uint8).ravel()))
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            v = np.unpackbits(self.bits, count=self.grid.n_pts).reshape(self.grid.dims)
+            v.setflags(write=False)
+            self._values = v
+        return self._values
+
+    def solid_count(self) -> int:
+        return int(np.bitwise_count(self.bits).sum())
+
+    def solid_fraction(self) -> float:
+        return self.solid_count() / self.grid.n_pts
+
+    def all_solid(self) -> bool:
+        return self.solid_count() == self.grid.n_pts
+
+    @property
+    def degenerate(self) -> bool:
+        frac = self.solid_fraction()
+        return frac == 0.0 or frac == 1.0
+
+    def as_float(self) -> np.ndarray:
+        return self.values.astype(np.float64)
+
+
+def all_solid(indicator) -> bool:
+    """True if every voxel is solid (the solvers' fast path); packed indicators
+    answer from a popcount of their bits."""
+    f = getattr(indicator, "all_solid", None)
+    return bool(f()) if f is not None else bool(np.asarray(indicator.values).all())
+
+
 def porosity(indicator: IndicatorField) -> float:
     """grid.py:108-110."""
     return 1.0 - indicator.solid_fraction()

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from .device import get_plan, require_cuda, solid_on_device, to_device, to_host_many, torch
-from .grid import IndicatorField
+from .grid import IndicatorField, all_solid
 from .report import ConvergenceReport
 from .spectral import CENTRAL, SYMBOL_MODES
 
@@ -284,7 +284,7 @@ def solve_stokes_device(indicator: IndicatorField, cfg: StokesConfig | None = No
     if penalties.b <= 0.0:
         raise ValueError("coupling penalty b must be positive for the zero mode")
     dev = require_cuda(device)
-    if indicator.values.all():
+    if all_solid(indicator):
         return DeviceAdmmState.zeros(grid, dev), _fast_path(grid, cfg, penalties)
     if init is not None:
         _validate_init(init, grid)

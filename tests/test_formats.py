@@ -106,3 +106,25 @@ def test_run_config_mirrors_reference():
     with pytest.raises(runner.ConfigError):
         runner.GeometrySpec(kind="cube").build()
     assert runner.GeometrySpec(kind="packing", resolution=32, seed=0).build().grid.dims == (32, 32, 32)
+
+
+def test_packed_indicator_roundtrip(tmp_path):
+    """Bit-packed indicator: numpy.packbits order, host values and
+    solid fraction equal the byte indicator's, file round trip, validation."""
+    import paper_2312_15554_b200 as pf
+
+    for dims in [(13, 7, 5), (16, 16, 16), (9, 11)]:
+        rng = np.random.default_rng(sum(dims))
+        ind = pf.IndicatorField(pf.UnitCellGrid(dims), (rng.random(dims) < 0.3).astype(np.uint8))
+        pk = pf.PackedIndicator.from_indicator(ind)
+        assert pk.bits.size == (ind.grid.n_pts + 7) // 8
+        assert np.array_equal(pk.values, ind.values) and pk.solid_fraction() == ind.solid_fraction()
+        f = pf.save_indicator_bits(pk, tmp_path / "ind.bits")
+        back = pf.load_indicator_bits(f, dims)
+        assert np.array_equal(back.values, ind.values)
+    full = pf.PackedIndicator.from_indicator(pf.IndicatorField(pf.UnitCellGrid((5, 5)), np.ones((5, 5), np.uint8)))
+    assert full.all_solid() and full.degenerate
+    with pytest.raises(ValueError):
+        pf.PackedIndicator(pf.UnitCellGrid((5, 5)), np.zeros(3, np.uint8))  # needs 4 bytes
+    with pytest.raises(ValueError):
+        pf.PackedIndicator(pf.UnitCellGrid((5, 5)), np.array([0, 0, 0, 0x7F], np.uint8))  # nonzero padding bits
