@@ -204,3 +204,29 @@ def test_fused_slab_rank_alone_matches_cufft_slab(pf, n, world):
     for k in ("u", "q", "lam"):
         assert rel_l2(out[True][k], out[False][k]) <= 1e-10, k
     assert np.linalg.norm(out[True]["u"]) > 0
+
+
+@pytest.mark.parametrize("exchange,overlap", [("a2a", True), ("p2p", False)])
+def test_fused_slab_eight_ranks_128(pf, exchange, overlap):
+    """P = 8 (16 x-planes / k1-planes per rank) at 128^3, both exchange modes,
+    against the single-GPU fused pipeline."""
+    from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
+    from slab_loopback import run_ranks
+
+    ind = pf.random_packing_geometry(128, seed=9)
+    cfg = pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=(0.2, 0.0, 1.0), max_iter=6)
+    ref, rref = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    vals = np.asarray(ind.values)
+
+    def rank_fn(r, comm):
+        lo, hi = slab_range(128, 8, r)
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, comm=comm, fused=True, overlap=overlap,
+                                    exchange=exchange)
+        return {k: v.cpu().numpy() for k, v in st.items()}, rep
+
+    res = run_ranks(8, rank_fn)
+    for _, rep in res:
+        assert rep.meta["pipeline"] == "slab-fused" and rep.iterations == rref.iterations == 6
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        full = np.concatenate([st[k] for st, _ in res], axis=0 if k == "q" else 1)
+        assert rel_l2(full, getattr(ref, k).cpu().numpy()) <= 1e-10, k
