@@ -1,4 +1,4 @@
-// Fused Stokes ADMM pipeline for cubic power-of-two grids (N = 64, 128, 256).
+// Fused Stokes ADMM pipeline for cubic power-of-two grids (N = 64 ... 1024).
 //
 // Every 3D transform of the loop is split along its axes and fused with the
 // pointwise / spectral work that consumes it, so each iteration streams the
@@ -22,7 +22,12 @@
 // Spectra are stored as [rows][N/2] complex plus a separate Nyquist column
 // [rows] so rows stay 2 KiB aligned.  All FFTs are hand-written radix-8/16
 // Stockham-style passes in registers with one padded shared-memory transpose
-// (fft_seq); a thread group of 8 or 16 lanes transforms one sequence.
+// (fft_seq); a thread group of 8 or 16 lanes transforms one sequence.  N = 512 /
+// 1024 sequences are 2 / 4 such 256-point blocks plus a radix-2 / radix-4 stage
+// across them (pf_fft.cuh radix_stage, fft_units; spectra in block-interleaved
+// order in shared memory only).  Slab mode (SL) runs the same passes on one
+// rank's x- / y-slab, with the transpose either by all_to_all between the passes
+// or fused into PK's / MF's stores to the owning ranks' buffers (Bufs::peers).
 #include <cmath>
 #include <cstring>
 

@@ -1,5 +1,5 @@
 // Fused comparison-medium transport pipeline for cubic power-of-two grids
-// (N = 64, 128, 256) — reference pkg/src/poreflow/transport.py:225-258 and
+// (N = 64 ... 512; long sequences as in pf_fused.cu) — reference pkg/src/poreflow/transport.py:225-258 and
 // backends/pure.py:71-115.
 //
 // One iteration streams 25 words + 1 byte per voxel through HBM (the
