@@ -150,6 +150,15 @@ int pf_slab_finalize(pf_plan* plan, const double* totals9);
 int pf_slab_form_r(pf_plan* plan, double* R, int gated);
 int pf_slab_scale(pf_plan* plan, const double* src, double* dst, int64_t count, double scale);
 int pf_slab_read(pf_plan* plan, pf_stokes_result* result);
+/* Permeability of a slab-decomposed cell (replaces poreflow.effective.permeability,
+ * src/effective.py:43-72, for fields no rank holds whole): the spectral gradient
+ * i kappa_axis F / n of one T-layout spectrum (pf_slab_forward /
+ * pf_slab_forward_finish of a velocity component), and this rank's six masked
+ * Gram sums sum_pore sum_m G[i][m] G[j][m] (i <= j) of one velocity component
+ * over its x-slab, G = 9 contiguous real slab fields [flow i][axis m]; the caller
+ * all-reduces the sums and scales by h^3. */
+int pf_slab_grad(pf_plan* plan, const double* t_spec, int axis, double* t_out);
+int pf_slab_gram(pf_plan* plan, const uint8_t* solid, const double* G, double* sums6);
 
 /* Fused slab pipeline (cubic N in {64, 128, 256, 512, 1024}, P a power of two, slabs of
  * whole tiles; pf_slab_fused_sizes reports 0 when unsupported).  Per iteration:

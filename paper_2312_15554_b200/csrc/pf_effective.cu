@@ -207,6 +207,20 @@ static int diffusivity_t(pf_plan* p, const uint8_t* solid, const double* const* 
   return PF_OK;
 }
 
+// Masked Gram partials of one velocity component over a (slab-local) set of 9
+// gradient fields G[flow][axis][x] (3D): the 6 pair sums before the h^3 factor.
+int slab_gram_host(pf_plan* p, const uint8_t* solid, const double* G, int64_t n, double* out6) {
+  const int nb = blocks_for(n);
+  k_gram<3><<<nb, kThreads, 0, p->work>>>(n, G, solid, p->partials);
+  PF_CK_CUDA(cudaGetLastError());
+  double* out = p->partials + 24 * kMaxBlocks;
+  k_reduce_rows_e<<<1, kFinalizeThreads, 0, p->work>>>(p->partials, 6, nb, out);
+  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->work));
+  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  for (int k = 0; k < 6; ++k) out6[k] = p->h_small[k];
+  return PF_OK;
+}
+
 }  // namespace pf
 
 using namespace pf;

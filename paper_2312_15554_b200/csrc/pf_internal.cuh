@@ -207,6 +207,7 @@ int fused_slab_pk(pf_plan* p);
 int fused_slab_rs(pf_plan* p, double* totals);
 int fused_slab_mf(pf_plan* p);
 int fused_slab_rs_part(pf_plan* p, int comp);
+int slab_gram_host(pf_plan* p, const uint8_t* solid, const double* G, int64_t n, double* out6);
 int fused_slab_totals(pf_plan* p, double* totals);
 int fused_slab_mf_part(pf_plan* p, int comp, int fix);
 int fused_slab_set_peers(pf_plan* p, const uint64_t* yy, const uint64_t* yyn, const uint64_t* yx,

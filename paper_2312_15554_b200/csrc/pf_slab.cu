@@ -100,6 +100,18 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_slab_totals(const double* 
   }
 }
 
+// G = i kappa_axis F / n on a T-layout spectrum (global mode indices; spectral.py:118-124)
+__global__ void k_slab_grad(Geom gs, const double* __restrict__ kap, int axis, const double2* __restrict__ F,
+                            double2* __restrict__ G, double inv_n) {
+  const int64_t n2h = gs.n2h, n1 = gs.n[1];
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < gs.nh; m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = m / n2h;
+    const int64_t idx = axis == 0 ? t / n1 : (axis == 1 ? gs.k1off + t % n1 : m - t * n2h);
+    const double2 f = make_double2(F[m].x * inv_n, F[m].y * inv_n);
+    G[m] = cik(__ldg(kap + idx), f);
+  }
+}
+
 static int slab_ensure_work(pf_plan* p, SlabPlan* s, size_t need) {
   if (need <= s->work_bytes) return PF_OK;
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
@@ -369,6 +381,30 @@ int pf_slab_read(pf_plan* p, pf_stokes_result* res) {
   return PF_OK;
 }
 
+
+// Distributed permeability pieces (slab.slab_permeability): the spectral
+// gradient of one T-layout component, and this rank's 6 masked Gram sums of one
+// velocity component over its x-slab (G = 9 real slab fields [flow][axis]).
+int pf_slab_grad(pf_plan* p, const double* Tspec, int axis, double* Tout) {
+  SlabPlan* s;
+  PF_CK(slab_checked(p, &s));
+  PF_ARG(Tspec && Tout && axis >= 0 && axis < 3, "bad argument");
+  PF_CK(enter(p));
+  const double inv_n = 1.0 / ((double)s->N0 * s->N1 * s->N2);
+  k_slab_grad<<<blocks_for(s->gs.nh), kThreads, 0, p->work>>>(s->gs, p->kap[axis], axis, (const double2*)Tspec,
+                                                               (double2*)Tout, inv_n);
+  PF_CK_CUDA(cudaGetLastError());
+  return leave(p);
+}
+
+int pf_slab_gram(pf_plan* p, const uint8_t* solid, const double* G, double* sums6) {
+  SlabPlan* s;
+  PF_CK(slab_checked(p, &s));
+  PF_ARG(solid && G && sums6, "null argument");
+  PF_CK(enter(p));
+  PF_CK(slab_gram_host(p, solid, G, (int64_t)s->L0 * s->N1 * s->N2, sums6));
+  return leave(p);
+}
 
 int pf_slab_fused_sizes(pf_plan* p, int64_t* y_main, int64_t* y_nyq) {
   SlabPlan* s;

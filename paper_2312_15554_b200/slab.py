@@ -22,6 +22,7 @@ import numpy as np
 from . import _native as N
 from .device import require_cuda, torch
 from .report import ConvergenceReport
+from .spectral import CENTRAL as CENTRAL_MODE
 from .stokes import REPORT_COLUMNS, PenaltyParams, StokesConfig, _params
 
 
@@ -107,6 +108,14 @@ class DeviceSlabBackend:
 
     def scale(self, src, dst, count, s):
         N.check(self.lib.pf_slab_scale(self.h, self._p(src), self._p(dst), int(count), float(s)))
+
+    def grad(self, tspec, axis, out):
+        N.check(self.lib.pf_slab_grad(self.h, self._p(tspec), int(axis), self._p(out)))
+
+    def gram(self, solid, G) -> np.ndarray:
+        out = (ctypes.c_double * 6)()
+        N.check(self.lib.pf_slab_gram(self.h, self._p(solid), self._p(G), out))
+        return np.asarray(out[:])
 
     # fused slab pipeline (pf_slab_fused_*)
     def fused_sizes(self) -> tuple:
@@ -483,6 +492,89 @@ class SymmetricMemoryExchange:
 
     def p2p_barrier(self):
         next(iter(self.handles.values())).barrier(channel=0)
+
+
+def slab_permeability(u_locals, solid_local, dims, symbol_mode: str = CENTRAL_MODE, group=None, device=None,
+                      comm=None) -> np.ndarray:
+    """K_ij = h^3 sum_pore sum_{c,m} d_m u^i_c d_m u^j_c (effective.py:43-72) of a
+    slab-decomposed cell: ``u_locals`` = this rank's x-slabs (3, N0/P, N1, N2) of
+    the three unit-flow solutions (e.g. from ``solve_stokes_slab``).  Each
+    component goes through the distributed forward transform, its three spectral
+    gradients back through the distributed inverse, the rank sums its masked Gram
+    over its slab and the sums are all-reduced — no rank ever holds a whole field.
+    Returns the same 3 x 3 tensor on every rank."""
+    import torch.distributed as dist
+
+    t = torch()
+    if comm is not None:
+        world, rank, d = comm.get_world_size(group), comm.get_rank(group), comm
+    else:
+        d = dist if dist.is_available() and dist.is_initialized() else None
+        world = d.get_world_size(group) if d else 1
+        rank = d.get_rank(group) if world > 1 else 0
+    dims = tuple(int(x) for x in dims)
+    if len(dims) != 3 or len(u_locals) != 3:
+        raise ValueError("slab permeability needs three 3D unit-flow solutions")
+    lo, hi = slab_range(dims[0], world, rank)
+    be = DeviceSlabBackend(dims, world, rank, symbol_mode, device)
+    be.bind()
+    dev = be.dev
+    L = (hi - lo) * dims[1] * dims[2]
+    us = [t.as_tensor(np.asarray(u) if not hasattr(u, "data_ptr") else u).to(dev, t.float64).reshape(-1)
+          for u in u_locals]
+    for u in us:
+        if u.numel() != 3 * L:
+            raise ValueError("u_locals must be this rank's x-slab of each (3, N0, N1, N2) solution")
+    solid = t.as_tensor(np.array(solid_local, dtype=np.uint8, copy=True)).reshape(-1).to(dev)
+    tr = _SlabTransforms(be, world, d, group)
+    spec = be.alloc_complex(be.tspec)
+    grad = be.alloc_complex(be.tspec)
+    G = be.alloc_real(9 * L)
+    sums = np.zeros(6)
+    for c in range(3):
+        for i in range(3):
+            tr.to_spectrum(us[i][c * L:(c + 1) * L], 1, spec)
+            for m in range(3):
+                be.grad(spec, m, grad)
+                tr.to_real(grad, 1, G[(3 * i + m) * L:(3 * i + m + 1) * L])
+        sums += be.gram(solid, G)
+    tot = t.as_tensor(sums, dtype=t.float64, device=dev)
+    if world > 1:
+        d.all_reduce(tot, group=group)
+    s6 = tot.cpu().numpy()
+    be.close()
+    cell = 1.0 / float(np.prod(dims))
+    K = np.empty((3, 3))
+    k = 0
+    for i in range(3):
+        for j in range(i, 3):
+            K[i, j] = K[j, i] = s6[k] * cell
+            k += 1
+    return K
+
+
+class _SlabTransforms:
+    """Distributed 3D transforms of single components on a slab backend (forward:
+    x-slab real -> T-layout spectrum; inverse: back), blocking exchanges."""
+
+    def __init__(self, backend, world, dist, group):
+        self.b, self.world, self.dist, self.group = backend, world, dist, group
+        self.send = backend.alloc_complex(backend.exch)
+        self.recv = backend.alloc_complex(backend.exch) if world > 1 else self.send
+
+    def _exchange(self):
+        if self.world > 1:
+            self.dist.all_to_all_single(self.recv, self.send, group=self.group)
+
+    def to_spectrum(self, real, ncomp, tspec):
+        self.b.forward(real, ncomp, self.send)
+        self._exchange()
+        self.b.forward_finish(self.recv, ncomp, tspec)
+
+    def to_real(self, tspec, ncomp, real):
+        self.b.inverse(tspec, ncomp, self.send)
+        self._exchange()
+        self.b.inverse_finish(self.recv, ncomp, real)
 
 
 def solve_stokes_slab(solid_local, dims, cfg: StokesConfig | None = None, penalties: PenaltyParams | None = None,
