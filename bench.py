@@ -426,7 +426,10 @@ def run_pipeline_workload(args):
     from oracle import poreflow_oracle as O
 
     n = args.n
-    ind = pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25)
+    if args.geometry == "packing":  # cfg 3 / 4 geometry (SURVEY §8d generator, seed 0)
+        ind = pf.random_packing_geometry(n, seed=0)
+    else:
+        ind = pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25)
     scfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(1.0, 0.0, 0.0))
     tcfg = pf.TransportConfig(pe=10.0, a0=0.55, eps=1e-5, composition_gradient=(1.0, 0.0, 0.0))
     host = np.array(ind.values)
@@ -436,33 +439,53 @@ def run_pipeline_workload(args):
                                             max_iter=3))  # warm-up (plans)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = pf.effective_tensors(pf.IndicatorField(pf.UnitCellGrid((n, n, n)), host), scfg, tcfg)
-    K, D = np.asarray(res.tensors.permeability), np.asarray(res.tensors.diffusivity)
-    torch.cuda.synchronize()
-    gpu_s = time.perf_counter() - t0
-    s_its = [r.iterations for r in res.flow_reports]
-    t_its = [r.iterations for r in res.transport_reports]
+    if args.stokes_only:  # cfg 3: the three load cases and K* only
+        cell = pf.IndicatorField(pf.UnitCellGrid((n, n, n)), host)
+        from paper_2312_15554_b200.batch import solve_stokes_many_device
+
+        flows = solve_stokes_many_device([cell] * 3, [pf.StokesConfig.with_tolerance(
+            1e-5, pressure_gradient=tuple(float(i == a) for i in range(3))) for a in range(3)])
+        K = pf.permeability([st.u for st, _ in flows], cell, "central")
+        D = np.full((3, 3), np.nan)
+        torch.cuda.synchronize()
+        gpu_s = time.perf_counter() - t0
+        s_its, t_its = [r.iterations for _, r in flows], []
+        conv = all(r.converged for _, r in flows)
+        u_flow = flows[0][0].u
+    else:
+        res = pf.effective_tensors(pf.IndicatorField(pf.UnitCellGrid((n, n, n)), host), scfg, tcfg)
+        K, D = np.asarray(res.tensors.permeability), np.asarray(res.tensors.diffusivity)
+        torch.cuda.synchronize()
+        gpu_s = time.perf_counter() - t0
+        s_its = [r.iterations for r in res.flow_reports]
+        t_its = [r.iterations for r in res.transport_reports]
+        conv = bool(res.converged)
+        u_flow = res.u_phys
     vox_it = n ** 3 * (sum(s_its) + sum(t_its))
     # CPU: oracle rates on a bounded sample (loop time only), extrapolated
     tm = {}
     k_s = 2
     O.solve_stokes(ind.values, (1.0, 0.0, 0.0), 1e-5, 1e-5, max_iter=k_s, timer=tm)
     stokes_rate = n ** 3 * k_s / tm["loop_s"]
-    u1 = res.u_phys.cpu().numpy()
-    k_t = 2
-    t1 = time.perf_counter()
-    O.solve_transport(ind.values, u1, (1.0, 0.0, 0.0), pe=10.0, a0=0.55, eps=1e-5, max_iter=k_t)
-    transport_rate = n ** 3 * k_t / (time.perf_counter() - t1)
-    cpu_s = n ** 3 * sum(s_its) / stokes_rate + n ** 3 * sum(t_its) / transport_rate
-    print(json.dumps({"metric": f"cfg-2 cell-to-tensors run (cli.run flow) at {n}^3, wall clock (secondary)",
+    transport_rate = None
+    cpu_s = n ** 3 * sum(s_its) / stokes_rate
+    if t_its:
+        u1 = u_flow.cpu().numpy()
+        k_t = 2
+        t1 = time.perf_counter()
+        O.solve_transport(ind.values, u1, (1.0, 0.0, 0.0), pe=10.0, a0=0.55, eps=1e-5, max_iter=k_t)
+        transport_rate = n ** 3 * k_t / (time.perf_counter() - t1)
+        cpu_s += n ** 3 * sum(t_its) / transport_rate
+    what = "cfg-3 three load cases + K*" if args.stokes_only else "cfg-2 cell-to-tensors run (cli.run flow)"
+    print(json.dumps({"metric": f"{what} at {n}^3 ({args.geometry}), wall clock (secondary)",
                       "value": gpu_s, "unit": "s", "higher_is_better": False, "dtype": "f64",
                       "voxel_iters_per_s": vox_it / gpu_s, "stokes_iterations": s_its,
-                      "transport_iterations": t_its, "converged": bool(res.converged),
-                      "K": K.tolist(), "D": D.tolist(),
-                      "config": {"workload": f"pipeline_sphere_{n}^3", "stokes": "eps 1e-5, adaptive penalties",
-                                 "transport": "Pe 10, a0 0.55, eps 1e-5"},
+                      "transport_iterations": t_its, "converged": conv,
+                      "K": K.tolist(), "D": None if args.stokes_only else D.tolist(),
+                      "config": {"workload": f"pipeline_{args.geometry}_{n}^3", "stokes": "eps 1e-5, adaptive penalties",
+                                 "transport": None if args.stokes_only else "Pe 10, a0 0.55, eps 1e-5"},
                       "cpu_extrapolated": {"seconds": cpu_s, "kind": "port", "cores": os.cpu_count(),
-                                           "sample": f"{k_s} Stokes + {k_t} transport iterations of the same cell "
+                                           "sample": f"{k_s} Stokes (+ 2 transport) iterations of the same cell "
                                                      f"(numpy + scipy.fft), rate x GPU iteration counts",
                                            "stokes_rate": stokes_rate, "transport_rate": transport_rate},
                       "speedup_vs_cpu_extrapolated": cpu_s / gpu_s}), flush=True)
@@ -631,6 +654,9 @@ def main():
     ap.add_argument("--slab-cufft", action="store_true", help="--workload slab: the cuFFT slab pipeline")
     ap.add_argument("--exchange", default="a2a", choices=("a2a", "p2p"),
                     help="--workload slab: all_to_all exchange or the transpose fused into the passes over P2P")
+    ap.add_argument("--geometry", default="spheres", choices=("spheres", "packing"),
+                    help="--workload pipeline: cfg 1/2 sphere array or the cfg 3/4 random packing")
+    ap.add_argument("--stokes-only", action="store_true", help="--workload pipeline: cfg 3 (load cases + K* only)")
     ap.add_argument("--tcells", type=int, default=1,
                     help="--workload transport: concurrent solves (cfg 2's load cases e_1..e_3), own plan + stream each")
     args = ap.parse_args()

@@ -250,6 +250,7 @@ int pf_pore_average(pf_plan* p, const uint8_t* solid, const double* f, int ncomp
 }
 
 int pf_permeability(pf_plan* p, const uint8_t* solid, const double* const* us, double* K) {
+  PF_NVTX("pf_permeability");
   PF_ARG(p && solid && us && K, "null argument");
   for (int i = 0; i < p->g.d; ++i) PF_ARG(us[i], "null velocity solution %d", i);
   if (p->active) {
@@ -268,6 +269,7 @@ int pf_permeability(pf_plan* p, const uint8_t* solid, const double* const* us, d
 
 int pf_diffusivity(pf_plan* p, const uint8_t* solid, const double* const* us, const double* const* chi,
                    const double* const* gchi, double pe, double* D) {
+  PF_NVTX("pf_diffusivity");
   PF_ARG(p && solid && us && chi && gchi && D, "null argument");
   if (p->active) {
     set_error("pf_diffusivity while a solve is active on this plan");

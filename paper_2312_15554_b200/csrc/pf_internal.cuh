@@ -1,5 +1,6 @@
 // Internal declarations shared by the poreflow_b200 translation units.
 #pragma once
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <utility>
@@ -15,6 +16,17 @@
 #include "../../include/poreflow_b200.h"
 
 namespace pf {
+
+// NVTX range over a C-ABI entry point (stage ranges for nsys / ncu
+// --nvtx filtering); header-only NVTX3, a no-op without an attached tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PF_NVTX(name) ::pf::NvtxRange pf_nvtx_range_(name)
+
 
 // ---------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);

@@ -214,6 +214,7 @@ int pf_slab_sizes(pf_plan* p, int64_t* exchange_per_comp, int64_t* tspec_per_com
 }
 
 int pf_slab_forward(pf_plan* p, const double* real, int ncomp, double* send) {
+  PF_NVTX("pf_slab_forward");
   SlabPlan* s;
   PF_CK(slab_checked(p, &s));
   PF_ARG(ncomp >= 1 && ncomp <= 3, "ncomp 1..3");
@@ -242,6 +243,7 @@ int pf_slab_forward_finish(pf_plan* p, const double* recv, int ncomp, double* ts
 }
 
 int pf_slab_inverse(pf_plan* p, double* tspec, int ncomp, double* send) {
+  PF_NVTX("pf_slab_inverse");
   SlabPlan* s;
   PF_CK(slab_checked(p, &s));
   PF_ARG(ncomp >= 1 && ncomp <= 3, "ncomp 1..3");
@@ -439,6 +441,7 @@ static int fslab_checked(pf_plan* p, SlabPlan** s) {
 }
 
 int pf_slab_fused_setup(pf_plan* p, const double* Tq, const double* Td, double* R) {
+  PF_NVTX("pf_slab_fused_setup");
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));
   PF_ARG(Tq && Td && R, "null argument");
@@ -448,6 +451,7 @@ int pf_slab_fused_setup(pf_plan* p, const double* Tq, const double* Td, double* 
 }
 
 int pf_slab_fused_pk(pf_plan* p) {
+  PF_NVTX("pf_slab_fused_pk");
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));
   PF_CK(enter(p));
@@ -456,6 +460,7 @@ int pf_slab_fused_pk(pf_plan* p) {
 }
 
 int pf_slab_fused_rs(pf_plan* p, double* totals) {
+  PF_NVTX("pf_slab_fused_rs");
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));
   PF_ARG(totals, "null argument");
@@ -465,6 +470,7 @@ int pf_slab_fused_rs(pf_plan* p, double* totals) {
 }
 
 int pf_slab_fused_mf(pf_plan* p) {
+  PF_NVTX("pf_slab_fused_mf");
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));
   PF_CK(enter(p));
@@ -477,6 +483,7 @@ int pf_slab_fused_mf(pf_plan* p) {
 // once all three ran; MF of one component (fix = 1 on the first one of an
 // iteration runs the gated RSF pass of every component first).
 int pf_slab_fused_rs_part(pf_plan* p, int comp) {
+  PF_NVTX("pf_slab_fused_rs_part");
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));
   PF_ARG(comp >= 0 && comp < 3, "comp 0..2");
@@ -495,6 +502,7 @@ int pf_slab_fused_totals(pf_plan* p, double* totals) {
 }
 
 int pf_slab_fused_mf_part(pf_plan* p, int comp, int fix) {
+  PF_NVTX("pf_slab_fused_mf_part");
   SlabPlan* s;
   PF_CK(fslab_checked(p, &s));
   PF_ARG(comp >= 0 && comp < 3, "comp 0..2");

@@ -426,6 +426,7 @@ extern "C" {
 
 int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
                     double* a, double* lam, double* history) {
+  PF_NVTX("pf_stokes_begin");
   PF_ARG(p && P && solid && u && ut && q && a && lam && history, "null argument");
   PF_ARG(P->b > 0.0, "coupling penalty b must be positive for the zero mode");
   PF_ARG(P->nu > 0.0, "viscosity must be positive");
@@ -475,6 +476,7 @@ int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid,
 }
 
 int pf_stokes_iterate(pf_plan* p, int64_t n_iter, int poll, pf_stokes_result* res) {
+  PF_NVTX("pf_stokes_iterate");
   PF_ARG(p, "null plan");
   if (p->active != 1) {
     set_error("pf_stokes_iterate without pf_stokes_begin");
@@ -496,6 +498,7 @@ int pf_stokes_iterate(pf_plan* p, int64_t n_iter, int poll, pf_stokes_result* re
 }
 
 int pf_stokes_end(pf_plan* p, pf_stokes_result* res) {
+  PF_NVTX("pf_stokes_end");
   PF_ARG(p, "null plan");
   if (p->active != 1) {
     set_error("pf_stokes_end without pf_stokes_begin");
@@ -564,6 +567,7 @@ int pf_stokes_pipeline(const pf_plan* p) {
 
 int pf_stokes_solve(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
                     double* a, double* lam, double* history, pf_stokes_result* res) {
+  PF_NVTX("pf_stokes_solve");
   PF_CK(pf_stokes_begin(p, P, solid, u, ut, q, a, lam, history));
   pf_stokes_result r{};
   PF_CK(pf_stokes_iterate(p, P->max_iter, 1, &r));

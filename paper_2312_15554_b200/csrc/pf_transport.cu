@@ -303,6 +303,7 @@ extern "C" {
 
 int pf_transport_begin(pf_plan* p, const pf_transport_params* P, const uint8_t* solid, const double* u, double* chi,
                        double* grad, double* history, pf_transport_result* res) {
+  PF_NVTX("pf_transport_begin");
   PF_ARG(p && P && solid && u && chi && grad && history, "null argument");
   PF_ARG(P->pe >= 0.0, "Peclet number must be nonnegative");
   PF_ARG(P->eta > 0.0 && P->eta <= 1.0, "fictitious diffusivity eta must lie in (0, 1]");
@@ -373,6 +374,7 @@ static void fill_tres(pf_plan* p, const Ctrl& c, pf_transport_result* res) {
 }
 
 int pf_transport_iterate(pf_plan* p, int64_t n_iter, int poll, pf_transport_result* res) {
+  PF_NVTX("pf_transport_iterate");
   PF_ARG(p, "null plan");
   if (p->active != 2) {
     set_error("pf_transport_iterate without pf_transport_begin");
@@ -387,6 +389,7 @@ int pf_transport_iterate(pf_plan* p, int64_t n_iter, int poll, pf_transport_resu
 }
 
 int pf_transport_end(pf_plan* p, pf_transport_result* res) {
+  PF_NVTX("pf_transport_end");
   PF_ARG(p, "null plan");
   if (p->active != 2) {
     set_error("pf_transport_end without pf_transport_begin");
@@ -432,6 +435,7 @@ int pf_transport_profile(pf_plan* p, int64_t n_iter, double* stage_ms) {
 
 int pf_transport_solve(pf_plan* p, const pf_transport_params* P, const uint8_t* solid, const double* u, double* chi,
                        double* grad, double* history, pf_transport_result* res) {
+  PF_NVTX("pf_transport_solve");
   PF_CK(pf_transport_begin(p, P, solid, u, chi, grad, history, res));
   pf_transport_result r{};
   PF_CK(pf_transport_iterate(p, P->max_iter, 1, &r));
