@@ -176,6 +176,14 @@ int pf_slab_gram(pf_plan* plan, const uint8_t* solid, const double* G, double* s
 int pf_slab_fused_sizes(pf_plan* plan, int64_t* y_main, int64_t* y_nyq);
 int pf_slab_fused_bind(pf_plan* plan, double* Yy, double* Yy_nyq, double* Yx, double* Yx_nyq);
 int pf_slab_fused_setup(pf_plan* plan, const double* Q_tspec, const double* D_tspec, double* R_scratch);
+/* Cold-start setup (the caller's u, u~, q, a, lam are all zero): Q^ = D^ = 0 and
+ * Y = 0 with no transform, exchange or scratch — in place of pf_slab_setup +
+ * pf_slab_fused_setup and the first Y exchange. */
+int pf_slab_fused_setup_zero(pf_plan* plan);
+/* Release the slab transforms' cuFFT plans, work area and scratch (re-created
+ * on the next pf_slab_forward / pf_slab_inverse): the fused slab needs them only
+ * at setup and teardown. */
+int pf_slab_release_transforms(pf_plan* plan);
 int pf_slab_fused_pk(pf_plan* plan);
 int pf_slab_fused_rs(pf_plan* plan, double* totals9);
 int pf_slab_fused_mf(pf_plan* plan);

@@ -119,6 +119,8 @@ SIGNATURES = {
     "pf_slab_fused_set_peers": [_P, _P, _P, _P, _P, ctypes.c_int],
     "pf_unpack_bits": [_P, _P, ctypes.c_int64, _P],
     "pf_slab_grad": [_P, _P, ctypes.c_int, _P],
+    "pf_slab_fused_setup_zero": [_P],
+    "pf_slab_release_transforms": [_P],
     "pf_slab_gram": [_P, _P, _P, _P],
     "pf_transport_solve": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],
     "pf_transport_begin": [_P, ctypes.POINTER(TransportParams), _P, _P, _P, _P, _P, ctypes.POINTER(TransportResult)],

@@ -128,8 +128,9 @@ struct Bufs {
   // plane window of one launch of the x-slab passes (SL kernels): planes
   // [i0a, i0a + nl) of the l0; RS partial rows at [q * pst + poff + block]
   int i0a, nl, pst, poff;
-  // the host encoded the TMA tensor maps of this layout (else the passes stage with LDGSTS)
-  int tma;
+  // the host encoded the TMA tensor maps of this layout (else the passes stage with
+  // LDGSTS); tma_yx: the 5D x-slab map of MI too (its box spans l1 <= 256 rows)
+  int tma, tma_yx;
   // peer-memory exchange (slab, P2P-mapped Y buffers of every rank; null = exchange by
   // all_to_all): PK stores straight into the x-slab owners' Yx, MF into the y-slab
   // owners' Yy, so the transpose rides on the passes' own stores over NVLink
@@ -883,7 +884,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
                : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
   constexpr bool TMA = K::TMA_OK && PF_M_TMA;
-  if (TMA && !nyq && B.tma) {
+  if (TMA && !nyq && B.tma && (!(SL && INV) || B.tma_yx)) {
     // one 2D bulk tensor copy of the (N rows x CM columns) tile, 128B-swizzled
     // (long sequences: M copies of 256 rows, 64B-swizzled)
     __shared__ uint64_t mbar;
@@ -1572,7 +1573,7 @@ int fused_ensure(pf_plan* p) {
     PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
     PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, cp, 3));
-    f->b.tma = 1;
+    f->b.tma = f->b.tma_yx = 1;
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
   // right-hand side at setup time.
@@ -1932,25 +1933,19 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
     default: fz::pass1_twiddles<1024>(tw.data()); break;
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
-  // axes-(1, 2) transform of this slab's R at setup
-  size_t ws = 0;
-  long long dims2[2] = {N, N};
-  PF_CK_FFT(cufftCreate(&f->plan2d));
-  PF_CK_FFT(cufftSetAutoAllocation(f->plan2d, 0));
-  PF_CK_FFT(cufftMakePlanMany64(f->plan2d, 2, dims2, nullptr, 1, (long long)N * N, nullptr, 1,
-                                (long long)N * (H + 1), CUFFT_D2Z, 3LL * l0, &ws));
-  PF_CK_CUDA(cudaMalloc(&f->ws, ws > 0 ? ws : 256));
-  PF_CK_CUDA(cudaMalloc(&f->spec, sizeof(double2) * 3 * (size_t)l0 * N * (H + 1)));
-  PF_CK_FFT(cufftSetWorkArea(f->plan2d, f->ws));
-  PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
-  f->b.tma = 0;
-  if (N >= 128 && l1 <= 256 && N / l1 <= 256) {  // TMA maps of this slab's layouts (box dims <= 256)
+  // (the axes-(1, 2) transform of a warm start's R is planned in fused_slab_setup
+  // and released after it: no setup-only memory stays resident)
+  f->b.tma = f->b.tma_yx = 0;
+  if (N >= 128) {  // TMA maps of this slab's layouts (every box dimension <= 256)
     const int cm = N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : (N == 512 ? fz::M2<512>::CM : fz::M2<1024>::CM));
     const int cp = N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : (N == 512 ? fz::PK2<512>::CP : fz::PK2<1024>::CP));
-    PF_CK(encode_yx_map(&f->tm_y, Yx, N, cm, l0, l1));
     PF_CK(encode_axis1_rows(&f->tm_xr, f->b.XR, N, cm, 3 * (int64_t)l0 * N));
     PF_CK(encode_pk_map_l1(&f->tm_pk, Yy, N, cp, l1));
     f->b.tma = 1;
+    if (l1 <= 256 && N / l1 <= 256) {  // MI's 5D box spans (l1, P) rows
+      PF_CK(encode_yx_map(&f->tm_y, Yx, N, cm, l0, l1));
+      f->b.tma_yx = 1;
+    }
   }
   switch (N) {
     case 64: PF_CK(set_attrs<64>(f)); break;
@@ -1959,7 +1954,7 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
     case 512: PF_CK(set_attrs<512>(f)); break;
     default: PF_CK(set_attrs<1024>(f)); break;
   }
-  p->scratch_bytes += f->bytes + ws + sizeof(double2) * 3 * (size_t)l0 * N * (H + 1);
+  p->scratch_bytes += f->bytes;
   return PF_OK;
 }
 
@@ -1968,9 +1963,22 @@ int fused_slab_bind(pf_plan* p, int N, int l0, int l1, int k1off, double2* Yy, d
 int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R) {
   FusedPlan* f = fp_of(p);
   const int N = f->N;
+  const int64_t H = N / 2, l0 = f->b.l0;
   PF_CK(to_tilemajor(N, Tq, f->b.Q, 1.0, true, p->work, f->b.l1));
   PF_CK(to_tilemajor(N, Td, f->b.D, 1.0, true, p->work, f->b.l1));
   PF_CK(stokes_form_r_gated(p, R, 0));
+  if (!f->plan2d) {  // axes-(1, 2) transform of this slab's R (setup only)
+    size_t ws = 0;
+    long long dims2[2] = {N, N};
+    PF_CK_FFT(cufftCreate(&f->plan2d));
+    PF_CK_FFT(cufftSetAutoAllocation(f->plan2d, 0));
+    PF_CK_FFT(cufftMakePlanMany64(f->plan2d, 2, dims2, nullptr, 1, (long long)N * N, nullptr, 1,
+                                  (long long)N * (H + 1), CUFFT_D2Z, 3LL * l0, &ws));
+    PF_CK_CUDA(cudaMalloc(&f->ws, ws > 0 ? ws : 256));
+    PF_CK_CUDA(cudaMalloc(&f->spec, sizeof(double2) * 3 * (size_t)l0 * N * (H + 1)));
+    PF_CK_FFT(cufftSetWorkArea(f->plan2d, f->ws));
+    PF_CK_FFT(cufftSetStream(f->plan2d, p->work));
+  }
   PF_CK_FFT(cufftExecD2Z(f->plan2d, (cufftDoubleReal*)R, (cufftDoubleComplex*)f->spec));
   const int grid = blocks_for((int64_t)3 * f->b.l0 * N * (N / 2 + 1));
   switch (N) {
@@ -1989,6 +1997,40 @@ int fused_slab_setup(pf_plan* p, const double2* Tq, const double2* Td, double* R
     default: PF_CK(compact_setup_t<1024>(p, f)); break;
   }
   f->lam_pore = p->sc.lam_pore_sq;  // local: enters the totals before the all-reduce
+  p->sc.lam_pore_sq = 0.0;
+  // release the setup-only transform (a 1024^3 slab of 2 ranks needs the memory)
+  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  cufftDestroy(f->plan2d);
+  f->plan2d = 0;
+  PF_CK_CUDA(cudaFree(f->ws));
+  PF_CK_CUDA(cudaFree(f->spec));
+  f->ws = nullptr;
+  f->spec = nullptr;
+  return PF_OK;
+}
+
+// Cold start (the whole state zero, as the reference's default): Q^ = D^ = 0 and
+// the Y-space right-hand side is FFT(b 0 - 0) = 0, so setup needs no transform,
+// exchange or scratch at all — only the compact layout.
+int fused_slab_setup_zero(pf_plan* p, int64_t y_main, int64_t y_nyq) {
+  FusedPlan* f = fp_of(p);
+  double2 *Yy = f->b.Y, *Yyn = f->b.Yn, *Yx = f->b.Yx, *Yxn = f->b.Yxn;
+  const int N = f->N;
+  const size_t qd = (size_t)f->b.l1 * N * (N / 2) + (size_t)f->b.l1 * N;
+  PF_CK_CUDA(cudaMemsetAsync(f->b.Q, 0, sizeof(double2) * qd, p->work));
+  PF_CK_CUDA(cudaMemsetAsync(f->b.D, 0, sizeof(double2) * qd, p->work));
+  PF_CK_CUDA(cudaMemsetAsync(Yy, 0, sizeof(double2) * y_main, p->work));
+  PF_CK_CUDA(cudaMemsetAsync(Yyn, 0, sizeof(double2) * y_nyq, p->work));
+  if (Yx != Yy) PF_CK_CUDA(cudaMemsetAsync(Yx, 0, sizeof(double2) * y_main, p->work));
+  if (Yxn != Yyn) PF_CK_CUDA(cudaMemsetAsync(Yxn, 0, sizeof(double2) * y_nyq, p->work));
+  switch (N) {
+    case 64: PF_CK(compact_setup_t<64>(p, f)); break;
+    case 128: PF_CK(compact_setup_t<128>(p, f)); break;
+    case 256: PF_CK(compact_setup_t<256>(p, f)); break;
+    case 512: PF_CK(compact_setup_t<512>(p, f)); break;
+    default: PF_CK(compact_setup_t<1024>(p, f)); break;
+  }
+  f->lam_pore = p->sc.lam_pore_sq;
   p->sc.lam_pore_sq = 0.0;
   return PF_OK;
 }

@@ -219,6 +219,7 @@ int fused_slab_pk(pf_plan* p);
 int fused_slab_rs(pf_plan* p, double* totals);
 int fused_slab_mf(pf_plan* p);
 int fused_slab_rs_part(pf_plan* p, int comp);
+int fused_slab_setup_zero(pf_plan* p, int64_t y_main, int64_t y_nyq);
 int slab_gram_host(pf_plan* p, const uint8_t* solid, const double* G, int64_t n, double* out6);
 int fused_slab_totals(pf_plan* p, double* totals);
 int fused_slab_mf_part(pf_plan* p, int comp, int fix);

@@ -33,16 +33,12 @@ struct SlabPlan {
 
 static SlabPlan* sp_of(pf_plan* p) { return reinterpret_cast<SlabPlan*>(p->slab); }
 
+static void slab_release(pf_plan* p, SlabPlan* s);
+
 void slab_free(pf_plan* p) {
   SlabPlan* s = sp_of(p);
   if (!s) return;
-  for (int k = 1; k <= 3; ++k) {
-    if (s->f2d[k]) cufftDestroy(s->f2d[k]);
-    if (s->i2d[k]) cufftDestroy(s->i2d[k]);
-  }
-  if (s->z0) cufftDestroy(s->z0);
-  cudaFree(s->work);
-  cudaFree(s->A);
+  slab_release(p, s);
   delete s;
   p->slab = nullptr;
 }
@@ -130,43 +126,14 @@ static int slab_ensure_work(pf_plan* p, SlabPlan* s, size_t need) {
 
 using namespace pf;
 
-static int slab_checked(pf_plan* p, SlabPlan** out) {
-  PF_ARG(p && p->slab, "not a slab plan");
-  *out = sp_of(p);
-  return PF_OK;
-}
+namespace pf {
 
-extern "C" {
-
-int pf_slab_plan_create(pf_plan** out, const int64_t* dims, int nranks, int rank, int symbol_mode, int device,
-                        void* stream) {
-  PF_ARG(out && dims, "null argument");
-  PF_ARG(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank %d of %d", rank, nranks);
-  PF_ARG(dims[0] % nranks == 0 && dims[1] % nranks == 0, "N0 and N1 must be divisible by the rank count");
-  PF_CK(pf_plan_create(out, 3, dims, symbol_mode, device, stream));  // global symbol tables, no scratch
-  pf_plan* p = *out;
-  SlabPlan* s = new SlabPlan();
-  p->slab = s;
-  s->N0 = (int)dims[0];
-  s->N1 = (int)dims[1];
-  s->N2 = (int)dims[2];
-  s->P = nranks;
-  s->rank = rank;
-  s->L0 = s->N0 / nranks;
-  s->L1 = s->N1 / nranks;
-  s->H2 = s->N2 / 2 + 1;
-  Geom& gs = s->gs;
-  gs = p->g;  // global dn / inv_n
-  gs.n[0] = s->N0;
-  gs.n[1] = s->L1;
-  gs.n[2] = s->N2;
-  gs.n2h = s->H2;
-  gs.nh = (int64_t)s->N0 * s->L1 * s->H2;
-  gs.k1off = rank * s->L1;
-  // local real slab as the plan geometry (S3 / S4 sizes)
-  p->g.n[0] = s->L0;
-  p->g.nr = (int64_t)s->L0 * s->N1 * s->N2;
-  // cuFFT plans
+// cuFFT plans (2D over (i1, i2) for 1..3 components, 1D along i0), their work
+// area and the A-layout scratch: created on first use.  The fused slab uses them
+// only at setup / teardown and releases them in between (a 1024^3 cell over two
+// ranks needs that memory).
+static int slab_transforms(pf_plan* p, SlabPlan* s) {
+  if (s->A) return PF_OK;
   long long d2[2] = {s->N1, s->N2};
   size_t need = 0, ws = 0;
   for (int k = 1; k <= 3; ++k) {
@@ -198,7 +165,65 @@ int pf_slab_plan_create(pf_plan** out, const int64_t* dims, int nranks, int rank
   PF_CK_FFT(cufftSetWorkArea(s->z0, s->work));
   PF_CK_FFT(cufftSetStream(s->z0, p->work));
   PF_CK_CUDA(cudaMalloc(&s->A, sizeof(double2) * 3 * (size_t)s->L0 * s->N1 * s->H2));
-  p->scratch_bytes += sizeof(double2) * 3 * (size_t)s->L0 * s->N1 * s->H2 + s->work_bytes;
+  return PF_OK;
+}
+
+static void slab_release(pf_plan* p, SlabPlan* s) {
+  cudaStreamSynchronize(p->work);
+  for (int k = 1; k <= 3; ++k) {
+    if (s->f2d[k]) cufftDestroy(s->f2d[k]);
+    if (s->i2d[k]) cufftDestroy(s->i2d[k]);
+    s->f2d[k] = s->i2d[k] = 0;
+  }
+  if (s->z0) cufftDestroy(s->z0);
+  s->z0 = 0;
+  cudaFree(s->work);
+  cudaFree(s->A);
+  s->work = nullptr;
+  s->work_bytes = 0;
+  s->A = nullptr;
+}
+
+static int slab_checked(pf_plan* p, SlabPlan** out) {
+  PF_ARG(p && p->slab, "not a slab plan");
+  *out = sp_of(p);
+  return PF_OK;
+}
+
+}  // namespace pf
+
+extern "C" {
+
+int pf_slab_plan_create(pf_plan** out, const int64_t* dims, int nranks, int rank, int symbol_mode, int device,
+                        void* stream) {
+  PF_ARG(out && dims, "null argument");
+  PF_ARG(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank %d of %d", rank, nranks);
+  PF_ARG(dims[0] % nranks == 0 && dims[1] % nranks == 0, "N0 and N1 must be divisible by the rank count");
+  PF_CK(pf_plan_create(out, 3, dims, symbol_mode, device, stream));  // global symbol tables, no scratch
+  pf_plan* p = *out;
+  SlabPlan* s = new SlabPlan();
+  p->slab = s;
+  s->N0 = (int)dims[0];
+  s->N1 = (int)dims[1];
+  s->N2 = (int)dims[2];
+  s->P = nranks;
+  s->rank = rank;
+  s->L0 = s->N0 / nranks;
+  s->L1 = s->N1 / nranks;
+  s->H2 = s->N2 / 2 + 1;
+  Geom& gs = s->gs;
+  gs = p->g;  // global dn / inv_n
+  gs.n[0] = s->N0;
+  gs.n[1] = s->L1;
+  gs.n[2] = s->N2;
+  gs.n2h = s->H2;
+  gs.nh = (int64_t)s->N0 * s->L1 * s->H2;
+  gs.k1off = rank * s->L1;
+  // local real slab as the plan geometry (S3 / S4 sizes)
+  p->g.n[0] = s->L0;
+  p->g.nr = (int64_t)s->L0 * s->N1 * s->N2;
+  // the cuFFT plans, their work area and the A-layout scratch are created on
+  // first use (slab_transforms) and can be released (pf_slab_release_transforms)
   return PF_OK;
 }
 
@@ -218,6 +243,7 @@ int pf_slab_forward(pf_plan* p, const double* real, int ncomp, double* send) {
   SlabPlan* s;
   PF_CK(slab_checked(p, &s));
   PF_ARG(ncomp >= 1 && ncomp <= 3, "ncomp 1..3");
+  PF_CK(slab_transforms(p, s));
   PF_CK(enter(p));
   PF_CK_FFT(cufftExecD2Z(s->f2d[ncomp], (cufftDoubleReal*)real, (cufftDoubleComplex*)s->A));
   const int64_t total = (int64_t)s->P * ncomp * s->L0 * s->L1 * s->H2;
@@ -230,6 +256,7 @@ int pf_slab_forward_finish(pf_plan* p, const double* recv, int ncomp, double* ts
   SlabPlan* s;
   PF_CK(slab_checked(p, &s));
   PF_ARG(ncomp >= 1 && ncomp <= 3, "ncomp 1..3");
+  PF_CK(slab_transforms(p, s));
   PF_CK(enter(p));
   const int64_t total = (int64_t)s->P * ncomp * s->L0 * s->L1 * s->H2;
   k_slab_move<<<blocks_for(total), kThreads, 0, p->work>>>(*s, ncomp, 1, (const double2*)recv, (double2*)tspec);
@@ -247,6 +274,7 @@ int pf_slab_inverse(pf_plan* p, double* tspec, int ncomp, double* send) {
   SlabPlan* s;
   PF_CK(slab_checked(p, &s));
   PF_ARG(ncomp >= 1 && ncomp <= 3, "ncomp 1..3");
+  PF_CK(slab_transforms(p, s));
   PF_CK(enter(p));
   const int64_t per = (int64_t)s->N0 * s->L1 * s->H2;
   for (int c = 0; c < ncomp; ++c) {
@@ -263,6 +291,7 @@ int pf_slab_inverse_finish(pf_plan* p, const double* recv, int ncomp, double* re
   SlabPlan* s;
   PF_CK(slab_checked(p, &s));
   PF_ARG(ncomp >= 1 && ncomp <= 3, "ncomp 1..3");
+  PF_CK(slab_transforms(p, s));
   PF_CK(enter(p));
   const int64_t total = (int64_t)s->P * ncomp * s->L0 * s->L1 * s->H2;
   k_slab_move<<<blocks_for(total), kThreads, 0, p->work>>>(*s, ncomp, 3, (const double2*)recv, s->A);
@@ -448,6 +477,24 @@ int pf_slab_fused_setup(pf_plan* p, const double* Tq, const double* Td, double* 
   PF_CK(enter(p));
   PF_CK(fused_slab_setup(p, (const double2*)Tq, (const double2*)Td, R));
   return leave(p);
+}
+
+int pf_slab_fused_setup_zero(pf_plan* p) {
+  PF_NVTX("pf_slab_fused_setup_zero");
+  SlabPlan* s;
+  PF_CK(fslab_checked(p, &s));
+  PF_CK(enter(p));
+  int64_t ym = 0, yn = 0;
+  PF_CK(pf_slab_fused_sizes(p, &ym, &yn));
+  PF_CK(fused_slab_setup_zero(p, ym, yn));
+  return leave(p);
+}
+
+int pf_slab_release_transforms(pf_plan* p) {
+  SlabPlan* s;
+  PF_CK(slab_checked(p, &s));
+  slab_release(p, s);
+  return PF_OK;
 }
 
 int pf_slab_fused_pk(pf_plan* p) {

@@ -129,6 +129,12 @@ class DeviceSlabBackend:
     def fused_setup(self, Q, D, R):
         N.check(self.lib.pf_slab_fused_setup(self.h, self._p(Q), self._p(D), self._p(R)))
 
+    def fused_setup_zero(self):
+        N.check(self.lib.pf_slab_fused_setup_zero(self.h))
+
+    def release_transforms(self):
+        N.check(self.lib.pf_slab_release_transforms(self.h))
+
     def fused_pk(self):
         N.check(self.lib.pf_slab_fused_pk(self.h))
 
@@ -195,16 +201,32 @@ class SlabStokes:
             self.dist = dist if dist.is_available() and dist.is_initialized() else None
         self.world = self.dist.get_world_size(group) if self.dist else 1
         be = backend
-        self.send = be.alloc_complex(3 * be.exch)
-        self.recv = be.alloc_complex(3 * be.exch) if self.world > 1 else self.send
-        self.TR = be.alloc_complex(3 * be.tspec)
-        self.TU = be.alloc_complex(3 * be.tspec)
-        self.Q = be.alloc_complex(be.tspec)
-        self.D = be.alloc_complex(be.tspec)
-        self.R = be.alloc_real(3 * be.real)
-        self.unew = be.alloc_real(3 * be.real)
+        if self._eager_buffers:
+            self._alloc_buffers(3)
         self.totals = be.alloc_real(9)
         self.hist = be.alloc_real(cfg.max_iter * len(REPORT_COLUMNS))
+
+    # the cuFFT-slab transform buffers (every iteration of SlabStokes; only setup
+    # and teardown of FusedSlabStokes, which allocates them for those phases only)
+    _eager_buffers = True
+
+    def _alloc_buffers(self, ncomp, teardown: bool = False):
+        """``teardown``: only what end() needs (Q^, one T-layout component, one
+        component's exchange buffers)."""
+        be = self.b
+        self.send = be.alloc_complex(ncomp * be.exch)
+        self.recv = be.alloc_complex(ncomp * be.exch) if self.world > 1 else self.send
+        self.TU = be.alloc_complex(ncomp * be.tspec)
+        self.Q = be.alloc_complex(be.tspec)
+        if teardown:
+            return
+        self.TR = be.alloc_complex(ncomp * be.tspec)
+        self.D = be.alloc_complex(be.tspec)
+        self.R = be.alloc_real(ncomp * be.real)
+        self.unew = be.alloc_real(ncomp * be.real)
+
+    def _free_buffers(self):
+        self.send = self.recv = self.TR = self.TU = self.Q = self.D = self.R = self.unew = None
 
     def _exchange(self, ncomp):
         if self.world == 1:
@@ -361,15 +383,27 @@ class FusedSlabStokes(SlabStokes):
             self.dist.all_to_all_single(dst[c * per:(c + 1) * per], src[c * per:(c + 1) * per], group=self.group)
         self.dist.all_to_all_single(dstn, srcn, group=self.group)
 
+    _eager_buffers = False  # the transform buffers exist only during setup / teardown
+
     def begin(self):
         cfg, st, be = self.cfg, self.state, self.b
         params = _params(cfg, self.pen, cfg.max_iter)
         be.begin(params, self.solid, st["u"], st["u_tilde"], st["q"], st["a"], st["lam"], self.hist)
-        self._to_spectrum(st["q"], 1, self.TU)
-        self._to_spectrum(st["u"], 3, self.TR)
-        be.setup(self.TU, self.TR, self.Q, self.D)  # T-layout Q^ (gauged), D^
-        be.fused_setup(self.Q, self.D, self.R)       # tile-major Q^, D^; x-slab Y of R; compact layout
-        self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
+        t = torch()
+        nz = t.stack([t.count_nonzero(v) for v in st.values()]).sum().to(t.float64).reshape(1)
+        if self.world > 1:  # every rank must take the same setup path (the transforms exchange)
+            self.dist.all_reduce(nz, group=self.group)
+        if float(nz.item()) == 0.0:
+            be.fused_setup_zero()  # cold start: zero spectra and Y, no transform or scratch
+        else:
+            self._alloc_buffers(3)
+            self._to_spectrum(st["q"], 1, self.TU)
+            self._to_spectrum(st["u"], 3, self.TR)
+            be.setup(self.TU, self.TR, self.Q, self.D)  # T-layout Q^ (gauged), D^
+            be.fused_setup(self.Q, self.D, self.R)       # tile-major Q^, D^; x-slab Y of R; compact layout
+            self._free_buffers()
+            be.release_transforms()
+            self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
         self.it = 0
         return self
 
@@ -449,8 +483,11 @@ class FusedSlabStokes(SlabStokes):
 
     def end(self) -> ConvergenceReport:
         self._drain()
+        self._alloc_buffers(1, teardown=True)  # one component's transform buffers
         self.b.fused_end(self.Q)  # Q^ back to T layout; u~, a, lam materialised
         rep = super().end()
+        self._free_buffers()
+        self.b.release_transforms()
         rep.meta["pipeline"] = "slab-fused"
         rep.meta["exchange"] = "p2p" if self.p2p else ("a2a-overlapped" if self.overlap else "a2a")
         return rep

@@ -258,3 +258,32 @@ def test_slab_permeability_matches_single_gpu(pf, world):
 
     for K in run_ranks(world, rank_fn):
         np.testing.assert_allclose(K, K_ref, rtol=1e-12, atol=1e-14 * np.abs(K_ref).max())
+
+
+def test_fused_slab_warm_start_two_ranks(pf):
+    """Warm start through the fused slab (the transform setup path, its buffers
+    allocated for setup only): 10 + 10 iterations over two loopback ranks equal
+    20 uninterrupted single-GPU iterations."""
+    from paper_2312_15554_b200.slab import slab_range, solve_stokes_slab
+    from slab_loopback import run_ranks
+
+    ind = pf.random_packing_geometry(64, seed=13)
+    g = (1.0, 0.5, 0.0)
+    pen = pf.PenaltyParams(alpha=500.0, beta=500.0, b=500.0, adaptive=False)
+    full, _ = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=g, max_iter=20), pen,
+                                     pipeline="fused")
+    half, _ = pf.solve_stokes_device(ind, pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=g, max_iter=10), pen,
+                                     pipeline="fused")
+    init = {k: getattr(half, k).cpu().numpy() for k in ("u", "u_tilde", "q", "a", "lam")}
+    vals = np.asarray(ind.values)
+    cfg = pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=g, max_iter=10)
+
+    def rank_fn(r, comm):
+        lo, hi = slab_range(64, 2, r)
+        loc = {k: (v[lo:hi] if k == "q" else v[:, lo:hi]) for k, v in init.items()}
+        st, rep = solve_stokes_slab(vals[lo:hi], vals.shape, cfg, pen, init_local=loc, comm=comm, fused=True)
+        return st["u"].cpu().numpy(), rep
+
+    res = run_ranks(2, rank_fn)
+    u = np.concatenate([x for x, _ in res], axis=1)
+    assert rel_l2(u, full.u.cpu().numpy()) <= 1e-10
