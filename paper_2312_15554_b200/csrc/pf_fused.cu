@@ -73,14 +73,14 @@
 #ifndef PF_PK512_MINB
 #define PF_PK512_MINB 2
 #endif
-#ifndef PF_PK1024_T  // PK at N = 1024
-#define PF_PK1024_T 128
+#ifndef PF_PK1024_T  // PK at N = 1024: 2 columns (32-byte pencil rows) x 192 threads, 2 blocks/SM
+#define PF_PK1024_T 192  // (1024^3 rank of 2: 18.8 ms vs 31.5 with 1 column x 128 threads; rank of 8: 3.66 vs 3.70)
 #endif
 #ifndef PF_PK1024_CP
-#define PF_PK1024_CP 1
+#define PF_PK1024_CP 2
 #endif
 #ifndef PF_PK1024_MINB
-#define PF_PK1024_MINB 3
+#define PF_PK1024_MINB 2
 #endif
 #ifndef PF_RS1024_T
 #define PF_RS1024_T 64
