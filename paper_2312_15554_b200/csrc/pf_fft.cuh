@@ -277,6 +277,78 @@ __device__ __forceinline__ void radix_twiddle(double2* a, const double2* __restr
   }
 }
 
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+// One 256-point FFT (unnormalised; same input / output positions and padding as
+// fft_seq<256>) by a whole warp: each 16-point DFT of the two passes is split
+// over a lane pair (j, j + 16) as an 8-point DFT of its even / odd inputs and a
+// radix-2 merge through one shuffle exchange, so a sequence's two passes take
+// half the dependent-instruction latency of the 16-lane version and both warps
+// of a two-sequence tile can work at once.  Every lane must call it.
+template <bool INV>
+__device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict__ tw, int lane, bool active) {
+  using C = Cfg<256>;
+  const int j = lane & 15, h = lane >> 4;
+  double2 x[8];
+  auto merge = [&](void) {
+    Dft<8, INV>::run(x);
+    if (h) {
+#pragma unroll
+      for (int k = 1; k < 8; ++k) x[k] = rot16<INV>(x[k], k);  // O'[k] = w16^k O[k]
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 y = shfl_xor2(x[k], 16);
+      x[k] = h ? csub(y, x[k]) : cadd(x[k], y);  // X[k] = E + O' (h = 0), X[k + 8] = E - O' (h = 1)
+    }
+  };
+  // pass 1: sub-DFT j over n1 (elements 16 n1 + j); this lane's half n1 = 2 m + h
+  if (active) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = s[C::pad(16 * (2 * m + h) + j)];
+  }
+  merge();
+  {
+    // twiddle w^(k1 j), k1 = k + 8 h = 4 a + b, from the [k1][l] table rows
+    double2 wb[4], wa[2];
+#pragma unroll
+    for (int b = 1; b < 4; ++b) wb[b] = tw[(b - 1) * C::B + j];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int a = 2 * h + q;
+      wa[q] = a == 0 ? make_double2(1.0, 0.0) : tw[(2 + a) * C::B + j];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = k / 4, b = k % 4;
+      if (h == 0 && k == 0) continue;
+      double2 w = b == 0 ? wa[q] : (h == 0 && q == 0 ? wb[b] : cmul(wa[q], wb[b]));
+      if (INV) w.y = -w.y;
+      x[k] = cmul(x[k], w);
+    }
+  }
+  __syncwarp();
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[C::pad(k + 8 * h + 16 * j)] = x[k];
+  }
+  __syncwarp();
+  // pass 2: sub-DFT j over n2 (elements j + 16 n2); half n2 = 2 m + h
+  if (active) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = s[C::pad(j + 16 * (2 * m + h))];
+  }
+  merge();
+  __syncwarp();
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[C::pad(j + 16 * (k + 8 * h))] = x[k];
+  }
+  __syncwarp();
+}
+
 // Radix-M stage of long sequences (Cfg<N>::M > 1; no-op otherwise), all threads
 // of the block: forward = DIF butterfly + twiddle w_N^(j r) (natural order in,
 // blocks ready for their L-point transforms); inverse = conjugate twiddle +

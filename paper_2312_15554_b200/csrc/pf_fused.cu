@@ -43,6 +43,9 @@
 // forcing 5 squeezes ptxas to 168 with spills and is 16 % slower; N <= 128 at 3)
 #define PF_RSC_MINB (N == 256 ? 4 : 3)
 #endif
+#ifndef PF_RS_W32
+#define PF_RS_W32 1  // RS at N = 256: each row-pair FFT on a whole warp (fft256_w32): 0.479 -> 0.453 ms
+#endif
 #ifndef PF_RS_HALFT
 #define PF_RS_HALFT(N) ((N) <= 128)
 #endif
@@ -245,7 +248,11 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     }
     for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
-    fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
+    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
+      fft256_w32<true>(SI + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    } else {
+      fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
+    }
     if constexpr (C::M > 1) {
       __syncthreads();
       radix_stage<N, true>(SI, NP, SS, tw, t, T);
@@ -294,7 +301,11 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
+      fft256_w32<false>(SF + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    } else {
+      fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    }
     __syncthreads();
     // (3) separate the two real transforms of each row pair, store X-space rows of R
     for (int idx = t; idx < NP * H; idx += T) {
@@ -365,7 +376,11 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
+      fft256_w32<false>(SF + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    } else {
+      fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    }
     __syncthreads();
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
@@ -474,6 +489,8 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   static_assert(T % 32 == 0, "segment bases are per warp");
   // segment bases: groups of 32 segments of 32 voxels (V = 1024: one; 2048 at N = 1024: two)
   constexpr int SG = V / 1024;
+  // one warp per row-pair sequence (fft256_w32) where the tile has exactly one per warp
+  constexpr bool W32 = PF_RS_W32 && N == 256 && T == 32 * NP;
   if (V != 1024 && V != 2048) return;  // (never launched otherwise)
   pdl_wait();
   if (ctrl->done) return;
@@ -488,7 +505,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   double2* sx = (double2*)(sc + 3 * CS);
   double2* sxn = (double2*)((unsigned char*)sx + K::XM);
   uint8_t* sh = (uint8_t*)((unsigned char*)sxn + K::XN);
-  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31, warp = t >> 5;
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
   const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
@@ -532,7 +549,11 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     }
     for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
-    fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
+    if constexpr (W32) {
+      fft256_w32<true>(SI + (warp < NP ? warp : 0) * SS, tw, lane, warp < NP);
+    } else {
+      fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
+    }
     if constexpr (C::M > 1) {
       __syncthreads();
       radix_stage<N, true>(SI, NP, SS, tw, t, T);
@@ -586,7 +607,11 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    if constexpr (W32) {
+      fft256_w32<false>(SF + (warp < NP ? warp : 0) * SS, tw, lane, warp < NP);
+    } else {
+      fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    }
     __syncthreads();
     for (int idx = t; idx < NP * H; idx += T) {
       const int p = idx / H, k = idx % H;
@@ -652,7 +677,11 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
+      fft256_w32<false>(SF + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    } else {
+      fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    }
     __syncthreads();
     double2* XU = B.XU + (size_t)c * (SL ? B.l0 : N) * N * H;
     double2* XUn = B.XUn + (size_t)c * (SL ? B.l0 : N) * N;
