@@ -349,6 +349,18 @@ __device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict
   __syncwarp();
 }
 
+// The 256-point block transforms of nseq sequences (stride ss) with one warp per
+// block (fft256_w32): unit = warp index; the caller has exactly nseq * M warps.
+template <int N, bool INV>
+__device__ __forceinline__ void fft_units_w32(double2* S, int nseq, int ss, const double2* tw, int t) {
+  using C = Cfg<N>;
+  static_assert(C::L == 256, "one-warp block transforms are 256-point");
+  const int u = t >> 5;
+  const bool act = u < nseq * C::M;
+  const int uu = act ? u : 0;
+  fft256_w32<INV>(S + (size_t)(uu / C::M) * ss + (uu % C::M) * C::SSL, tw, t & 31, act);
+}
+
 // Radix-M stage of long sequences (Cfg<N>::M > 1; no-op otherwise), all threads
 // of the block: forward = DIF butterfly + twiddle w_N^(j r) (natural order in,
 // blocks ready for their L-point transforms); inverse = conjugate twiddle +

@@ -86,7 +86,7 @@
 #define PF_PK1024_MINB 2
 #endif
 #ifndef PF_RS1024_T
-#define PF_RS1024_T 64
+#define PF_RS1024_T 128  // one warp per 256-point block (fft_units_w32): rank of 8 RS 5.97 -> 5.71 ms
 #endif
 #ifndef PF_RS512_T  // RS threads at N = 512 (one row pair per tile: 2 block transforms of 16 lanes)
 #define PF_RS512_T 64  // (measured 3.93 ms vs 4.38 at 32 and 4.48 at 128)
@@ -248,8 +248,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     }
     for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
-    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
-      fft256_w32<true>(SI + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    if constexpr (PF_RS_W32 && C::L == 256 && T == 32 * NP * C::M) {
+      fft_units_w32<N, true>(SI, NP, SS, tw, t);
     } else {
       fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
     }
@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
-      fft256_w32<false>(SF + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    if constexpr (PF_RS_W32 && C::L == 256 && T == 32 * NP * C::M) {
+      fft_units_w32<N, false>(SF, NP, SS, tw, t);
     } else {
       fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     }
@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix(Bufs B, const double* __res
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
-      fft256_w32<false>(SF + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    if constexpr (PF_RS_W32 && C::L == 256 && T == 32 * NP * C::M) {
+      fft_units_w32<N, false>(SF, NP, SS, tw, t);
     } else {
       fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     }
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   // segment bases: groups of 32 segments of 32 voxels (V = 1024: one; 2048 at N = 1024: two)
   constexpr int SG = V / 1024;
   // one warp per row-pair sequence (fft256_w32) where the tile has exactly one per warp
-  constexpr bool W32 = PF_RS_W32 && N == 256 && T == 32 * NP;
+  constexpr bool W32 = PF_RS_W32 && C::L == 256 && T == 32 * NP * C::M;
   if (V != 1024 && V != 2048) return;  // (never launched otherwise)
   pdl_wait();
   if (ctrl->done) return;
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
     if constexpr (W32) {
-      fft256_w32<true>(SI + (warp < NP ? warp : 0) * SS, tw, lane, warp < NP);
+      fft_units_w32<N, true>(SI, NP, SS, tw, t);
     } else {
       fft_units<N, true>(SI, NP, SS, tw, g, l, T / C::G);
     }
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
       __syncthreads();
     }
     if constexpr (W32) {
-      fft256_w32<false>(SF + (warp < NP ? warp : 0) * SS, tw, lane, warp < NP);
+      fft_units_w32<N, false>(SF, NP, SS, tw, t);
     } else {
       fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     }
@@ -677,8 +677,8 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
     }
-    if constexpr (PF_RS_W32 && N == 256 && T == 32 * NP) {
-      fft256_w32<false>(SF + ((t >> 5) < NP ? (t >> 5) : 0) * SS, tw, t & 31, (t >> 5) < NP);
+    if constexpr (PF_RS_W32 && C::L == 256 && T == 32 * NP * C::M) {
+      fft_units_w32<N, false>(SF, NP, SS, tw, t);
     } else {
       fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
     }
