@@ -287,11 +287,13 @@ __device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
 // radix-2 merge through one shuffle exchange, so a sequence's two passes take
 // half the dependent-instruction latency of the 16-lane version and both warps
 // of a two-sequence tile can work at once.  Every lane must call it.
+// fft256_w32 once pass 1's inputs are in registers: x[m] = element 16 (2 m + h) + j
+// (lane = 16 h + j) — lets a caller read them straight from a TMA tile.
 template <bool INV>
-__device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict__ tw, int lane, bool active) {
+__device__ __forceinline__ void fft256_w32_x(double2* x, double2* s, const double2* __restrict__ tw, int lane,
+                                             bool active) {
   using C = Cfg<256>;
   const int j = lane & 15, h = lane >> 4;
-  double2 x[8];
   auto merge = [&](void) {
     Dft<8, INV>::run(x);
     if (h) {
@@ -305,10 +307,6 @@ __device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict
     }
   };
   // pass 1: sub-DFT j over n1 (elements 16 n1 + j); this lane's half n1 = 2 m + h
-  if (active) {
-#pragma unroll
-    for (int m = 0; m < 8; ++m) x[m] = s[C::pad(16 * (2 * m + h) + j)];
-  }
   merge();
   {
     // twiddle w^(k1 j), k1 = k + 8 h = 4 a + b, from the [k1][l] table rows
@@ -347,6 +345,18 @@ __device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict
     for (int k = 0; k < 8; ++k) s[C::pad(j + 16 * (k + 8 * h))] = x[k];
   }
   __syncwarp();
+}
+
+template <bool INV>
+__device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict__ tw, int lane, bool active) {
+  using C = Cfg<256>;
+  const int j = lane & 15, h = lane >> 4;
+  double2 x[8];
+  if (active) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = s[C::pad(16 * (2 * m + h) + j)];
+  }
+  fft256_w32_x<INV>(x, s, tw, lane, active);
 }
 
 // The 256-point block transforms of nseq sequences (stride ss) with one warp per
