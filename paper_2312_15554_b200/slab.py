@@ -339,8 +339,12 @@ class FusedSlabStokes(SlabStokes):
     inverse + rows + local step (MI, RS), the 9-double all-reduce and finalize,
     the axis-1 forward (MF), and the all-to-all back.  Y is exchanged in the
     exchange-native layouts of ``pf_slab_fused_*`` (contiguous equal splits:
-    one all_to_all per component plus one for the Nyquist columns), so there is
-    no packing pass; at P = 1 both layouts coincide and nothing moves."""
+    one all_to_all per component plus one for the Nyquist columns, overlapped
+    with the per-component passes), so there is no packing pass; at P = 1 both
+    layouts coincide and nothing moves.  Only the Y buffers and the passes'
+    own state stay resident: a cold start needs no transform (zero spectra),
+    and the cuFFT-slab transforms of a warm start / the teardown exist only
+    while they run — so a 1024^3 cell fits on two ranks."""
 
     def __init__(self, backend, dims, cfg, penalties, solid_local, state, group=None, poll_every: int = 8,
                  comm=None, overlap: bool = True, exchange: str = "a2a"):
