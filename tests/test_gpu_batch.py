@@ -75,3 +75,41 @@ def test_transport_batch_bitwise_equals_sequential(pf, dims):
         assert r1.iterations == r2.iterations and r1.converged == r2.converged
         assert np.array_equal(r1.history, r2.history)
         assert bool((s1.chi == s2.chi).all()) and bool((s1.grad_chi == s2.grad_chi).all())
+
+
+def test_solver_instances_on_host_threads(pf):
+    """The reference's concurrency contract (tests/test_backends.py:131-149):
+    independent solves issued from several host threads at once (each thread
+    its own plans and current stream) equal the same solves run one by one."""
+    import threading
+
+    import torch
+
+    cells = [pf.random_packing_geometry(48, seed=s) for s in range(3)]
+    cfg = pf.StokesConfig.with_tolerance(1e-6, pressure_gradient=(1.0, 0.0, 0.0), max_iter=80)
+    tcfg = pf.TransportConfig(pe=5.0, eps=1e-8, composition_gradient=(0.0, 1.0, 0.0), max_iter=40)
+    seq = []
+    for ind in cells:
+        st, rep = pf.solve_stokes(ind, cfg)
+        ts, trep = pf.solve_transport(ind, st.u, tcfg)
+        seq.append((st.u, rep.iterations, ts.chi, trep.iterations))
+    out, errs = [None] * len(cells), []
+
+    def work(k):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                st, rep = pf.solve_stokes(cells[k], cfg)
+                ts, trep = pf.solve_transport(cells[k], st.u, tcfg)
+            out[k] = (st.u, rep.iterations, ts.chi, trep.iterations)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(cells))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    for a, b in zip(seq, out):
+        assert a[1] == b[1] and a[3] == b[3]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
