@@ -195,3 +195,25 @@ def test_fused_long_sequences_512_match_cufft_pipeline(pf, compact):
     _hist_close(ra.history, rb.history)
     del b
     torch.cuda.empty_cache()
+
+
+def test_fused_256_headline_cell_matches_cufft_pipeline(pf):
+    """The bench's own size (256^3 random packing, compact storage, whole-warp RS
+    transforms, TMA pencils): a truncated adaptive solve equals the cuFFT
+    pipeline's to round-off."""
+    import torch
+
+    ind = pf.random_packing_geometry(256, seed=1)
+    cfg = pf.StokesConfig.with_tolerance(1e-9, pressure_gradient=(0.3, 1.0, -0.5), max_iter=5)
+    a, ra = pf.solve_stokes_device(ind, cfg, pipeline="fused")
+    assert ra.meta["pipeline"] == "fused-compact"
+    ah = {k: getattr(a, k).cpu().numpy() for k in ("u", "u_tilde", "q", "a", "lam")}
+    del a
+    torch.cuda.empty_cache()
+    b, rb = pf.solve_stokes_device(ind, cfg, pipeline="cufft")
+    assert ra.iterations == rb.iterations == 5
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(ah[k], getattr(b, k).cpu().numpy()) <= FIELD_TOL, k
+    _hist_close(ra.history, rb.history)
+    del b
+    torch.cuda.empty_cache()
