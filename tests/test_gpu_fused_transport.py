@@ -95,13 +95,13 @@ def test_fused_transport_warm_start(pf, flow64):
     _hist_close(rep.history, hist)
 
 
-def test_fused_transport_512_matches_cufft_pipeline(pf):
-    """Long sequences (N = 512, two 256-point blocks + radix-2 stage) in the
-    transport passes: truncated solve under a synthetic flow against the cuFFT
-    transport pipeline (iterations, chi and grad chi to round-off, history)."""
+@pytest.mark.parametrize("n", [256, 512])
+def test_fused_transport_long_matches_cufft_pipeline(pf, n):
+    """256^3 (the transport bench size) and 512^3 (long sequences: two 256-point
+    blocks + radix-2 stage): truncated solve under a synthetic flow against the
+    cuFFT transport pipeline (iterations, chi and grad chi to round-off, history)."""
     import torch
 
-    n = 512
     ind = pf.random_packing_geometry(n, seed=6)
     dev = torch.device("cuda", 0)
     x = torch.arange(n, dtype=torch.float64, device=dev) / n
