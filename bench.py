@@ -591,8 +591,10 @@ def run_slab_workload(args):
 
         dist.init_process_group("nccl", device_id=dev)
     n = args.n
-    ind = pf.random_packing_geometry(n, seed=0)
+    from paper_2312_15554_b200.grid import rasterize_packing_slab, random_sphere_packing
+
     lo, hi = S.slab_range(n, world, rank)
+    solid_np = rasterize_packing_slab(random_sphere_packing(0), (n, n, n), lo, hi)  # this rank's planes only
     cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=(1.0, 0.0, 0.0),
                                          max_iter=args.warmup + args.steps + 1)
     be = S.DeviceSlabBackend((n, n, n), world, rank, "central", dev)
@@ -600,7 +602,7 @@ def run_slab_workload(args):
     L = (hi - lo) * n * n
     st = {k: torch.zeros(3 * L, dtype=torch.float64, device=dev) for k in ("u", "u_tilde", "a", "lam")}
     st["q"] = torch.zeros(L, dtype=torch.float64, device=dev)
-    solid = torch.as_tensor(np.ascontiguousarray(ind.values[lo:hi])).reshape(-1).to(dev)
+    solid = torch.as_tensor(solid_np).reshape(-1).to(dev)
     fused = be.fused_sizes()[0] > 0 and not args.slab_cufft
     if fused:
         comm = S.SymmetricMemoryExchange() if (args.exchange == "p2p" and world > 1) else None

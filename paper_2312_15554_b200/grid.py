@@ -246,3 +246,36 @@ def rasterize_packing(packing: SpherePacking, dims) -> IndicatorField:
 def random_packing_geometry(n: int, seed: int = 0, **kwargs) -> IndicatorField:
     """BASELINE cfg-3/4/5 microstructure at n^3."""
     return rasterize_packing(random_sphere_packing(seed, **kwargs), (n, n, n))
+
+
+def rasterize_packing_slab(packing: SpherePacking, dims, lo: int, hi: int) -> np.ndarray:
+    """The x-slab i0 in [lo, hi) of ``rasterize_packing(packing, dims).values``
+    (uint8, (hi - lo, N1, N2)) without materialising the whole cell — each rank
+    of a slab-decomposed solve (slab.py) builds only its own planes."""
+    dims = tuple(int(x) for x in dims)
+    if len(dims) != 3 or not (0 <= lo < hi <= dims[0]):
+        raise ValueError("slab rasterization needs 3D dims and 0 <= lo < hi <= N0")
+    solid = np.zeros((hi - lo,) + dims[1:], dtype=bool)
+    for c, r in zip(packing.centers, packing.radii):
+        sel, d2 = [], []
+        for a in range(3):
+            n = dims[a]
+            a_lo = int(np.floor((c[a] - r) * n - 0.5)) - 1
+            a_hi = int(np.ceil((c[a] + r) * n - 0.5)) + 1
+            idx = np.arange(a_lo, a_hi + 1)
+            y = (idx + 0.5) / n
+            dy = y - c[a]
+            dy -= np.round(dy)
+            keep = dy * dy <= r * r
+            ii = np.mod(idx[keep], n)
+            dd = dy[keep] ** 2
+            if a == 0:  # only this slab's planes, shifted to local indices
+                m = (ii >= lo) & (ii < hi)
+                ii, dd = ii[m] - lo, dd[m]
+            sel.append(ii)
+            d2.append(dd)
+        if any(x.size == 0 for x in sel):
+            continue
+        inside = (d2[0][:, None, None] + d2[1][None, :, None] + d2[2][None, None, :]) <= r * r
+        solid[np.ix_(*sel)] |= inside
+    return solid.astype(np.uint8)

@@ -115,3 +115,17 @@ def test_backend_env_rejects_unknown(monkeypatch):
         importlib.reload(backends)
     monkeypatch.delenv("POREFLOW_BACKEND")
     importlib.reload(backends)
+
+
+def test_packing_slab_rasterization_equals_full_cell():
+    """Each slab rank can rasterize only its x-planes (grid.rasterize_packing_slab):
+    identical to the corresponding planes of the whole cell, wrap-around included."""
+    import numpy as np
+
+    from paper_2312_15554_b200.grid import rasterize_packing, rasterize_packing_slab, random_sphere_packing
+
+    pk = random_sphere_packing(3)
+    dims = (32, 28, 24)
+    full = rasterize_packing(pk, dims).values
+    for lo, hi in [(0, 8), (8, 16), (24, 32), (31, 32)]:
+        assert np.array_equal(rasterize_packing_slab(pk, dims, lo, hi), full[lo:hi]), (lo, hi)

@@ -51,10 +51,10 @@ def stage_times(sol, be, iters):
 
 def run(n, world, iters, fused, stages=False):
     dev = torch.device("cuda", 0)
-    ind = pf.random_packing_geometry(n, seed=0)
+    from paper_2312_15554_b200.grid import rasterize_packing_slab, random_sphere_packing
+
     lo, hi = S.slab_range(n, world, 0)
-    solid_np = np.ascontiguousarray(ind.values[lo:hi])
-    del ind
+    solid_np = rasterize_packing_slab(random_sphere_packing(0), (n, n, n), lo, hi)  # rank 0's planes only
     cfg = pf.StokesConfig.with_tolerance(1e-12, pressure_gradient=(1.0, 0.0, 0.0), max_iter=iters + 8)
     be = S.DeviceSlabBackend((n, n, n), world, 0, "central", dev)
     be.bind()
