@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = (SL ? B.nc : 3) * TPC;  // component window [c0, c0 + nc) (slab)
-  constexpr int SPR = N / 32;  // 32-voxel segments per row
+  // (32-voxel segments: N / 32 per row)
   const int CS = cp.cs;
   static_assert(T % 32 == 0, "segment bases are per warp");
   // segment bases: groups of 32 segments of 32 voxels (V = 1024: one; 2048 at N = 1024: two)
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   double2* sx = (double2*)(sc + 3 * CS);
   double2* sxn = (double2*)((unsigned char*)sx + K::XM);
   uint8_t* sh = (uint8_t*)((unsigned char*)sxn + K::XN);
-  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
   for (int j = t; j < Cfg<N>::TWN; j += T) tw[j] = B.tw[j];
   const double alpha = ctrl->alpha, b = ctrl->b;
   const double inv_bs = 1.0 / (b + alpha);  // solid divisor of pure.py:61
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
   constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
   const int TPC = (SL ? B.nl : N) * N / R;
   const int NT = 3 * TPC;
-  constexpr int SPR = N / 32;
+
   static_assert(T % 32 == 0, "segment bases are per warp");
   constexpr int SG = V / 1024;  // segment-base groups (see k_rs_compact)
   if (V != 1024 && V != 2048) return;  // (never launched otherwise)
