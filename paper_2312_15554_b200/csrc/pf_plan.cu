@@ -164,6 +164,10 @@ int plan_ensure_scratch(pf_plan* p) {
   return PF_OK;
 }
 
+#ifndef PF_GRAPH_ITERS_LARGE
+#define PF_GRAPH_ITERS_LARGE 4  // iterations per graph chunk for grids of >= 2^21 points
+#endif
+
 // Run up to n_iter iterations of the active solver in CUDA-graph chunks.
 // Every kernel of an iteration is gated on ctrl->done, so chunks launched
 // after convergence are no-ops apart from cuFFT passes on scratch buffers.
@@ -175,7 +179,7 @@ int run_chunks(pf_plan* p, int64_t n_iter, int poll, int (*enqueue)(pf_plan*), C
     return PF_OK;
   }
   const int64_t nr = p->g.nr;
-  const int K = nr >= (1 << 21) ? 4 : (nr >= (1 << 15) ? 8 : 16);
+  const int K = nr >= (1 << 21) ? PF_GRAPH_ITERS_LARGE : (nr >= (1 << 15) ? 8 : 16);
   if (!p->graph.exec || p->graph.iters != K) {
     p->graph.reset();
     PF_CK_CUDA(cudaStreamBeginCapture(p->work, cudaStreamCaptureModeThreadLocal));
