@@ -408,6 +408,10 @@ class FusedSlabStokes(SlabStokes):
             self._free_buffers()
             be.release_transforms()
             self._swap(self.Yx, self.Yxn, self.Yy, self.Yyn)
+        if self.p2p:
+            # the first PK stores into the peers' Yx: every rank's setup writes to
+            # its own Y buffers (cold-start zeroing, the swap's reads) come first
+            self.dist.p2p_barrier()
         self.it = 0
         return self
 
