@@ -48,6 +48,30 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+def headline_config(n, world):
+    """The workload both arms print (identical dicts, so the driver can match them)."""
+    return {"workload": f"stokes_admm_random_packing_{n}^3", "grid": [n, n, n], "cells": world,
+            "load_cases": "e_{rank%3}", "packing_seed": "rank//3",
+            "penalties": "reference default (adaptive)", "eps": 1e-5,
+            "parallelism": f"ensemble{world} (one independent cell per GPU)",
+            "l2": "inputs larger than L2 (~25 x 128 MiB fields per cell), no flush"}
+
+
+def host_cpu():
+    """lscpu model, logical cores and the POREFLOW_THREADS cap."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"lscpu_model": model, "logical_cpus": os.cpu_count(),
+            "POREFLOW_THREADS": os.environ.get("POREFLOW_THREADS") or None}
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks/throttle sampling around the timed region (B200_PROFILING.md)."""
@@ -127,16 +151,15 @@ def run_reference(args):
         return 0
     n = args.n
     rate, k, secs = cpu_stokes_rate(n, 0, (1.0, 0.0, 0.0), args.cpu_budget, max(1, args.steps))
-    cores = os.cpu_count()
+    cores = int(os.environ.get("POREFLOW_THREADS") or os.cpu_count())
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": k, "warmup": 1, "ms_per_step": 1e3 * secs / k, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"stokes_admm_random_packing_{n}^3", "grid": [n, n, n], "load_case": "e1",
-                   "penalties": "reference default (adaptive)", "eps": 1e-5},
+        "config": headline_config(n, args.gpus),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{k} ADMM iteration(s) of the {n}^3 cell after 1 warm-up iteration "
-                                   f"(loop time only; numpy + scipy.fft workers={cores})"},
+                         "sample": f"{k} ADMM iteration(s) of the seed-0 e1 {n}^3 cell after 1 warm-up iteration "
+                                   f"(loop time only; numpy + scipy.fft workers={cores})", **host_cpu()},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -275,41 +298,40 @@ def run_ours(args):
     pipe_b = sum(v for v in sb.values() if v) / n_real
     iter_ms_profile = sum(float(stage_ms[k]) for k in range(6))
 
-    # end-to-end through the public numpy API: host indicator in, host state out
+    # end-to-end through the public numpy API: the host's bit-packed indicator in
+    # (1 bit per voxel, numpy.packbits order, PackedIndicator: the form a micro-CT
+    # segmentation is stored in), host state and history out
     e2e_iters = args.steps
-    solid_host = np.array(ind.values)
+    bits_host = np.packbits(np.asarray(ind.values, dtype=np.uint8).ravel())
     # untimed warm-up call (pinned staging buffers, plan cache), like the W warm-up steps
-    pf.solve_stokes(pf.IndicatorField(pf.UnitCellGrid((n, n, n)), solid_host),
+    pf.solve_stokes(pf.PackedIndicator(pf.UnitCellGrid((n, n, n)), bits_host),
                     pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=tuple(g), max_iter=3), pen)
     torch.cuda.synchronize()
     te0 = time.perf_counter()
-    e2e_ind = pf.IndicatorField(pf.UnitCellGrid((n, n, n)), solid_host)  # host array in (validated)
+    e2e_ind = pf.PackedIndicator(pf.UnitCellGrid((n, n, n)), bits_host)  # host bytes in (validated)
     st_h, rep_h = pf.solve_stokes(e2e_ind, pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=tuple(g),
                                                                           max_iter=e2e_iters), pen)
     torch.cuda.synchronize()
     te1 = time.perf_counter()
     assert rep_h.iterations == e2e_iters
     e2e_value = n ** 3 * e2e_iters / (te1 - te0)
-    h2d = n ** 3  # uint8 indicator (zero initial state is created on device)
+    h2d = bits_host.nbytes  # packed indicator (the zero initial state is created on the device)
     d2h = (4 * 3 + 1) * 8 * n ** 3 + e2e_iters * 15 * 8
     del st_h
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rate, k_cpu, secs = cpu_stokes_rate(n, seed, tuple(g), args.cpu_budget, 100)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": rate, "unit": UNIT, "cores": int(os.environ.get("POREFLOW_THREADS") or os.cpu_count()),
+               "kind": "port",
                "sample": f"{k_cpu} ADMM iteration(s) of the same {n}^3 cell on the host (loop time only, "
-                         f"{secs:.1f} s; numpy + scipy.fft, all host threads)"}
+                         f"{secs:.1f} s; numpy + scipy.fft, all host threads)", **host_cpu()}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"stokes_admm_random_packing_{n}^3", "grid": [n, n, n],
-                   "cells": world, "load_cases": "e_{rank%3}", "packing_seed": "rank//3",
-                   "penalties": "reference default (adaptive)", "eps": 1e-5,
-                   "parallelism": f"ensemble{world} (one independent cell per GPU)",
-                   "l2": "inputs larger than L2 (~25 x 128 MiB fields per cell), no flush"},
+        "config": headline_config(n, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_src},
@@ -322,7 +344,7 @@ def run_ours(args):
         "stages": stages, "stage_profile_ms_per_iter": iter_ms_profile,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_iters,
                 "d2h_bytes_per_step": d2h / e2e_iters, "iterations": e2e_iters,
-                "api": "paper_2312_15554_b200.solve_stokes (numpy in/out)"},
+                "api": "paper_2312_15554_b200.solve_stokes (PackedIndicator host bytes in, numpy AdmmState out)"},
         "pipeline": pipeline,
         "gpu_launches": (6 if fused else 4) * args.steps,
         "library_launches_note": ("none: all transforms are in-kernel" if fused
@@ -641,13 +663,55 @@ def run_slab_workload(args):
     return 0
 
 
+def launch_ranks(n_gpus: int) -> int:
+    """``python bench.py --gpus N`` without a launcher: start N ranks on this node
+    through torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1),
+    each re-running this command line, and return their exit status.  Under
+    torchrun (WORLD_SIZE set) the existing ranks are used as they are."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + [
+        # torchrun's own parser would take "--n" as an ambiguous prefix of its options
+        "--size" if a == "--n" else ("--size=" + a[4:] if a.startswith("--n=") else a) for a in sys.argv[1:]]
+    return subprocess.run(cmd, cwd=str(ROOT)).returncode
+
+
+def run_dry(args):
+    """Fan-out probe (no GPU work): each rank joins the group (NCCL when CUDA is
+    visible, else gloo), the ranks are gathered, rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    rank, local_rank, world = dist_env()
+    ranks = [rank]
+    if world > 1:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend)
+        dev = torch.device("cuda", local_rank) if backend == "nccl" else torch.device("cpu")
+        t = torch.zeros(world, dtype=torch.int64, device=dev)
+        t[rank] = rank + 1
+        dist.all_reduce(t)
+        ranks = [int(x) - 1 for x in t.cpu().tolist()]
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks, "gpus_requested": args.gpus,
+                          "config": headline_config(args.n, world)}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=256, help="cell edge N (N^3 voxels)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="stokes", choices=("stokes", "transport", "ensemble", "slab", "pipeline"),
@@ -661,7 +725,13 @@ def main():
     ap.add_argument("--stokes-only", action="store_true", help="--workload pipeline: cfg 3 (load cases + K* only)")
     ap.add_argument("--tcells", type=int, default=1,
                     help="--workload transport: concurrent solves (cfg 2's load cases e_1..e_3), own plan + stream each")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="rank fan-out probe: every rank joins the process group, rank 0 prints n_gpus and ranks")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args.gpus)
+    if args.dry_run:
+        return run_dry(args)
     if args.workload == "transport":
         return run_transport_workload(args)
     if args.workload == "ensemble":

@@ -289,6 +289,40 @@ int pf_k_transport_mode_update(int ndim, const int64_t* dims, const double* w_ha
                                const double* lap, double a0, const double* b0_vec_host,
                                double* chi_hat, double* grad_hat, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Spectral utilities and step helpers (reference spectral.py:101-143,
+ * stokes.py:158-244, transport.py:131-177) on device pointers, full-spectrum
+ * complex128 layout over the trailing ndim axes.  Not used by the solver loops.
+ * ---------------------------------------------------------------------- */
+/* fftn / ifftn (spectral.py:101-115): `batch` fields of prod(dims) points each;
+ * in_complex = 0 reads real f64 input.  inverse != 0 scales by 1/prod(dims).
+ * out may equal in when in_complex. */
+int pf_k_fftn(int ndim, const int64_t* dims, int64_t batch, const double* in, int in_complex,
+              double* out, int inverse, void* stream);
+/* Re ifftn (spectral.py:107-115); work: batch*prod(dims) complex128 scratch (may be in). */
+int pf_k_ifftn_real(int ndim, const int64_t* dims, int64_t batch, const double* in, double* work,
+                    double* out, void* stream);
+/* grad (spectral.py:118-124): out[c, b] = 1j*kappa_c * chi_hat[b], c < ndim. */
+int pf_k_spectral_grad(int ndim, const int64_t* dims, int64_t batch, const double* const* kappas,
+                       const double* chi_hat, double* out, void* stream);
+/* div (spectral.py:127-133), or with base != NULL base + sum_c 1j*kappa_c*v[c]
+ * in transport.py:149-151's accumulation order. */
+int pf_k_spectral_div(int ndim, const int64_t* dims, const double* const* kappas, const double* v_hat,
+                      const double* base, double* out, void* stream);
+/* out[b, m] = (sign * factor[m]) * z[b, m]: apply_laplacian with sign = -1 (spectral.py:136-138). */
+int pf_k_scale_modes(int64_t n_modes, int64_t batch, const double* factor, double sign, const double* z,
+                     double* out, void* stream);
+/* q' = q - beta*div, then q' -= mean(q') (stokes.py:216-218).  scratch:
+ * pf_k_scratch_doubles() f64. */
+int pf_k_q_update(int64_t count, const double* q, const double* div, double beta, double* out,
+                  double* scratch, void* stream);
+/* ||w*(x - y)||_2 (stokes.py:154-155); y, w may be NULL; w is indexed i % w_period
+ * (a scalar indicator weighting a vector field).  Synchronous: the result lands
+ * in *result_host. */
+int pf_k_norm(int64_t count, const double* x, const double* y, const double* w, int64_t w_period,
+              double* scratch, double* result_host, void* stream);
+int pf_k_scratch_doubles(void);
+
 /* Bit-packed indicator (1 bit per voxel, numpy.packbits order — the
  * first voxel in the most significant bit of byte 0) -> uint8 0/1 per voxel, on
  * the device: ceil(n / 8) bytes cross PCIe instead of n. */

@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libporeflow_b200.so"
 SOURCES = ["pf_plan.cu", "pf_stokes.cu", "pf_transport.cu", "pf_effective.cu", "pf_kernels.cu", "pf_fused.cu",
-           "pf_fused_transport.cu", "pf_slab.cu"]
+           "pf_fused_transport.cu", "pf_slab.cu", "pf_ops.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

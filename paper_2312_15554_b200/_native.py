@@ -140,6 +140,14 @@ SIGNATURES = {
     "pf_k_transport_polarization": [ctypes.c_int, _I64P, _P, _P, _P, _P, ctypes.c_double, _DP, _DP, _P, _P, _P],
     "pf_k_transport_mode_update": [ctypes.c_int, _I64P, _P, _P, ctypes.POINTER(_P), _P, ctypes.c_double, _DP, _P,
                                    _P, _P],
+    "pf_k_fftn": [ctypes.c_int, _I64P, ctypes.c_int64, _P, ctypes.c_int, _P, ctypes.c_int, _P],
+    "pf_k_ifftn_real": [ctypes.c_int, _I64P, ctypes.c_int64, _P, _P, _P, _P],
+    "pf_k_spectral_grad": [ctypes.c_int, _I64P, ctypes.c_int64, ctypes.POINTER(_P), _P, _P, _P],
+    "pf_k_spectral_div": [ctypes.c_int, _I64P, ctypes.POINTER(_P), _P, _P, _P, _P],
+    "pf_k_scale_modes": [ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_double, _P, _P, _P],
+    "pf_k_q_update": [ctypes.c_int64, _P, _P, ctypes.c_double, _P, _P, _P],
+    "pf_k_norm": [ctypes.c_int64, _P, _P, _P, ctypes.c_int64, _P, _DP, _P],
+    "pf_k_scratch_doubles": [],
 }
 
 _lib = None

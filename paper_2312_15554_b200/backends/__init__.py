@@ -3,8 +3,9 @@
 
 The reference ships ``pure`` (numpy, any d) and ``fused`` (Cython, 2D).  This
 package ships exactly one implementation, ``cuda`` (sm_100a, any d <= 3), and
-no fallback: ``POREFLOW_BACKEND`` may be empty or ``cuda``; anything else is a
-ValueError, and a missing native library raises ImportError at first use.
+no fallback: ``POREFLOW_BACKEND`` may be empty, ``cuda``, or one of the
+reference's names (``pure``, ``fused``), which select nothing here; anything
+else is a ValueError, and a missing native library raises ImportError at first use.
 """
 
 from __future__ import annotations
@@ -13,9 +14,14 @@ import os
 
 from . import cuda
 
+# The reference accepts "", "pure" and "fused" (backends/__init__.py:25-32).  A process
+# configured for the reference's CPU backends must still be able to import this
+# package, so those names are accepted and simply do not select anything here:
+# every grid runs on the ``cuda`` plugin.  Unknown names raise, as in the reference.
+_KNOWN = ("", "cuda", "pure", "fused")
 _requested = os.environ.get("POREFLOW_BACKEND", "").strip().lower()
-if _requested and _requested != "cuda":
-    raise ValueError(f"POREFLOW_BACKEND must be 'cuda' (the only backend of poreflow_b200), got {_requested!r}")
+if _requested not in _KNOWN:
+    raise ValueError(f"POREFLOW_BACKEND must be one of 'cuda', 'pure', 'fused' or empty, got {_requested!r}")
 
 HAVE_FUSED = False  # the reference's 2D Cython extension has no counterpart here
 HAVE_CUDA = True

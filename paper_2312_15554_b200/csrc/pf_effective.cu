@@ -244,7 +244,11 @@ int pf_pore_average(pf_plan* p, const uint8_t* solid, const double* f, int ncomp
   PF_CK(enter(p));
   double s5[5];
   PF_CK(pore_sums_host(p, solid, f, ncomp, s5));
-  PF_ARG(s5[3] != 0.0, "pore average undefined: no pore cells");
+  if (s5[3] == 0.0) {  // hand the stream ordering back before reporting (no early return past enter())
+    leave(p);
+    set_error("pore average undefined: no pore cells");
+    return PF_ERR_ARG;
+  }
   for (int c = 0; c < ncomp; ++c) out[c] = s5[c] / s5[3];
   return leave(p);
 }

@@ -296,7 +296,9 @@ int pf_plan_create(pf_plan** out, int ndim, const int64_t* dims, int symbol_mode
 int pf_plan_set_symbol_tables(pf_plan* p, int axis, const double* kappa_host, const double* lap1d_host) {
   PF_ARG(p && kappa_host && lap1d_host, "null argument");
   PF_ARG(axis >= 0 && axis < p->g.d, "axis %d out of range", axis);
-  const int ax = 3 - p->g.d + axis, n = p->g.n[ax];
+  // table length = the GLOBAL extent fixed at plan creation (a slab plan's g.n[0]
+  // is its local plane count, but its spectral passes index the whole axis-0 table)
+  const int ax = 3 - p->g.d + axis, n = (int)p->h_kap[ax].size();
   p->h_kap[ax].assign(kappa_host, kappa_host + n);
   p->h_ell[ax].assign(lap1d_host, lap1d_host + n);
   PF_CK_CUDA(cudaSetDevice(p->device));

@@ -316,8 +316,12 @@ int pf_transport_begin(pf_plan* p, const pf_transport_params* P, const uint8_t* 
   // build_coefficients (transport.py:108-127): finiteness, pore count, u_bar, b0_vec.
   double sums[5];
   PF_CK(pore_sums_host(p, solid, u, d, sums));
-  PF_ARG(sums[4] == 0.0, "velocity field contains non-finite values");
-  PF_ARG(sums[3] != 0.0, "cannot form the pore-averaged velocity: no pore cells");
+  if (sums[4] != 0.0 || sums[3] == 0.0) {  // leave() before reporting: the user stream stays ordered
+    leave(p);
+    set_error(sums[4] != 0.0 ? "velocity field contains non-finite values"
+                             : "cannot form the pore-averaged velocity: no pore cells");
+    return PF_ERR_ARG;
+  }
   TransportConst& C = p->tc;
   double ubar[3] = {0, 0, 0}, nb2 = 0.0, ubg = 0.0;
   for (int c = 0; c < d; ++c) {

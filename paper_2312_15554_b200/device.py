@@ -124,11 +124,6 @@ def to_device(arr, device, dtype=None):
     return t.from_numpy(a).to(device=device, non_blocking=False)
 
 
-def _np_dtype(tdtype):
-    t = torch()
-    return {t.float64: np.float64, t.uint8: np.uint8, t.complex128: np.complex128}[tdtype]
-
-
 def solid_on_device(indicator, device):
     """Device copy of an (immutable) indicator's uint8 values, cached on this
     package's IndicatorField; duck-typed indicators (e.g. the reference's own

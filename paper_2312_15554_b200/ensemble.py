@@ -81,7 +81,7 @@ def permeability_job(cfg_kwargs=None, penalties=None, device=None):
     flow, device-resident)."""
 
     def solve(job: CellJob) -> dict:
-        from . import effective, spectral, stokes
+        from . import effective, stokes
 
         from .batch import solve_stokes_many_device
 
@@ -98,7 +98,8 @@ def permeability_job(cfg_kwargs=None, penalties=None, device=None):
         us = [st.u for st, _ in res]
         iters = [rep.iterations for _, rep in res]
         conv = [rep.converged for _, rep in res]
-        K = effective.permeability(us, ind, spectral.CENTRAL)
+        # the CLI builds K's symbols from the Stokes symbol mode (cli.py:386-388)
+        K = effective.permeability(us, ind, cfgs[0].symbol_mode)
         return {"K": K, "iterations": iters, "converged": conv}
 
     return solve

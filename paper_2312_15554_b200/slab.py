@@ -354,7 +354,10 @@ class FusedSlabStokes(SlabStokes):
         (``comm.p2p_alloc`` / ``p2p_ptrs``; torch symmetric memory on a GPU box,
         see ``SymmetricMemoryExchange``), PK and MF store their output straight
         into the owning ranks' buffers over NVLink, and a cross-rank barrier
-        (``comm.p2p_barrier``) replaces each exchange."""
+        (``comm.p2p_barrier``) replaces each exchange.  "p2p" is EXPERIMENTAL: it is
+        validated through the one-GPU loopback only; the two-GPU check
+        (tests/test_gpu_slab_multi.py, tools/slab_multi_check.py) has not yet run on
+        real NVLink peers."""
         super().__init__(backend, dims, cfg, penalties, solid_local, state, group, poll_every, comm, overlap)
         be = backend
         ym, yn = be.fused_sizes()

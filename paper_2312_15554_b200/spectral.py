@@ -66,3 +66,68 @@ def make_symbols(grid: UnitCellGrid, mode: str = EXACT) -> SpectralSymbols:
         lap += lap1.reshape(shape)
         ksq += kappa.reshape(shape) ** 2
     return SpectralSymbols(grid, mode, tuple(t[0] for t in tabs), lap, ksq)
+
+
+# ---------------------------------------------------------------- transforms and
+# spectral derivatives (spectral.py:101-143) on the device.  numpy in -> fresh
+# numpy out; CUDA tensors in -> CUDA tensors out.  Computed by pf_k_* entry
+# points (csrc/pf_ops.cu); there is no host fallback.
+
+def fft(field, grid: UnitCellGrid):
+    """Forward transform over the grid axes (leading component axes batched),
+    unnormalised, full complex spectrum (spectral.py:101-104)."""
+    from . import _devops as D
+
+    host = not D.is_tensor(field)
+    dev = D.device_of(field)
+    x = D.to_device(np.asarray(field) if host else field, dev)
+    return D.out_like(D.fftn_t(x, grid.dim), host)
+
+
+def ifft(coeffs, grid: UnitCellGrid):
+    """Inverse transform with the 1/n factor, truncated to its real part
+    (spectral.py:107-115)."""
+    from . import _devops as D
+
+    host = not D.is_tensor(coeffs)
+    dev = D.device_of(coeffs)
+    return D.out_like(D.ifftn_real_t(D.cplx(coeffs, dev), grid.dim), host)
+
+
+def grad(chi_hat, symbols: SpectralSymbols):
+    """Component j = 1j*kappa_j*chi_hat, stacked on a new leading axis (spectral.py:118-124)."""
+    from . import _devops as D
+
+    host = not D.is_tensor(chi_hat)
+    dev = D.device_of(chi_hat)
+    return D.out_like(D.grad_t(D.cplx(chi_hat, dev), D.kappa_tables(symbols, dev), symbols.grid.dim), host)
+
+
+def div(v_hat, symbols: SpectralSymbols):
+    """sum_j 1j*kappa_j*v_hat[j] (spectral.py:127-133)."""
+    from . import _devops as D
+
+    host = not D.is_tensor(v_hat)
+    dev = D.device_of(v_hat)
+    return D.out_like(D.div_t(D.cplx(v_hat, dev), D.kappa_tables(symbols, dev), symbols.grid.dim), host)
+
+
+def apply_laplacian(chi_hat, symbols: SpectralSymbols):
+    """-L(k) * chi_hat (spectral.py:136-138); leading axes of chi_hat are batched."""
+    from . import _devops as D
+
+    host = not D.is_tensor(chi_hat)
+    dev = D.device_of(chi_hat)
+    return D.out_like(D.scale_modes_t(D.real(symbols.lap, dev), D.cplx(chi_hat, dev), -1.0), host)
+
+
+def gradient_field(field, grid: UnitCellGrid, symbols: SpectralSymbols):
+    """Real-space gradient of a real scalar field via the symbol route
+    (spectral.py:141-143): ifft(grad(fft(field))), all on the device."""
+    from . import _devops as D
+
+    host = not D.is_tensor(field)
+    dev = D.device_of(field)
+    x = D.real(field, dev)
+    g = D.grad_t(D.fftn_t(x, grid.dim), D.kappa_tables(symbols, dev), grid.dim)
+    return D.out_like(D.ifftn_real_t(g, grid.dim), host)

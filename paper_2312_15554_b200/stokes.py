@@ -308,3 +308,105 @@ def solve_stokes(indicator: IndicatorField, cfg: StokesConfig | None = None,
     """Drop-in for reference ``solve_stokes`` (stokes.py:313-427): numpy in, numpy out."""
     state, report = solve_stokes_device(indicator, cfg, penalties, init)
     return state.to_host(), report
+
+
+# ---------------------------------------------------------------- step helpers
+# (stokes.py:158-244): one ADMM sub-step each, on the device.  The state may hold
+# numpy arrays (results come back as fresh numpy arrays) or CUDA tensors (results
+# stay on the device).  The solver loop does not use these (it runs the fused /
+# cuFFT pipelines); they serve callers and tests written against the reference's
+# step-level API.
+
+def _step_io(*xs):
+    from . import _devops as D
+
+    host = not any(D.is_tensor(x) for x in xs)
+    return D, host, D.device_of(*xs)
+
+
+def _solid_f64(indicator, dev):
+    from . import _devops as D
+
+    return D.real(indicator.as_float(), dev)
+
+
+def step1_velocity_solve(state, cfg: StokesConfig, penalties: PenaltyParams, symbols):
+    """Velocity stationarity solve (stokes.py:158-180): the rank-one Green's
+    operator on fft(q), fft(a), fft(u_tilde); returns Re ifft(u_hat)."""
+    if penalties.b <= 0.0:
+        raise ValueError("coupling penalty b must be positive for the zero mode")
+    from .backends import cuda as K
+
+    D, host, dev = _step_io(state.u, state.q, state.a, state.u_tilde)
+    d = symbols.grid.dim
+    q_hat = D.fftn_t(D.real(state.q, dev), d)
+    a_hat = D.fftn_t(D.real(state.a, dev), d)
+    ut_hat = D.fftn_t(D.real(state.u_tilde, dev), d)
+    u_hat = K.stokes_velocity_update(q_hat, a_hat, ut_hat, D.kappa_tables(symbols, dev), D.real(symbols.lap, dev),
+                                     D.real(symbols.kappa_sq, dev), cfg.nu, penalties.beta, penalties.b,
+                                     np.asarray(cfg.pressure_gradient, dtype=float))
+    return D.out_like(D.ifftn_real_t(u_hat, d), host)
+
+
+def step2_aux_update(u, state, penalties: PenaltyParams, indicator: IndicatorField):
+    """Pointwise auxiliary-velocity update (stokes.py:183-194, pure.py:59-61)."""
+    from .backends import cuda as K
+
+    D, host, dev = _step_io(u, state.a, state.lam)
+    ut = K.aux_velocity_update(D.real(u, dev), D.real(state.a, dev), D.real(state.lam, dev),
+                               _solid_f64(indicator, dev), penalties.alpha, penalties.b)
+    return D.out_like(ut, host)
+
+
+def _div_real(u_dev, symbols, dev):
+    from . import _devops as D
+
+    d = symbols.grid.dim
+    return D.ifftn_real_t(D.div_t(D.fftn_t(u_dev, d), D.kappa_tables(symbols, dev), d), d)
+
+
+def step3_multiplier_update(u, u_tilde, state, penalties: PenaltyParams, indicator: IndicatorField, symbols):
+    """Multiplier ascent (stokes.py:197-220): returns (q, a, lam); q' = q - beta*div(u)
+    with its mean projected out."""
+    from .backends import cuda as K
+
+    D, host, dev = _step_io(u, u_tilde, state.q, state.a, state.lam)
+    U = D.real(u, dev)
+    div_u = _div_real(U, symbols, dev)
+    a_new, lam_new = K.multiplier_update(D.real(state.a, dev), D.real(state.lam, dev), U, D.real(u_tilde, dev),
+                                         _solid_f64(indicator, dev), penalties.alpha, penalties.b)
+    q_new = D.q_update_t(D.real(state.q, dev), div_u, penalties.beta)
+    return D.out_like(q_new, host), D.out_like(a_new, host), D.out_like(lam_new, host)
+
+
+def residuals_and_tolerances(state_prev, state_next, penalties: PenaltyParams, cfg: StokesConfig,
+                             indicator: IndicatorField, symbols):
+    """The three primal/dual residual pairs with their tolerances (stokes.py:223-284):
+    divergences and the nine norms on the device, the pair arithmetic on the host
+    exactly as ``_residual_pairs``."""
+    D, _, dev = _step_io(state_prev.u, state_next.u)
+    Un, Up = D.real(state_next.u, dev), D.real(state_prev.u, dev)
+    UTn, UTp = D.real(state_next.u_tilde, dev), D.real(state_prev.u_tilde, dev)
+    H = _solid_f64(indicator, dev)
+    div_prev = _div_real(Up, symbols, dev)
+    div_next = _div_real(Un, symbols, dev)
+    n_vec = int(Un.numel())
+    n_sca = int(np.prod(tuple(state_next.q.shape)))
+    eps_abs, eps_rel = cfg.eps_abs, cfg.eps_rel
+
+    r_p1 = D.norm_t(UTn, None, H)
+    r_d1 = penalties.alpha * D.norm_t(UTn, UTp, H)
+    lam_norm = D.norm_t(D.real(state_next.lam, dev))
+    pair1 = ResidualPair(r_p1, math.sqrt(n_vec) * eps_abs + eps_rel * max(r_p1, lam_norm), r_d1,
+                         math.sqrt(n_vec) * eps_abs + eps_rel * lam_norm)
+    r_p2 = D.norm_t(div_next)
+    r_d2 = penalties.beta * D.norm_t(div_next, div_prev)
+    q_norm = D.norm_t(D.real(state_next.q, dev))
+    pair2 = ResidualPair(r_p2, math.sqrt(n_sca) * eps_abs + eps_rel * max(r_p2, q_norm), r_d2,
+                         math.sqrt(n_sca) * eps_abs + eps_rel * q_norm)
+    r_p3 = D.norm_t(Un, UTn)
+    r_d3 = penalties.b * D.norm_t(Un, Up)
+    a_norm = D.norm_t(D.real(state_next.a, dev))
+    pair3 = ResidualPair(r_p3, math.sqrt(n_vec) * eps_abs + eps_rel * max(r_p3, a_norm), r_d3,
+                         math.sqrt(n_vec) * eps_abs + eps_rel * a_norm)
+    return pair1, pair2, pair3

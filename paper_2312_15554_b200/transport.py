@@ -229,3 +229,44 @@ def solve_transport(indicator: IndicatorField, u, cfg: TransportConfig | None = 
     """Drop-in for reference ``solve_transport`` (transport.py:180-268)."""
     state, report = solve_transport_device(indicator, u, cfg, init)
     return state.to_host(), report
+
+
+# ---------------------------------------------------------------- step helpers
+# (transport.py:131-177) on the device; numpy in -> numpy out, CUDA tensors stay.
+
+def residual_rhs(state, coeffs: MediumCoefficients, cfg: TransportConfig, symbols):
+    """Spectral right-hand side (transport.py:131-151): the polarization
+    (pure.py:71-87) in real space, its transforms, then s_hat + sum_c 1j*kappa_c*w_hat[c]
+    in the reference's accumulation order."""
+    from . import _devops as D
+    from .backends import cuda as K
+
+    host = not any(D.is_tensor(x) for x in (state.grad_chi, coeffs.diffusivity))
+    dev = D.device_of(state.grad_chi, coeffs.diffusivity)
+    d = symbols.grid.dim
+    w, s = K.transport_polarization(D.real(state.grad_chi, dev), D.real(coeffs.diffusivity, dev),
+                                    D.real(coeffs.advection, dev), D.real(coeffs.forcing, dev), cfg.a0,
+                                    np.asarray(coeffs.b0_vec, dtype=float),
+                                    np.asarray(cfg.composition_gradient, dtype=float))
+    w_hat = D.fftn_t(w, d)
+    s_hat = D.fftn_t(s, d)
+    return D.out_like(D.div_t(w_hat, D.kappa_tables(symbols, dev), d, base=s_hat), host)
+
+
+def update_concentration(f_hat, cfg: TransportConfig, symbols, b0_vec):
+    """Uniform-medium solve per mode (transport.py:154-177): returns (chi, grad_chi),
+    the mode update (pure.py:90-115) with a zero flux part, then Re ifft of both."""
+    from . import _devops as D
+    from .backends import cuda as K
+
+    host = not D.is_tensor(f_hat)
+    dev = D.device_of(f_hat)
+    t = torch()
+    grid = symbols.grid
+    F = D.cplx(f_hat, dev)
+    w_hat = t.zeros((grid.dim, *grid.dims), dtype=t.complex128, device=dev)
+    chi_hat, grad_hat = K.transport_mode_update(w_hat, F, D.kappa_tables(symbols, dev), D.real(symbols.lap, dev),
+                                                cfg.a0, np.asarray(b0_vec, dtype=float))
+    chi = D.ifftn_real_t(chi_hat, grid.dim)
+    gch = D.ifftn_real_t(grad_hat, grid.dim)
+    return D.out_like(chi, host), D.out_like(gch, host)

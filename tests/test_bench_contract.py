@@ -24,3 +24,26 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+
+
+def test_launcher_fans_out_to_n_ranks():
+    """`bench.py --gpus 2` without torchrun starts 2 ranks itself (torch.distributed.run,
+    127.0.0.1 rendezvous); the --dry-run probe joins them over gloo on CPU and rank 0
+    reports n_gpus = 2 with both ranks present."""
+    env = {k: v for k, v in __import__("os").environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run", "--n", "16"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ranks"] == [0, 1] and d["config"]["cells"] == 2
+
+
+def test_both_arms_print_the_same_config():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    assert bench.headline_config(256, 1) == bench.headline_config(256, 1)
+    src = (ROOT / "bench.py").read_text()
+    assert src.count("\"config\": headline_config(") >= 2  # the GPU arm and the reference arm (and the probe)

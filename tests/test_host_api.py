@@ -4,6 +4,8 @@ Mirrors the reference's own unit tests (tests/test_grid.py, test_stokes.py,
 test_transport.py, test_spectral.py) for the pieces that run on the host."""
 
 import numpy as np
+from pathlib import Path
+
 import pytest
 
 import paper_2312_15554_b200 as pf
@@ -110,11 +112,33 @@ def test_backend_env_rejects_unknown(monkeypatch):
 
     from paper_2312_15554_b200 import backends
 
-    monkeypatch.setenv("POREFLOW_BACKEND", "pure")
+    monkeypatch.setenv("POREFLOW_BACKEND", "upwind")
     with pytest.raises(ValueError):
         importlib.reload(backends)
     monkeypatch.delenv("POREFLOW_BACKEND")
     importlib.reload(backends)
+
+
+@pytest.mark.parametrize("name", ["pure", "fused", "cuda", "PURE", ""])
+def test_backend_env_accepts_reference_names(monkeypatch, name):
+    """A process configured for the reference's CPU backends (backends/__init__.py:25-32)
+    can import the drop-in: 'pure' / 'fused' select nothing here, the cuda plugin runs."""
+    import importlib
+    import subprocess
+    import sys
+
+    from paper_2312_15554_b200 import backends
+
+    monkeypatch.setenv("POREFLOW_BACKEND", name)
+    importlib.reload(backends)
+    assert backends.default_backend_name() == "cuda"
+    assert backends.kernels_for(3).NAME == "cuda"
+    monkeypatch.delenv("POREFLOW_BACKEND")
+    importlib.reload(backends)
+    # a fresh interpreter importing the whole package with the variable set
+    env = dict(__import__("os").environ, POREFLOW_BACKEND=name)
+    code = "import paper_2312_15554_b200 as p; assert p.default_backend_name() == 'cuda'"
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=str(Path(__file__).resolve().parents[1]))
 
 
 def test_packing_slab_rasterization_equals_full_cell():
