@@ -29,6 +29,7 @@
 // rank's x- / y-slab, with the transpose either by all_to_all between the passes
 // or fused into PK's / MF's stores to the owning ranks' buffers (Bufs::peers).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "pf_internal.cuh"
@@ -63,6 +64,15 @@
 #endif
 #ifndef PF_PK_MINB
 #define PF_PK_MINB 3  // __launch_bounds__ min blocks per SM for k_pk (1 lets ptxas take 216 regs: 2 blocks/SM, slower)
+#endif
+#ifndef PF_PK_PIPE
+#define PF_PK_PIPE 0  // N = 128 / 256 single GPU: persistent pipelined PK (measured slower: 0.37 vs 0.31 ms)
+#endif
+#ifndef PF_PK_TMASTORE
+#define PF_PK_TMASTORE 1  // k_pk stores Y with TMA tensor stores from its boxes (single GPU, N = 128/256)
+#endif
+#ifndef PF_YBLOCK
+#define PF_YBLOCK 1  // single GPU, N <= 256: i0-blocked Y layout (Bufs::yb; POREFLOW_B200_YBLOCK=0 disables)
 #endif
 #ifndef PF_PK_THREADS
 #define PF_PK_THREADS 128
@@ -103,6 +113,14 @@ __device__ __forceinline__ int swz16(int e) {
   return RB == 128 ? (e & 7) : (RB == 64 ? ((e >> 1) & 3) : (RB == 32 ? ((e >> 2) & 1) : 0));
 }
 
+// offset of Y main element (c, i0, k1, k2) on a single GPU (k1 < N, k2 < N/2)
+template <int N>
+__device__ __forceinline__ size_t ymain(int yb, int c, int i0, int k1, int k2) {
+  constexpr int H = N / 2;
+  return yb ? ((((size_t)(c * (N / 4) + (i0 >> 2)) * N + k1) * 4 + (i0 & 3)) * H + k2)
+            : (((size_t)(c * N + i0) * N + k1) * H + k2);
+}
+
 constexpr int kMaxRanks = 16;
 struct Peers {
   double2 *yy[kMaxRanks], *yyn[kMaxRanks];  // y-slab Y of each rank
@@ -134,6 +152,12 @@ struct Bufs {
   // the host encoded the TMA tensor maps of this layout (else the passes stage with
   // LDGSTS); tma_yx: the 5D x-slab map of MI too (its box spans l1 <= 256 rows)
   int tma, tma_yx;
+  // single GPU, N <= 256: Y main array i0-blocked by 4, [c][i0/4][k1][i0%4][k2] (yb = 1).
+  // PK's pencils then touch 4 consecutive i0 rows 2 KB apart instead of one 64-byte
+  // piece per 512 KB plane: a plain copy in PK's access pattern runs at 5.4 TB/s
+  // instead of 3.5 - 3.9, while the axis-1 passes' tiles (all k1 of one (c, i0)) keep
+  // 5.5 - 5.7 (tools/micro/layout_copy.cu, B200).  Slab layouts are unchanged (yb = 0).
+  int yb;
   // peer-memory exchange (slab, P2P-mapped Y buffers of every rank; null = exchange by
   // all_to_all): PK stores straight into the x-slab owners' Yx, MF into the y-slab
   // owners' Yy, so the transpose rides on the passes' own stores over NVLink
@@ -909,6 +933,7 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   // Y in the x-slab exchange layout [r][i0][c][k1 - r l1][k2], r = k1 / l1 (see Bufs)
   auto yoff_of = [&](int e, int q) -> size_t {
     const int r = e >> s1, kl = e & (l1 - 1);
+    if (!SL && !nyq && B.yb) return ymain<N>(1, c, i0, e, ch * CM + q);
     return nyq ? ((size_t)((r * l0 + i0b + q) * 3 + c)) * l1 + kl
                : (((size_t)((c * (N >> s1) + r) * l0 + i0)) * l1 + kl) * H + ch * CM + q;
   };
@@ -938,6 +963,14 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
             "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
             "%6}], [%7];" ::"r"(su32(S)),
             "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(0), "r"(i0), "r"(0), "r"(c), "r"(su32(&mbar))
+            : "memory");
+      } else if (!SL && INV && B.yb) {
+        // i0-blocked Y [c i0/4][k1][i0%4][k2]: a 4D box (2 CM doubles, 1, N rows k1, 1)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+            "%5}], [%6];" ::"r"(su32(S)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0), "r"(i0 & 3), "r"(0), "r"(c * (N / 4) + (i0 >> 2)),
+            "r"(su32(&mbar))
             : "memory");
       } else {
         const int y0 = (c * l0 + i0) * N;  // rows of [c][i0][e] (Y at P = 1, or X)
@@ -1105,7 +1138,8 @@ struct SpecArgs {
 
 template <int N, bool SL>
 __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl,
-                                                              const __grid_constant__ CUtensorMap tmap) {
+                                                              const __grid_constant__ CUtensorMap tmap, int tile0,
+                                                              int pbase, int nparts) {
   using C = Cfg<N>;
   using K = PK2<N>;
   constexpr int H = C::H, SS = K::SS, CP = K::CP, NCH = K::NCH, NSEQ = K::NSEQ, T = K::T;
@@ -1117,13 +1151,14 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
   double2* tw = (double2*)(reg + K::REGION);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const double beta = ctrl->beta, b = ctrl->b;
-  const int tile = blockIdx.x;
+  const int tile = tile0 + blockIdx.x;  // (tile0 > 0: the Nyquist tiles beside k_pk_pipe)
   const int l1 = (SL ? B.l1 : N);
   const bool nyq = tile >= l1 * NCH;
   const int k1 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;  // k1: local to the y-slab
   const int k1b = nyq ? (tile - l1 * NCH) * CP : 0;
   // Y in the y-slab exchange layout [i0][c][k1 - k1off][k2] (see Bufs)
   auto yoff = [&](int c, int i0, int q) -> size_t {
+    if (!SL && !nyq && B.yb) return ymain<N>(1, c, i0, k1, ch * CP + q);
     return nyq ? (size_t)(i0 * 3 + c) * l1 + k1b + q : ((size_t)(c * N + i0) * l1 + k1) * H + ch * CP + q;
   };
   constexpr bool TMA = K::TMA_OK && PF_PK_TMA;
@@ -1142,6 +1177,14 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
                 "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(k1), "r"(c * N + b * C::L),
                 "r"(su32(&mbar))
                 : "memory");
+      } else if (!SL && B.yb) {  // i0-blocked Y: 4D box (2 CP doubles, 4, 1, N / 4) -> rows in i0 order
+        for (int c = 0; c < 3; ++c)
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+              "%5}], [%6];" ::"r"(su32(reg + K::BOX_OFF + c * K::BOX)),
+              "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(0), "r"(k1), "r"(c * (N / 4)),
+              "r"(su32(&mbar))
+              : "memory");
       } else
       for (int c = 0; c < 3; ++c)
         asm volatile(
@@ -1302,6 +1345,48 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
     radix_stage<N, true>(S, NSEQ, SS, tw, t, T);
   }
   __syncthreads();
+#if PF_PK_TMASTORE
+  if (!SL && tma && C::M == 1) {
+    // Y out by TMA tensor stores: each component's results are repacked from the
+    // padded sequences into its (swizzled) box, last component first — box c only
+    // overlaps sequences of components >= c, already consumed — then one thread
+    // stores the three boxes and waits until they have been read from shared memory.
+    constexpr int PER = (CP * N + T - 1) / T;
+    for (int c = 2; c >= 0; --c) {
+      double2 v[PER];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int idx = t + T * j, q = idx % CP, i0 = idx / CP;
+        if (idx < CP * N) v[j] = S[(c * CP + q) * SS + C::sp(i0)];
+      }
+      __syncthreads();
+      unsigned char* box = reg + K::BOX_OFF + c * K::BOX;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int idx = t + T * j, q = idx % CP, i0 = idx / CP;
+        if (idx < CP * N)
+          *reinterpret_cast<double2*>(box + (size_t)i0 * K::ROWB + ((q ^ swz16<K::ROWB>(i0)) << 4)) = v[j];
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (t == 0) {
+      for (int c = 0; c < 3; ++c) {
+        if (B.yb)
+          asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tmap)),
+                       "r"(2 * ch * CP), "r"(0), "r"(k1), "r"(c * (N / 4)), "r"(su32(reg + K::BOX_OFF + c * K::BOX))
+                       : "memory");
+        else
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tmap)),
+                       "r"(2 * ch * CP), "r"(k1), "r"(c * N), "r"(su32(reg + K::BOX_OFF + c * K::BOX))
+                       : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  } else
+#endif
   for (int idx = t; idx < 3 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
     const size_t o = yoff(c, i0, q);
@@ -1317,7 +1402,226 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
   }
   block_sum<3>(acc);
   if (t == 0)
-    for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+    for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * nparts + pbase + blockIdx.x] = acc[k];
+#if PF_PK_TMASTORE
+  if (!SL && tma && C::M == 1 && t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+}
+
+// ------------------------------------------------------------------ PK, persistent pipelined
+// Single GPU, N = 128 / 256, main tiles (the Nyquist tiles stay on k_pk).  One CTA
+// per SM walks the tiles blockIdx.x, + gridDim.x, ... with a two-stage input ring:
+// a stage holds the tile's three component pencils (3D TMA boxes, as k_pk) and its
+// tile-major Q^ / D^ chunks (two 1D bulk copies), all completing on the stage's
+// mbarrier.  The loads of tile i + 2 are issued into stage i & 1 as soon as tile
+// i's spectral step has consumed it, so about one tile of reads is always in
+// flight while the SM transforms — the non-persistent k_pk is bound by its per-tile
+// load -> FFT -> spectral -> FFT -> store chain at 3 CTAs / SM.
+// 12 lane groups of 16 transform the 3 x CP = 12 sequences in one round per
+// direction; Q^' / D^ go out coalesced per thread, Y from the padded sequences.
+#ifndef PF_PKP_CP
+#define PF_PKP_CP 4  // columns per pipelined-PK work unit (2: half tiles, 96 threads, 2 CTAs / SM)
+#endif
+#ifndef PF_PKP_ABL
+#define PF_PKP_ABL 0  // measurement-only ablations (results invalid): 1 = no Y stores, 2 = no FFTs, 3 = no Q/D stores
+#endif
+#ifndef PF_PKP_W32
+#define PF_PKP_W32 0  // N = 256: one warp per sequence (fft256_w32) instead of a 16-lane group
+#endif
+template <int N>
+struct PKP {
+  using C = Cfg<N>;
+  static constexpr int CPT = PK2<N>::CP;     // the tile-major Q^ / D^ tiles of k_pk
+  static constexpr int CP = PF_PKP_CP;       // columns per work unit (a unit = CPT / CP of a tile)
+  static constexpr int SPT = CPT / CP;       // units per tile
+  static constexpr bool W32 = PF_PKP_W32 && N == 256;
+  static constexpr int NSEQ = 3 * CP;
+  static constexpr int LPS = W32 ? 32 : C::G;  // lanes per sequence
+  static constexpr int T = NSEQ * LPS;       // one lane group (or warp) per sequence
+  static constexpr int SS = PK2<N>::SS;
+  static constexpr int ROWB = CP * 16;
+  static constexpr size_t BOX = sizeof(double2) * CP * N;       // one component pencil
+  static constexpr size_t QD = sizeof(double2) * CP * N;        // one unit's Q^ or D^ chunk
+  static constexpr size_t STAGE = 3 * BOX + 2 * QD;
+  static constexpr uint32_t TX = (uint32_t)STAGE;
+  static constexpr int STAGES = 2;
+  static constexpr size_t REGION = sizeof(double2) * NSEQ * SS;
+  static constexpr size_t BYTES = 1024 + STAGES * STAGE + REGION + sizeof(double2) * C::TWN;
+  static constexpr int MAIN_TILES = N * PK2<N>::NCH;
+  static constexpr int UNITS = MAIN_TILES * SPT;
+  static_assert(C::M == 1, "pipelined PK: N <= 256");
+  static_assert(CPT % CP == 0 && (ROWB == 32 || ROWB == 64 || ROWB == 128), "pipelined PK unit shape");
+  static_assert(BOX % 1024 == 0 && QD % 1024 == 0, "stage members stay 1 KB aligned");
+};
+
+template <int N>
+__global__ void __launch_bounds__(PKP<N>::T, 1) k_pk_pipe(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl,
+                                                         const __grid_constant__ CUtensorMap tmap) {
+  using C = Cfg<N>;
+  using K = PKP<N>;
+  constexpr int H = C::H, SS = K::SS, CP = K::CP, CPT = K::CPT, SPT = K::SPT, NCH = PK2<N>::NCH, T = K::T;
+  constexpr int NU = K::UNITS, LPS = K::LPS;
+  pdl_wait();
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char ppraw[];
+  unsigned char* base = ppraw + ((1024 - (su32(ppraw) & 1023)) & 1023);  // 1 KB-aligned
+  unsigned char* stage0 = base;
+  double2* S = (double2*)(base + K::STAGES * K::STAGE);
+  double2* tw = (double2*)(base + K::STAGES * K::STAGE + K::REGION);
+  __shared__ uint64_t full[K::STAGES];
+  const int t = threadIdx.x, g = t / LPS, l = t % LPS;
+  const double beta = ctrl->beta, b = ctrl->b;
+
+  auto issue = [&](int unit, int s) {  // thread 0: the unit's pencils + Q^ / D^ chunks into stage s
+    unsigned char* st = stage0 + (size_t)s * K::STAGE;
+    const int tile = unit / SPT, half = unit % SPT;
+    const int k1 = tile / NCH, ch = tile % NCH;
+    fence_async_smem();
+    mbar_expect(&full[s], K::TX);
+    for (int c = 0; c < 3; ++c) {
+      if (B.yb)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+            "%5}], [%6];" ::"r"(su32(st + c * K::BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * (ch * CPT + half * CP)), "r"(0), "r"(k1),
+            "r"(c * (N / 4)), "r"(su32(&full[s]))
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(su32(st + c * K::BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * (ch * CPT + half * CP)), "r"(k1), "r"(c * N),
+            "r"(su32(&full[s]))
+            : "memory");
+    }
+    const size_t tb = (size_t)tile * CPT * N + (size_t)half * CP * N;
+    bulk_load(st + 3 * K::BOX, B.Q + tb, (uint32_t)K::QD, &full[s]);
+    bulk_load(st + 3 * K::BOX + K::QD, B.D + tb, (uint32_t)K::QD, &full[s]);
+  };
+
+  if (t == 0) {
+    for (int s = 0; s < K::STAGES; ++s) mbar_init(&full[s]);
+    for (int s = 0; s < K::STAGES; ++s) {
+      const int unit = blockIdx.x + s * gridDim.x;
+      if (unit < NU) issue(unit, s);
+    }
+  }
+  for (int j = t; j < C::TWN; j += T) tw[j] = B.tw[j];
+  __syncthreads();
+
+  double acc[3] = {0.0, 0.0, 0.0};
+  int it = 0;
+  for (int unit = blockIdx.x; unit < NU; unit += gridDim.x, ++it) {
+    const int s = it & 1;
+    const unsigned char* st = stage0 + (size_t)s * K::STAGE;
+    const double2* Qs = (const double2*)(st + 3 * K::BOX);
+    const double2* Ds = (const double2*)(st + 3 * K::BOX + K::QD);
+    const int tile = unit / SPT, half = unit % SPT;
+    const int k1 = tile / NCH, ch = tile % NCH;
+    const int col0 = ch * CPT + half * CP;  // first k2 column of the unit
+    mbar_wait(&full[s], (it >> 1) & 1);
+    {  // forward FFT_0, one sequence (c, q) per lane group / warp, pass-1 inputs straight from the box
+      const int cc = g / CP, q = g % CP;
+      const unsigned char* box = st + cc * K::BOX;
+      auto ld = [&](int e) {
+        return *reinterpret_cast<const double2*>(box + (size_t)e * K::ROWB + ((q ^ swz16<K::ROWB>(e)) << 4));
+      };
+      if constexpr (K::W32) {
+        const int j = l & 15, h = l >> 4;
+        double2 x[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[m] = ld(16 * (2 * m + h) + j);
+        fft256_w32_x<false>(x, S + g * SS, tw, l, true);
+      } else {
+        constexpr int A = C::A, BB = C::B;
+        double2 x[A > BB ? A : BB];
+        if (l < BB) {
+#pragma unroll
+          for (int n1 = 0; n1 < A; ++n1) x[n1] = ld(BB * n1 + l);
+        }
+#if PF_PKP_ABL == 2
+        if (l < BB)
+          for (int n1 = 0; n1 < A; ++n1) S[g * SS + C::pad(BB * n1 + l)] = x[n1];
+#else
+        fft_seq_x<N, false>(x, S + g * SS, tw, l, true);
+#endif
+      }
+    }
+    __syncthreads();
+    const size_t tbase = (size_t)tile * CPT * N + (size_t)half * CP * N;
+    for (int m = t; m < CP * N; m += T) {
+      const int q = m / N, k0 = m % N;
+      const int kk1 = k1, k2 = col0 + q;
+      const int idx3[3] = {k0, kk1, k2};
+      double kc[3];
+      double L = 0.0, ksq = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        kc[c] = __ldg(P.kap[c] + idx3[c]);
+        L = L + __ldg(P.ell[c] + idx3[c]);
+        ksq = ksq + kc[c] * kc[c];
+      }
+      const double2 qq = Qs[m];
+      const double2 dpj = Ds[m];
+      const bool zero = (k0 | kk1 | k2) == 0;
+      double2 r[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double2 rc = S[(c * CP + q) * SS + C::kp(k0)];
+        r[c] = make_double2(kc[c] * qq.y + rc.x, -(kc[c] * qq.x) + rc.y);  // -i k q + R^
+        if (zero) r[c].x = r[c].x + P.dn * P.g[c];                          // n g_p at k = 0
+      }
+      const double A = P.nu * L + b;
+      double2 kr = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) kr = cadd(kr, cscale(kc[c], r[c]));
+      const double Dn = A + beta * ksq;
+      const double rAD = 1.0 / (A * Dn);
+      const double f = beta * A * rAD;
+      const double2 corr = cscale(f, kr);
+      const double invA = Dn * rAD;
+      double2 dv = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double2 u = csub(r[c], cscale(kc[c], corr));
+        u = make_double2(u.x * invA, u.y * invA);
+        dv = cadd(dv, cik(kc[c], u));
+        S[(c * CP + q) * SS + C::kp(k0)] = make_double2(u.x * P.inv_n, u.y * P.inv_n);
+      }
+      double2 qn = csub(qq, cscale(beta, dv));
+      if (zero) qn = make_double2(0.0, 0.0);
+      const double w = (k2 == 0) ? 1.0 : 2.0;  // main tiles: k2 < N/2
+      acc[0] += w * cabs2(dv);
+      acc[1] += w * cabs2(csub(dv, dpj));
+      acc[2] += w * cabs2(qn);
+#if PF_PKP_ABL != 3
+      B.Q[tbase + m] = qn;
+      B.D[tbase + m] = dv;
+#endif
+    }
+    __syncthreads();  // stage s consumed: refill it with unit + 2 grid strides
+    if (t == 0) {
+      const int nxt = unit + K::STAGES * gridDim.x;
+      if (nxt < NU) issue(nxt, s);
+    }
+#if PF_PKP_ABL != 2
+    if constexpr (K::W32)
+      fft256_w32<true>(S + g * SS, tw, l, true);
+    else
+      fft_seq<N, true>(S + g * SS, tw, l, true);
+#endif
+    __syncthreads();
+#if PF_PKP_ABL != 1
+    for (int idx = t; idx < 3 * N * CP; idx += T) {
+      const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
+      B.Y[ymain<N>(B.yb, c, i0, k1, col0 + q)] = S[(c * CP + q) * SS + C::sp(i0)];
+    }
+#endif
+    __syncthreads();  // the next unit's forward pass overwrites S
+  }
+  block_sum<3>(acc);
+  if (t == 0)
+    for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * (gridDim.x + N / CPT) + blockIdx.x] = acc[k];
 }
 
 // natural full spectrum [k0][k1][N/2+1] <-> PK tile-major [tile][q][k0]
@@ -1361,8 +1665,12 @@ __global__ void k_split_yx(const double2* __restrict__ src, Bufs B) {
     rest /= N;
     const int i0 = (int)(rest % l0), c = (int)(rest / l0);
     const int r = k1 >> s1, kl = k1 & (l1 - 1);
-    if (k2 < H) B.Yx[(((int64_t)(c * (N >> s1) + r) * l0 + i0) * l1 + kl) * H + k2] = src[i];
-    else B.Yxn[((int64_t)(r * l0 + i0) * 3 + c) * l1 + kl] = src[i];
+    if (k2 < H) {
+      if (B.yb) B.Yx[ymain<N>(1, c, i0, k1, k2)] = src[i];  // single GPU, i0-blocked
+      else B.Yx[(((int64_t)(c * (N >> s1) + r) * l0 + i0) * l1 + kl) * H + k2] = src[i];
+    } else {
+      B.Yxn[((int64_t)(r * l0 + i0) * 3 + c) * l1 + kl] = src[i];
+    }
   }
 }
 
@@ -1404,11 +1712,14 @@ struct FusedPlan {
   int slab = 0;
   double lam_pore = 0.0;
   CUtensorMap tm_pk{};          // 3D map of Y for PK ([c i0][k1][k2] pencils)
+  CUtensorMap tm_pkp{};         // the same with the pipelined PK's unit width (PF_PKP_CP columns)
   CUtensorMap tm_y{}, tm_xr{};  // 2D maps of Y and XR ([c][i0][e] rows x N/2 columns) for the axis-1 TMA loads
   void* ws = nullptr;        // cuFFT work area of plan2d
   double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
   int nb_full = kSMs, nb_compact = kSMs;
   fz::Peers* peers = nullptr;  // device copy of the peer pointer table (P2P exchange)
+  int pk_pipe = 0;             // single GPU, N = 128 / 256: persistent pipelined PK (k_pk_pipe)
+  int nb_pkp = 0;              // its grid (resident CTAs)
 };
 
 static FusedPlan* fp_of(pf_plan* p) { return reinterpret_cast<FusedPlan*>(p->fused); }
@@ -1459,6 +1770,17 @@ static int set_attrs(FusedPlan* f) {
   int o1 = 0, o2 = 0;
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, fz::k_rs<N, false>, fz::RS2<N>::T, smem_rs<N>()));
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N, false>, fz::RS2<N>::T, smem_rsc<N>()));
+  if constexpr (N == 128 || N == 256) {
+    PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk_pipe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)fz::PKP<N>::BYTES));
+    int o3 = 0;
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, fz::k_pk_pipe<N>, fz::PKP<N>::T,
+                                                             fz::PKP<N>::BYTES));
+    f->nb_pkp = (o3 < 1 ? 1 : o3) * kSMs;
+    if (f->nb_pkp > fz::PKP<N>::UNITS) f->nb_pkp = fz::PKP<N>::UNITS;
+    const char* e = getenv("POREFLOW_B200_PK_PIPE");
+    f->pk_pipe = PF_PK_PIPE && !(e && e[0] == '0');
+  }
   f->nb_full = wave(o1, 3);
   f->nb_compact = wave(o2, kRsMaxBlocks / kSMs);
   f->nb_rs = f->nb_full;
@@ -1541,6 +1863,38 @@ static int encode_pk_map_gen(CUtensorMap* tm, const double2* base, int N, int cp
   return PF_OK;
 }
 
+// 4D tensor map of the i0-blocked Y [3 N/4 (c, i0/4)][N k1][4 (i0%4)][N/2 complex]:
+// box = (cols complex, bii, bk1, N/4 or 1 planes), swizzled by the box row width.
+// PK: (CP, 4, 1, N/4) = one component pencil in i0 order; MI: (CM, 1, N, 1) = one
+// (c, i0) tile in k1 order.
+static int encode_yb_map(CUtensorMap* tm, const double2* base, int N, int cols, int bii, int bk1) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PF_CK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return PF_ERR_CUDA;
+    }
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const int H = N / 2;
+  const cuuint64_t row = (cuuint64_t)H * sizeof(double2);
+  cuuint64_t gdim[4] = {(cuuint64_t)2 * H, 4, (cuuint64_t)N, (cuuint64_t)3 * N / 4};
+  cuuint64_t gstride[3] = {row, 4 * row, 4 * row * N};
+  cuuint32_t box[4] = {(cuuint32_t)2 * cols, (cuuint32_t)bii, (cuuint32_t)bk1, (cuuint32_t)(bii == 4 ? N / 4 : 1)};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, gdim, gstride, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cols * 16),
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+
 int fused_ensure(pf_plan* p) {
   if (p->fused) return PF_OK;
   const int N = p->g.n[0];
@@ -1596,12 +1950,23 @@ int fused_ensure(pf_plan* p) {
   }
   PF_CK_CUDA(cudaMemcpy(f->b.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   f->b.tma = 0;
+  {
+    const char* e = getenv("POREFLOW_B200_YBLOCK");
+    f->b.yb = (N <= 256 && PF_YBLOCK && !(e && e[0] == '0')) ? 1 : 0;
+  }
   if (N >= 128) {  // TMA maps (N > 256: M boxes of 256 rows per tile / component pencil)
     const int cm = N == 128 ? fz::M2<128>::CM : (N == 256 ? fz::M2<256>::CM : (N == 512 ? fz::M2<512>::CM : fz::M2<1024>::CM));
     const int cp = N == 128 ? fz::PK2<128>::CP : (N == 256 ? fz::PK2<256>::CP : (N == 512 ? fz::PK2<512>::CP : fz::PK2<1024>::CP));
-    PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
+    if (f->b.yb) {
+      PF_CK(encode_yb_map(&f->tm_y, f->b.Y, N, cm, 1, N));      // MI: (CM cols, 1, all k1, 1)
+      PF_CK(encode_yb_map(&f->tm_pk, f->b.Y, N, cp, 4, 1));     // PK: (CP cols, 4, 1, N/4)
+      PF_CK(encode_yb_map(&f->tm_pkp, f->b.Y, N, PF_PKP_CP, 4, 1));
+    } else {
+      PF_CK(encode_axis1_map(&f->tm_y, f->b.Y, N, cm, 3));
+      PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, cp, 3));
+      PF_CK(encode_pk_map(&f->tm_pkp, f->b.Y, N, PF_PKP_CP, 3));
+    }
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
-    PF_CK(encode_pk_map(&f->tm_pk, f->b.Y, N, cp, 3));
     f->b.tma = f->b.tma_yx = 1;
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
@@ -1792,6 +2157,17 @@ int fused_finish(pf_plan* p) {
 }
 
 template <int N>
+static cudaError_t launch_pk_pipe(pf_plan* p, FusedPlan* f, const fz::SpecArgs& sa) {
+  if constexpr (N == 128 || N == 256) {
+    return launch_k(fz::k_pk_pipe<N>, f->nb_pkp, fz::PKP<N>::T, fz::PKP<N>::BYTES, p->work, f->b, sa,
+                    (const Ctrl*)p->ctrl, f->tm_pkp);
+  } else {
+    (void)p, (void)f, (void)sa;
+    return cudaErrorInvalidValue;
+  }
+}
+
+template <int N>
 static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   using C = fz::Cfg<N>;
   FusedPlan* f = fp_of(p);
@@ -1810,10 +2186,18 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
     return PF_OK;
   };
   PF_CK(mark(0));
-  const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
+  int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
   const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
-  PF_CK_CUDA(launch_k(fz::k_pk<N, false>, pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
-                      (const Ctrl*)p->ctrl, f->tm_pk));
+  if (f->pk_pipe && f->b.tma) {  // persistent pipelined PK on the main tiles + k_pk on the N / CP Nyquist tiles
+    const int main_tiles = N * fz::PK2<N>::NCH, nyq = N / fz::PK2<N>::CP;
+    PF_CK_CUDA(launch_pk_pipe<N>(p, f, sa));
+    PF_CK_CUDA(launch_k(fz::k_pk<N, false>, nyq, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
+                        (const Ctrl*)p->ctrl, f->tm_pk, main_tiles, f->nb_pkp, f->nb_pkp + nyq));
+    pk_tiles = f->nb_pkp + nyq;  // partial rows for the finalize
+  } else {
+    PF_CK_CUDA(launch_k(fz::k_pk<N, false>, pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
+                        (const Ctrl*)p->ctrl, f->tm_pk, 0, 0, pk_tiles));
+  }
   PF_CK(mark(1));
   int nb_part = f->nb_rs;
   PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
@@ -2081,7 +2465,8 @@ template <int N>
 static int fslab_pk_t(pf_plan* p) {
   FusedPlan* f = fp_of(p);
   const int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
-  fz::k_pk<N, true><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, spec_args(p), p->ctrl, f->tm_pk);
+  fz::k_pk<N, true><<<pk_tiles, fz::PK2<N>::T, smem_pk<N>(), p->work>>>(f->b, spec_args(p), p->ctrl, f->tm_pk, 0, 0,
+                                                                         pk_tiles);
   PF_CK_CUDA(cudaGetLastError());
   return PF_OK;
 }
