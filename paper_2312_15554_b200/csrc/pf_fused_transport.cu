@@ -33,6 +33,9 @@
 #ifndef PF_TPK_TMA
 #define PF_TPK_TMA 1  // PK_T loads its two component pencils with 3D TMA tensor copies (N = 128/256)
 #endif
+#ifndef PF_TPK_TMASTORE
+#define PF_TPK_TMASTORE 1  // PK_T stores Y with TMA tensor stores from its boxes (N = 128/256)
+#endif
 #ifndef PF_TM_TMA
 #define PF_TM_TMA 1  // transport axis-1 passes load their tiles with 2D TMA tensor copies (N = 128/256)
 #endif
@@ -223,6 +226,39 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
     fz::radix_stage<N, true>(S, NSEQ, SS, tw, t, T);
   }
   __syncthreads();
+#if PF_TPK_TMASTORE
+  if (tma && C::M == 1) {
+    // Y out by TMA tensor stores: component c's results repacked into its 64B-swizzled
+    // box (box c overlaps only sequences of components <= c, already consumed), then
+    // one thread stores both boxes and waits until they have been read.
+    constexpr int PER = CP * N / T;
+    for (int c = 0; c < 2; ++c) {
+      double2 v[PER];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int idx = t + T * j, q = idx % CP, i0 = idx / CP;
+        v[j] = S[(c * CP + q) * SS + C::sp(i0)];
+      }
+      __syncthreads();
+      unsigned char* box = reg + c * K::BOX;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int idx = t + T * j, q = idx % CP, i0 = idx / CP;
+        *reinterpret_cast<double2*>(box + (size_t)i0 * 64 + ((q ^ ((i0 >> 1) & 3)) << 4)) = v[j];
+      }
+    }
+    fz::fence_async_smem();
+    __syncthreads();
+    if (t == 0) {
+      for (int c = 0; c < 2; ++c)
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmap)),
+                     "r"(2 * ch * CP), "r"(k1), "r"(c * N), "r"(fz::su32(reg + c * K::BOX))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  } else
+#endif
   for (int idx = t; idx < 2 * N * CP; idx += T) {
     const int q = idx % CP, i0 = (idx / CP) % N, c = idx / (CP * N);
     const size_t o = yoff(c, i0, q);
@@ -234,6 +270,9 @@ __global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const C
     B.part[blockIdx.x] = acc[0];
     B.part[gridDim.x + blockIdx.x] = acc[1];
   }
+#if PF_TPK_TMASTORE
+  if (tma && C::M == 1 && t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ MI_T / MF_T
@@ -412,7 +451,11 @@ struct TRS {
   // gradients into registers first), so one buffer of max(SI, SF) bytes
   static constexpr size_t SQ = SI > SF ? SI : SF;
   static constexpr size_t BYTES = TW + SQ + XM + XN + UB + HB;
+#ifdef PF_TRS_MINB
+  static constexpr int MINB = PF_TRS_MINB;
+#else
   static constexpr int MINB = T <= 64 ? 4 : 3;  // register cap that keeps the smem-allowed blocks
+#endif
   static constexpr uint32_t TX = (uint32_t)(XM + XN + UB + HB);
 };
 
