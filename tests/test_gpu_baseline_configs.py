@@ -91,3 +91,74 @@ def test_cfg3_headline_cell_matches_reference(pf, packing256, case, compact):
     # the adaptation must actually have moved the penalties inside the window
     assert np.any(np.asarray(z["final_penalties"]) != 1.0)
     check_stokes(st.to_host(), rep, z, 256)
+
+
+# ---------------------------------------------------------------- cfg 2
+@pytest.fixture(scope="module")
+def cfg2_flow(pf):
+    """The cfg-2 velocity: 128^3 SC sphere array (r = 0.25), stiff penalties, e1,
+    eps 1e-5, converged — checked against the live reference, then reused as the
+    transport solves' flow (make_golden_baseline.py part cfg2)."""
+    z = load("stokes_sphere128_stiff")
+    n = int(z["n"])
+    ind = pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25)
+    pen = pf.PenaltyParams(*(float(x) for x in z["penalties"][:3]), adaptive=bool(z["penalties"][3]))
+    cfg = pf.StokesConfig.with_tolerance(float(z["eps"]), pressure_gradient=tuple(float(x) for x in z["g_p"]))
+    st, rep = pf.solve_stokes(ind, cfg, pen)
+    return ind, st, rep, z
+
+
+def test_cfg2_flow_matches_reference(pf, cfg2_flow):
+    ind, st, rep, z = cfg2_flow
+    assert rep.converged
+    check_stokes(st, rep, z, int(z["n"]))
+
+
+@pytest.mark.parametrize("tag", ["pe10", "pe50"])
+def test_cfg2_transport_matches_reference(pf, cfg2_flow, tag):
+    """transport.py:180-268 at the cfg-2 settings under the cfg-2 flow: Pe = 50 trips
+    the reference's divergence guard after the same number of iterations with the
+    same reason; Pe = 10 converges to the same field."""
+    ind, st, _, _ = cfg2_flow
+    z = load(f"transport_sphere128_{tag}")
+    n = int(z["n"])
+    pe, eta, a0, b0, eps = (float(x) for x in z["params"])
+    cfg = pf.TransportConfig(pe=pe, eta=eta, a0=a0, b0=b0, eps=eps, composition_gradient=tuple(float(x) for x in z["g_chi"]),
+                             max_iter=int(z["max_iter"]))
+    ts, rep = pf.solve_transport(ind, st.u, cfg)
+    assert rep.iterations == int(z["iterations"])
+    assert rep.converged == bool(z["converged"]) and rep.diverged == bool(z["diverged"])
+    assert str(rep.reason or "") == str(z["reason"]).replace("None", "")
+    # b0 = b0 u_bar / |u_bar|: the transverse components are round-off of the flow (~1e-14)
+    np.testing.assert_allclose(rep.meta["b0_vec"], z["b0_vec"], rtol=1e-12, atol=1e-12)
+    if rep.diverged:
+        # the guard fires on a residual that grew 1e6-fold: round-off of the flow is
+        # amplified with it, so the late rows are held to 1e-6 and the fields not at all
+        hist_close(rep.history, z["history"], rtol=1e-6, floor=1e-9, tol_rtol=1e-10, kind="transport")
+        return
+    hist_close(rep.history, z["history"], kind="transport")
+    check_field("chi", ts.chi, z, sample_idx(n ** 3))
+    check_field("grad_chi", ts.grad_chi, z, sample_idx(3 * n ** 3))
+
+
+# ---------------------------------------------------------------- cfg 1 (adaptive)
+@pytest.mark.skipif(not (GOLDEN / "stokes_sphere64_cfg1_adaptive.npz").exists(), reason="fixture not generated")
+def test_cfg1_adaptive_matches_reference(pf):
+    """64^3 SC sphere array, the reference's DEFAULT adaptive penalties (residual
+    balancing decides the iteration count, stokes.py:287-310), three load cases to
+    convergence, and K (Stokes symbols, cli.py:386-388)."""
+    z = load("stokes_sphere64_cfg1_adaptive")
+    n = int(z["n"])
+    ind = pf.make_model_geometry(pf.UnitCellGrid((n, n, n)), radius=0.25)
+    us = []
+    for ax in range(3):
+        g = [0.0, 0.0, 0.0]
+        g[ax] = 1.0
+        st, rep = pf.solve_stokes(ind, pf.StokesConfig.with_tolerance(float(z["eps"]), pressure_gradient=tuple(g)))
+        zz = {k: (v[ax] if getattr(v, "ndim", 0) >= 1 and v.shape[0] == 3 and k != "K" else v) for k, v in z.items()}
+        it = int(zz["iterations"])
+        zz["history"] = z["history"][ax, :it]
+        check_stokes(st, rep, zz, n)
+        us.append(st.u)
+    K = pf.permeability(us, ind, "central")
+    np.testing.assert_allclose(K, z["K"], rtol=1e-9, atol=1e-12 * np.abs(z["K"]).max())
