@@ -68,6 +68,12 @@
 #ifndef PF_PK_PIPE
 #define PF_PK_PIPE 0  // N = 128 / 256 single GPU: persistent pipelined PK (measured slower: 0.37 vs 0.31 ms)
 #endif
+#ifndef PF_M_PIPE
+// single GPU: persistent pipelined axis-1 passes (POREFLOW_B200_M_PIPE=0/1 overrides).
+// Measured: 128^3 cell 11.8 -> 12.4, 8-cell 128^3 ensemble 13.0 -> 14.3 Gvox-it/s;
+// at 256^3 (2 CTAs/SM of 101 KB) MI / MF slow from 0.129 to 0.15 ms, so N = 128 only
+#define PF_M_PIPE(N) ((N) == 128)
+#endif
 #ifndef PF_PK_TMASTORE
 #define PF_PK_TMASTORE 1  // k_pk stores Y with TMA tensor stores from its boxes (single GPU, N = 128/256)
 #endif
@@ -907,7 +913,7 @@ struct M2 {
 
 template <int N, bool INV, bool SL>
 __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl,
-                                                             const __grid_constant__ CUtensorMap tmap) {
+                                                             const __grid_constant__ CUtensorMap tmap, int nyq_only) {
   using C = Cfg<N>;
   using K = M2<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
@@ -922,7 +928,9 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
   const int l0 = (SL ? B.l0 : N), l1 = (SL ? B.l1 : N), s1 = (SL ? B.s1 : Cfg<N>::LOGN);
   const int nl = SL ? B.nl : N, i0a = SL ? B.i0a : 0;  // plane window of this launch
   const int TPC = nl * NCH + nl / CM;  // tiles per component over the window
-  const int c = (SL ? B.c0 : 0) + blockIdx.x / TPC, tile = blockIdx.x % TPC;
+  // nyq_only (beside k_m1_pipe): block -> (component, Nyquist tile)
+  const int c = (SL ? B.c0 : 0) + (nyq_only ? blockIdx.x / (nl / CM) : blockIdx.x / TPC);
+  const int tile = nyq_only ? nl * NCH + blockIdx.x % (nl / CM) : blockIdx.x % TPC;
   const bool nyq = tile >= nl * NCH;
   const int i0 = nyq ? 0 : i0a + tile / NCH, ch = nyq ? 0 : tile % NCH;  // i0: local plane
   const int i0b = nyq ? i0a + (tile - nl * NCH) * CM : 0;
@@ -1120,6 +1128,107 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
       const size_t o = off_of(e, q);
       if (nyq) B.XUn[o] = v; else B.XU[o] = v;
     }
+  }
+}
+
+// ------------------------------------------------------------------ MI / MF, persistent pipelined
+// Single GPU, N = 128 / 256 (M = 1), main tiles; the Nyquist tiles stay on k_maxis
+// (nyq_only).  One CTA walks the tiles blockIdx.x, + gridDim.x, ... with a two-stage
+// TMA ring: tile i + 2's copy is issued into stage i & 1 as soon as tile i has been
+// read into registers, so a tile's load latency and the CTA's per-tile setup
+// (twiddle table, mbarrier) are paid once per CTA instead of per tile — at 128^3
+// the non-persistent passes run at about half their 256^3 bandwidth.
+template <int N>
+struct MP {
+  using C = Cfg<N>;
+  static constexpr int T = M2<N>::T, CM = M2<N>::CM, NCH = M2<N>::NCH;
+  static constexpr int ROWB = CM * 16;
+  static constexpr size_t TILE = sizeof(double2) * CM * N;
+  static constexpr size_t SEQ = sizeof(double2) * CM * C::SS;
+  static constexpr int STAGES = 2;
+  static constexpr size_t BYTES = 1024 + STAGES * TILE + SEQ + sizeof(double2) * C::TWN;
+  static constexpr int UNITS = 3 * N * NCH;  // main tiles of the three components
+  static_assert(C::M == 1 && ROWB == 128, "pipelined axis-1 pass: N <= 256, 128-byte rows");
+  static_assert(TILE % 1024 == 0, "stages stay 1 KB aligned");
+};
+
+template <int N, bool INV>
+__global__ void __launch_bounds__(MP<N>::T, 1) k_m1_pipe(Bufs B, const Ctrl* __restrict__ ctrl,
+                                                         const __grid_constant__ CUtensorMap tmap) {
+  using C = Cfg<N>;
+  using K = MP<N>;
+  constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T, NU = K::UNITS;
+  pdl_wait();
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char mpraw[];
+  unsigned char* base = mpraw + ((1024 - (su32(mpraw) & 1023)) & 1023);
+  double2* S = (double2*)(base + K::STAGES * K::TILE);
+  double2* tw = (double2*)(base + K::STAGES * K::TILE + K::SEQ);
+  __shared__ uint64_t full[K::STAGES];
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+  const double db = INV ? 0.0 : ctrl->db;
+
+  auto issue = [&](int u, int s) {
+    const int c = u / (N * NCH), r = u % (N * NCH), i0 = r / NCH, ch = r % NCH;
+    unsigned char* dst = base + (size_t)s * K::TILE;
+    fence_async_smem();
+    mbar_expect(&full[s], (uint32_t)K::TILE);
+    if (INV && B.yb) {
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+          "%5}], [%6];" ::"r"(su32(dst)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CM), "r"(i0 & 3), "r"(0), "r"(c * (N / 4) + (i0 >> 2)),
+          "r"(su32(&full[s]))
+          : "memory");
+    } else {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              su32(dst)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CM), "r"((c * N + i0) * N), "r"(su32(&full[s]))
+          : "memory");
+    }
+  };
+
+  if (t == 0) {
+    for (int s = 0; s < K::STAGES; ++s) mbar_init(&full[s]);
+    for (int s = 0; s < K::STAGES; ++s)
+      if ((int)blockIdx.x + s * (int)gridDim.x < NU) issue(blockIdx.x + s * gridDim.x, s);
+  }
+  for (int j = t; j < C::TWN; j += T) tw[j] = B.tw[j];
+  __syncthreads();
+  int it = 0;
+  for (int u = blockIdx.x; u < NU; u += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int c = u / (N * NCH), r = u % (N * NCH), i0 = r / NCH, ch = r % NCH;
+    const unsigned char* tile = base + (size_t)s * K::TILE;
+    mbar_wait(&full[s], (it >> 1) & 1);
+    constexpr int A = C::A, BB = C::B;
+    double2 x[A > BB ? A : BB];
+    if (l < BB) {
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) {
+        const int e = BB * n1 + l;  // row e, column g: chunk g of the row, XOR-swizzled by e mod 8
+        x[n1] = *reinterpret_cast<const double2*>(tile + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
+      }
+      if (!INV && db != 0.0) {  // rare: b changed this iteration; XU holds X(u~') (k_rsfix)
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {
+          const double2 vu = B.XU[((size_t)(c * N + i0) * N + BB * n1 + l) * H + ch * CM + g];
+          x[n1] = make_double2(x[n1].x + db * vu.x, x[n1].y + db * vu.y);
+        }
+      }
+    }
+    __syncthreads();  // stage s read: refill it two grid strides ahead
+    if (t == 0 && u + K::STAGES * (int)gridDim.x < NU) issue(u + K::STAGES * gridDim.x, s);
+    fft_seq_x<N, INV>(x, S + g * SS, tw, l, true);
+    __syncthreads();
+    for (int idx = t; idx < N * CM; idx += T) {
+      const int q = idx % CM, e = idx / CM;
+      const double2 v = S[q * SS + (INV ? C::sp(e) : C::kp(e))];
+      if (INV) B.XU[((size_t)(c * N + i0) * N + e) * H + ch * CM + q] = v;
+      else B.Y[ymain<N>(B.yb, c, i0, e, ch * CM + q)] = v;
+    }
+    __syncthreads();  // S is rewritten by the next tile
   }
 }
 
@@ -1718,6 +1827,8 @@ struct FusedPlan {
   double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
   int nb_full = kSMs, nb_compact = kSMs;
   fz::Peers* peers = nullptr;  // device copy of the peer pointer table (P2P exchange)
+  int m_pipe = 0;              // single GPU, N = 128 / 256: persistent pipelined MI / MF (k_m1_pipe)
+  int nb_m1 = 0;
   int pk_pipe = 0;             // single GPU, N = 128 / 256: persistent pipelined PK (k_pk_pipe)
   int nb_pkp = 0;              // its grid (resident CTAs)
 };
@@ -1779,7 +1890,17 @@ static int set_attrs(FusedPlan* f) {
     f->nb_pkp = (o3 < 1 ? 1 : o3) * kSMs;
     if (f->nb_pkp > fz::PKP<N>::UNITS) f->nb_pkp = fz::PKP<N>::UNITS;
     const char* e = getenv("POREFLOW_B200_PK_PIPE");
-    f->pk_pipe = PF_PK_PIPE && !(e && e[0] == '0');
+    f->pk_pipe = e ? e[0] == '1' : PF_PK_PIPE;
+    for (int inv = 0; inv < 2; ++inv) {
+      auto kern = inv ? fz::k_m1_pipe<N, true> : fz::k_m1_pipe<N, false>;
+      PF_CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::MP<N>::BYTES));
+    }
+    int o4 = 0;
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, fz::k_m1_pipe<N, true>, fz::MP<N>::T,
+                                                             fz::MP<N>::BYTES));
+    f->nb_m1 = (o4 < 1 ? 1 : o4) * kSMs;
+    const char* e2 = getenv("POREFLOW_B200_M_PIPE");
+    f->m_pipe = e2 ? e2[0] == '1' : PF_M_PIPE(N);
   }
   f->nb_full = wave(o1, 3);
   f->nb_compact = wave(o2, kRsMaxBlocks / kSMs);
@@ -2156,6 +2277,17 @@ int fused_finish(pf_plan* p) {
   return PF_OK;
 }
 
+template <int N, bool INV>
+static cudaError_t launch_m1_pipe(pf_plan* p, FusedPlan* f, const CUtensorMap& tm) {
+  if constexpr (N == 128 || N == 256) {
+    return launch_k(fz::k_m1_pipe<N, INV>, f->nb_m1, fz::MP<N>::T, fz::MP<N>::BYTES, p->work, f->b,
+                    (const Ctrl*)p->ctrl, tm);
+  } else {
+    (void)p, (void)f, (void)tm;
+    return cudaErrorInvalidValue;
+  }
+}
+
 template <int N>
 static cudaError_t launch_pk_pipe(pf_plan* p, FusedPlan* f, const fz::SpecArgs& sa) {
   if constexpr (N == 128 || N == 256) {
@@ -2200,8 +2332,14 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   }
   PF_CK(mark(1));
   int nb_part = f->nb_rs;
-  PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
-                      (const Ctrl*)p->ctrl, f->tm_y));
+  if (f->m_pipe && f->b.tma) {  // persistent main tiles + k_maxis on the Nyquist tiles
+    PF_CK_CUDA((launch_m1_pipe<N, true>(p, f, f->tm_y)));
+    PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, 3 * (N / fz::M2<N>::CM), fz::M2<N>::T, smem_mi<N>(), p->work,
+                        f->b, (const Ctrl*)p->ctrl, f->tm_y, 1));
+  } else {
+    PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
+                        (const Ctrl*)p->ctrl, f->tm_y, 0));
+  }
   PF_CK(mark(2));
   if (f->compact) {
     PF_CK_CUDA(launch_k(fz::k_rs_compact<N, false>, f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work,
@@ -2221,8 +2359,14 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
                         (const double*)p->s_ut, (const Ctrl*)p->ctrl));
   }
   PF_CK(mark(5));
-  PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work, f->b,
-                      (const Ctrl*)p->ctrl, f->tm_xr));
+  if (f->m_pipe && f->b.tma) {
+    PF_CK_CUDA((launch_m1_pipe<N, false>(p, f, f->tm_xr)));
+    PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, 3 * (N / fz::M2<N>::CM), fz::M2<N>::T, smem_mf<N>(),
+                        p->work, f->b, (const Ctrl*)p->ctrl, f->tm_xr, 1));
+  } else {
+    PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work, f->b,
+                        (const Ctrl*)p->ctrl, f->tm_xr, 0));
+  }
   PF_CK(mark(6));
   return PF_OK;
 }
@@ -2495,7 +2639,7 @@ static int fslab_rs_t(pf_plan* p, int c0, int nc, double* totals) {
   f->b.pst = nc == 3 ? f->nb_rs : 3 * f->nb_rs;
   f->b.poff = nc == 3 ? 0 : c0 * f->nb_rs;
   f->rs_rows = f->b.pst;
-  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl, f->tm_y);
+  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl, f->tm_y, 0);
   PF_CK_CUDA(cudaGetLastError());
   if (f->compact) {
     fz::k_rs_compact<N, true><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(
@@ -2531,7 +2675,7 @@ static int fslab_mf_t(pf_plan* p, int c0, int nc, bool fix) {
   const int m_tiles = nc * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
   f->b.c0 = c0;
   f->b.nc = nc;
-  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_xr);
+  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_xr, 0);
   PF_CK_CUDA(cudaGetLastError());
   f->b.c0 = 0;
   f->b.nc = 3;
