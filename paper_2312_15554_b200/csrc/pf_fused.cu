@@ -74,6 +74,12 @@
 // at 256^3 (2 CTAs/SM of 101 KB) MI / MF slow from 0.129 to 0.15 ms, so N = 128 only
 #define PF_M_PIPE(N) ((N) == 128)
 #endif
+#ifndef PF_ABL_NOFIN
+#define PF_ABL_NOFIN 0  // measurement-only ablations of the per-iteration fixed costs (results invalid)
+#endif
+#ifndef PF_ABL_NORSF
+#define PF_ABL_NORSF 0
+#endif
 #ifndef PF_PK_TMASTORE
 #define PF_PK_TMASTORE 1  // k_pk stores Y with TMA tensor stores from its boxes (single GPU, N = 128/256)
 #endif
@@ -2349,9 +2355,12 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
                         (const Ctrl*)p->ctrl));
   }
   PF_CK(mark(3));
+#if PF_ABL_NOFIN == 0
   PF_CK_CUDA(k_stokes_finalize_launch_pdl(p, f->b.part_rs, nb_part, f->b.part_pk, pk_tiles));
+#endif
   PF_CK(mark(4));
-  if (f->compact) {
+  if (PF_ABL_NORSF) {
+  } else if (f->compact) {
     PF_CK_CUDA(launch_k(fz::k_rsfix_compact<N, false>, f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work, f->b,
                         (const double*)p->s_u, (const uint8_t*)p->s_solid, compact_of(f), (const Ctrl*)p->ctrl));
   } else {
