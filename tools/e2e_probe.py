@@ -15,6 +15,7 @@ import paper_2312_15554_b200 as pf  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=256)
 ap.add_argument("--iters", type=int, default=300)
+ap.add_argument("--packed", action="store_true", help="bit-packed indicator in (the bench e2e leg)")
 a = ap.parse_args()
 n = a.n
 vals = np.array(pf.random_packing_geometry(n, seed=0).values)
@@ -24,7 +25,8 @@ torch.cuda.synchronize()
 dev = torch.device("cuda", 0)
 T = {}
 t = time.perf_counter()
-ind = pf.IndicatorField(pf.UnitCellGrid((n, n, n)), vals)
+ind = (pf.PackedIndicator(pf.UnitCellGrid((n, n, n)), np.packbits(vals.ravel())) if a.packed
+       else pf.IndicatorField(pf.UnitCellGrid((n, n, n)), vals))
 T["indicator"] = time.perf_counter() - t
 t = time.perf_counter()
 st = pf.DeviceAdmmState.zeros(ind.grid, dev)
