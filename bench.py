@@ -287,11 +287,13 @@ def run_ours(args):
                         "GB_s": (sb[name] / (t_ms * 1e-3) / 1e9) if t_ms > 0 and sb[name] else None}
     ours = [s for s in stages if "cufft" not in s and s not in ("finalize", "RSF_rows_fix")]
     dom = max(ours, key=lambda s: stages[s]["ms"])
-    traffic = None
+    traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "traffic_per_launch.json"
-    if tfile.exists():
+    if tfile.exists():  # the ncu capture this figure comes from is named with its commit
         try:
-            traffic = json.loads(tfile.read_text()).get(pipeline, {}).get(dom)
+            ent = json.loads(tfile.read_text()).get(pipeline, {})
+            traffic = ent.get(dom)
+            traffic_src = f"{ent.get('_capture')} @ {ent.get('_commit')}" if traffic is not None else None
         except Exception:
             traffic = None
     achieved = stages[dom]["GB_s"]
@@ -334,7 +336,7 @@ def run_ours(args):
         "config": headline_config(n, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "peak_source": peak_src},
+                     "traffic_source": traffic_src, "peak_source": peak_src},
         "iteration_roofline": {"alg_bytes_per_voxel_iter": B_ALG_ITER,
                                "achieved_GB_s": B_ALG_ITER * value / world / 1e9,
                                "frac": B_ALG_ITER * value / world / 1e9 / peak,

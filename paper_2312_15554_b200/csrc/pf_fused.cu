@@ -80,6 +80,12 @@
 #ifndef PF_ABL_NORSF
 #define PF_ABL_NORSF 0
 #endif
+#ifndef PF_MP_STAGES
+#define PF_MP_STAGES 2  // TMA ring depth of the persistent axis-1 passes
+#endif
+#ifndef PF_MP_MINB
+#define PF_MP_MINB 1
+#endif
 #ifndef PF_PK_TMASTORE
 #define PF_PK_TMASTORE 1  // k_pk stores Y with TMA tensor stores from its boxes (single GPU, N = 128/256)
 #endif
@@ -1151,7 +1157,8 @@ struct MP {
   static constexpr int ROWB = CM * 16;
   static constexpr size_t TILE = sizeof(double2) * CM * N;
   static constexpr size_t SEQ = sizeof(double2) * CM * C::SS;
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = PF_MP_STAGES;
+  static constexpr int MINB = PF_MP_MINB;
   static constexpr size_t BYTES = 1024 + STAGES * TILE + SEQ + sizeof(double2) * C::TWN;
   static constexpr int UNITS = 3 * N * NCH;  // main tiles of the three components
   static_assert(C::M == 1 && ROWB == 128, "pipelined axis-1 pass: N <= 256, 128-byte rows");
@@ -1159,7 +1166,7 @@ struct MP {
 };
 
 template <int N, bool INV>
-__global__ void __launch_bounds__(MP<N>::T, 1) k_m1_pipe(Bufs B, const Ctrl* __restrict__ ctrl,
+__global__ void __launch_bounds__(MP<N>::T, MP<N>::MINB) k_m1_pipe(Bufs B, const Ctrl* __restrict__ ctrl,
                                                          const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = MP<N>;
@@ -1204,10 +1211,10 @@ __global__ void __launch_bounds__(MP<N>::T, 1) k_m1_pipe(Bufs B, const Ctrl* __r
   __syncthreads();
   int it = 0;
   for (int u = blockIdx.x; u < NU; u += gridDim.x, ++it) {
-    const int s = it & 1;
+    const int s = it % K::STAGES;
     const int c = u / (N * NCH), r = u % (N * NCH), i0 = r / NCH, ch = r % NCH;
     const unsigned char* tile = base + (size_t)s * K::TILE;
-    mbar_wait(&full[s], (it >> 1) & 1);
+    mbar_wait(&full[s], (it / K::STAGES) & 1);
     constexpr int A = C::A, BB = C::B;
     double2 x[A > BB ? A : BB];
     if (l < BB) {
