@@ -1871,22 +1871,20 @@ static size_t smem_pk() { return fz::PK2<N>::BYTES; }
 
 template <int N>
 static int set_attrs(FusedPlan* f) {
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rs<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rs_compact<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rsc<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_rsfix_compact<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_rsfix<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mf<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_maxis<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mi<N>()));
-  PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pk<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rs<N, false>, (int)smem_rs<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rsfix<N, false>, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rs_compact<N, false>, (int)smem_rsc<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rsfix_compact<N, false>, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_maxis<N, false, false>, (int)smem_mf<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_maxis<N, true, false>, (int)smem_mi<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_pk<N, false>, (int)smem_pk<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rs<N, true>, (int)smem_rs<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rsfix<N, true>, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rs_compact<N, true>, (int)smem_rsc<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_rsfix_compact<N, true>, (int)smem_rsfix<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_maxis<N, false, true>, (int)smem_mf<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_maxis<N, true, true>, (int)smem_mi<N>()));
+  PF_CK_CUDA(smem_attr(fz::k_pk<N, true>, (int)smem_pk<N>()));
   // persistent RS grids: one wave of resident blocks.  The full-layout kernel is
   // capped at 3 per SM: it streams 4 KB/voxel-row-tile at ~93% of HBM peak and a
   // 4th block only adds contention (256^3: 0.697 ms at 4/SM vs 0.662 ms at 3/SM).
@@ -1895,8 +1893,7 @@ static int set_attrs(FusedPlan* f) {
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, fz::k_rs<N, false>, fz::RS2<N>::T, smem_rs<N>()));
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fz::k_rs_compact<N, false>, fz::RS2<N>::T, smem_rsc<N>()));
   if constexpr (N == 128 || N == 256) {
-    PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk_pipe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)fz::PKP<N>::BYTES));
+    PF_CK_CUDA(smem_attr(fz::k_pk_pipe<N>, (int)fz::PKP<N>::BYTES));
     int o3 = 0;
     PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, fz::k_pk_pipe<N>, fz::PKP<N>::T,
                                                              fz::PKP<N>::BYTES));
@@ -1906,7 +1903,7 @@ static int set_attrs(FusedPlan* f) {
     f->pk_pipe = e ? e[0] == '1' : PF_PK_PIPE;
     for (int inv = 0; inv < 2; ++inv) {
       auto kern = inv ? fz::k_m1_pipe<N, true> : fz::k_m1_pipe<N, false>;
-      PF_CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::MP<N>::BYTES));
+      PF_CK_CUDA(smem_attr(kern, (int)fz::MP<N>::BYTES));
     }
     int o4 = 0;
     PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, fz::k_m1_pipe<N, true>, fz::MP<N>::T,

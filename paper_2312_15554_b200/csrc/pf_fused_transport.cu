@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
 template <int N>
 struct TRS {
   using C = Cfg<N>;
-  static constexpr int R = N > 256 ? 2 : 512 / N;  // rows per tile
+#ifndef PF_TRS_R256
+#define PF_TRS_R256 2
+#endif
+  static constexpr int R = N > 256 ? 2 : (N == 256 ? PF_TRS_R256 : 512 / N);  // rows per tile
   static constexpr int NSF = 2 * R;          // forward sequences: (w0 + i w1), (s + i w2) per row
   static constexpr int NSI = R + R / 2;      // inverse: (d0 + i d1) per row, (d2, d2) per row pair
   static constexpr int T = NSF * C::M * C::G;  // one group per forward block transform
@@ -692,10 +695,10 @@ static FusedTPlan* ftp(pf_plan* p) { return reinterpret_cast<FusedTPlan*>(p->tfu
 
 template <int N>
 static int tset_attrs(FusedTPlan* f) {
-  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_tpk<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TPK<N>::BYTES));
-  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_taxis<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TM<N>::BYTES));
-  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_taxis<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TM<N>::BYTES));
-  PF_CK_CUDA(cudaFuncSetAttribute(ft::k_trs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ft::TRS<N>::BYTES));
+  PF_CK_CUDA(smem_attr(ft::k_tpk<N>, (int)ft::TPK<N>::BYTES));
+  PF_CK_CUDA(smem_attr(ft::k_taxis<N, true>, (int)ft::TM<N>::BYTES));
+  PF_CK_CUDA(smem_attr(ft::k_taxis<N, false>, (int)ft::TM<N>::BYTES));
+  PF_CK_CUDA(smem_attr(ft::k_trs<N>, (int)ft::TRS<N>::BYTES));
   int o = 0;
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ft::k_trs<N>, ft::TRS<N>::T, ft::TRS<N>::BYTES));
   f->nb_trs = (o < 1 ? 1 : o) * kSMs;

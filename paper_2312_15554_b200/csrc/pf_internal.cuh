@@ -349,6 +349,20 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 
+// Dynamic shared memory limit of a kernel plus its carveout preference.  Left to
+// itself the driver picked a 200 KB carveout for the fused kernels (ncu "Shared
+// Memory Configuration Size"), which capped e.g. the transport RS at 4 CTAs/SM of
+// 45 KB; PF_CARVEOUT (percent of the maximum, -1 = driver default) asks for more.
+#ifndef PF_CARVEOUT
+#define PF_CARVEOUT -1  // measured: 100 (max shared) costs PK 0.29 -> 0.33 ms (less L1), RS_T no gain
+#endif
+template <typename... KArgs>
+inline cudaError_t smem_attr(void (*kern)(KArgs...), size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess || PF_CARVEOUT < 0) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, PF_CARVEOUT);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                             Args&&... args) {
