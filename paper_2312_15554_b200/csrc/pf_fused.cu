@@ -86,6 +86,12 @@
 #ifndef PF_MP_MINB
 #define PF_MP_MINB 1
 #endif
+#ifndef PF_RSFIX_TMA
+#define PF_RSFIX_TMA 1  // TMA-staged RS-fix on the single-GPU compact path (POREFLOW_B200_RSFIX_TMA=0/1)
+#endif
+#ifndef PF_GROUPED
+#define PF_GROUPED 0  // grouped last-block partial reductions in PK / RS (measured slower at 64^3 / 128^3, neutral at 256^3)
+#endif
 #ifndef PF_PK_TMASTORE
 #define PF_PK_TMASTORE 1  // k_pk stores Y with TMA tensor stores from its boxes (single GPU, N = 128/256)
 #endif
@@ -139,6 +145,46 @@ __device__ __forceinline__ size_t ymain(int yb, int c, int i0, int k1, int k2) {
             : (((size_t)(c * N + i0) * N + k1) * H + k2);
 }
 
+#ifndef PF_GRP_PK
+#define PF_GRP_PK 64  // PK tiles per partial group
+#endif
+#ifndef PF_GRP_RS
+#define PF_GRP_RS 16  // RS blocks per partial group
+#endif
+// Deterministic grouped reduction of per-block partials (thread 0 holds the
+// block's totals v): each block stores its NQ partials to part[q nb + b]; the last
+// block to arrive in its group of GS (atomic counter, threadfence pattern) sums the
+// group's partials in index order with one warp — lane i takes i, i + 32, ... then
+// a fixed shuffle tree — into gpart[q ng + g] and resets the counter.  The result
+// does not depend on which block arrives last.
+template <int NQ>
+__device__ __forceinline__ void group_reduce(const double (&v)[NQ], double* part, int nb, double* gpart,
+                                             unsigned* cnt, int GS) {
+  __shared__ int s_last;
+  const int b = blockIdx.x, g = b / GS, ng = (nb + GS - 1) / GS;
+  const int gsz = min(GS, nb - g * GS);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) part[(size_t)q * nb + b] = v[q];
+    __threadfence();
+    s_last = atomicAdd(&cnt[g], 1u) == (unsigned)(gsz - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    const int lane = threadIdx.x, b0 = g * GS;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double x = 0.0;
+      for (int i = lane; i < gsz; i += 32) x += __ldcg(part + (size_t)q * nb + b0 + i);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      if (lane == 0) gpart[(size_t)q * ng + g] = x;
+    }
+    if (lane == 0) cnt[g] = 0u;
+  }
+}
+
 constexpr int kMaxRanks = 16;
 struct Peers {
   double2 *yy[kMaxRanks], *yyn[kMaxRanks];  // y-slab Y of each rank
@@ -153,6 +199,11 @@ struct Bufs {
   double2* D;         // full spectrum D^_prev, same layout
   double2* tw;        // N forward twiddles
   double *part_rs, *part_pk;
+  // grouped partials (single GPU): the last block of each group of PF_GRP_PK PK tiles /
+  // PF_GRP_RS RS blocks sums its group's partials (index order) into gpk / grs, so the
+  // finalize reads ~100 - 600 values instead of one per PK tile and RS block
+  double *gpk, *grs;
+  unsigned *cpk, *crs;  // per-group arrival counters (reset by each group's last block)
   // slab layout (single GPU: l0 = l1 = N, s1 = log2 N, k1off = 0): this rank's
   // x-slab holds l0 i0-planes, its y-slab l1 k1-planes starting at k1off; P = N / l1
   // is a power of two (s1 = log2 l1).  Y (after axes 2, 1; axis 0 real) exists in
@@ -364,9 +415,12 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     __syncthreads();
   }
   block_sum<6>(acc);
-  if (t == 0)
+  if (!SL && B.crs) {
+    group_reduce<6>(acc, B.part_rs, gridDim.x, B.grs, B.crs, PF_GRP_RS);
+  } else if (t == 0) {
     for (int k = 0; k < 6; ++k)
       B.part_rs[SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x] = acc[k];
+  }
 }
 
 // RS-fix: X-space of u~' (row FFTs of the state), needed by MF only in the
@@ -669,9 +723,12 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     __syncthreads();
   }
   block_sum<6, RS2<N>::T / 32>(acc);
-  if (t == 0)
+  if (!SL && B.crs) {
+    group_reduce<6>(acc, B.part_rs, gridDim.x, B.grs, B.crs, PF_GRP_RS);
+  } else if (t == 0) {
     for (int k = 0; k < 6; ++k)
       B.part_rs[SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x] = acc[k];
+  }
 }
 
 // RS-fix on the compact path: u~' rows = u' on pore voxels, the compact u~ on solid ones.
@@ -738,6 +795,119 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rsfix_compact(Bufs B, const doubl
       XUn[row0 + 2 * p] = make_double2(z.x, 0.0);
       XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
     }
+  }
+}
+
+// RS-fix, TMA-staged (single GPU, solid-only storage): the same map as
+// k_rsfix_compact — X(u~') rows into XU when residual balancing changed b — with
+// each tile's u rows, indicator bytes and solid u~ range brought in by bulk copies
+// on an mbarrier and the next tile's copies issued as soon as the current tile has
+// been packed into its sequences.  The per-voxel global gathers of k_rsfix_compact
+// ran an active RS-fix at 0.45 ms at 256^3 (about 2 TB/s); it fires in about 6 % of
+// the iterations of an adaptive solve (17 of 300 in the bench window).
+template <int N>
+struct RSFX {
+  using K = RS2<N>;
+  static constexpr size_t bytes(int cs) {
+    return K::TW + K::INV + sizeof(double) * K::V + sizeof(double) * (size_t)cs + K::HB + 16;
+  }
+};
+
+template <int N>
+__global__ void __launch_bounds__(RS2<N>::T) k_rsfix_tma(Bufs B, const double* __restrict__ u,
+                                                         const uint8_t* __restrict__ Hs, Compact cp,
+                                                         const Ctrl* __restrict__ ctrl) {
+  using C = Cfg<N>;
+  using K = RS2<N>;
+  constexpr int H = C::H, SS = C::SS, R = K::R, T = K::T, V = K::V, NP = K::NP;
+  constexpr int TPC = N * N / R, NT = 3 * TPC;
+  constexpr int SG = V / 1024;
+  static_assert(T % 32 == 0, "segment bases are per warp");
+  if (V != 1024 && V != 2048) return;
+  pdl_wait();
+  if (ctrl->done || ctrl->db == 0.0) return;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t ros[2][R + 1];
+  double2* tw = (double2*)sraw;
+  double2* SF = (double2*)(sraw + K::TW);
+  double* su = (double*)(sraw + K::TW + K::INV);
+  double* sc = su + V;
+  uint8_t* sh = (uint8_t*)(sc + cp.cs);
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G, lane = t & 31;
+  for (int j = t; j < C::TWN; j += T) tw[j] = B.tw[j];
+  const int64_t n = (int64_t)N * N * N;
+  uint32_t ro[R + 1];
+  auto offs = [&](int tl) {
+    const int64_t r0 = (int64_t)(tl % TPC) * R;
+#pragma unroll
+    for (int r = 0; r <= R; ++r) ro[r] = cp.off[r0 + r];
+  };
+  auto issue = [&](int tl, uint32_t* slot) {  // thread 0: u rows, H bytes, solid u~ range of tile tl
+    const int c = tl / TPC;
+    const int64_t row0 = (int64_t)(tl % TPC) * R;
+    const uint32_t cb = sizeof(double) * (ro[R] - ro[0]);
+    for (int r = 0; r <= R; ++r) slot[r] = ro[r];
+    fence_async_smem();
+    mbar_expect(&mbar, (uint32_t)(sizeof(double) * V + K::HB) + cb);
+    bulk_load(su, u + (int64_t)c * n + row0 * N, sizeof(double) * V, &mbar);
+    bulk_load(sh, Hs + row0 * N, (uint32_t)K::HB, &mbar);
+    if (cb) bulk_load(sc, cp.ut + (int64_t)c * cp.ns + ro[0], cb, &mbar);
+  };
+  if (t == 0) {
+    mbar_init(&mbar);
+    if ((int)blockIdx.x < NT) {
+      offs(blockIdx.x);
+      issue(blockIdx.x, ros[0]);
+    }
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
+    const int c = tile / TPC;
+    const int64_t row0 = (int64_t)(tile % TPC) * R;
+    const bool has_next = tile + (int)gridDim.x < NT;
+    if (t == 0 && has_next) offs(tile + gridDim.x);
+    mbar_wait(&mbar, phase);
+    const uint32_t o0 = ros[phase][0];
+    int sb[2 > SG ? 2 : SG];
+#pragma unroll
+    for (int q = 0; q < SG; ++q) sb[q] = seg_base<N>(sh + q * 1024 + lane * 32, ros[phase][(q * 1024 + lane * 32) / N] - o0, lane);
+    for (int j = 0; j < K::VPT; ++j) {
+      const int v = t + T * j, row = v / N, col = v % N;
+      const bool solid = sh[v] != 0;
+      const unsigned mask = __ballot_sync(0xffffffffu, solid);
+      const int segb = __shfl_sync(0xffffffffu, (SG == 1 || (v >> 10) == 0) ? sb[0] : sb[1], (v >> 5) & 31);
+      double val = su[v];  // pore: u~' = u'
+      if (solid) val = sc[segb + __popc(mask & ((1u << lane) - 1u))];
+      reinterpret_cast<double*>(SF + (row >> 1) * SS + C::sp(col))[row & 1] = val;
+    }
+    __syncthreads();  // staged inputs consumed: the next tile's copies go out under the FFT
+    if (t == 0 && has_next) issue(tile + gridDim.x, ros[phase ^ 1u]);
+    if constexpr (C::M > 1) {
+      radix_stage<N, false>(SF, NP, SS, tw, t, T);
+      __syncthreads();
+    }
+    if constexpr (PF_RS_W32 && C::L == 256 && T == 32 * NP * C::M) {
+      fft_units_w32<N, false>(SF, NP, SS, tw, t);
+    } else {
+      fft_units<N, false>(SF, NP, SS, tw, g, l, T / C::G);
+    }
+    __syncthreads();
+    double2* XU = B.XU + (size_t)c * N * N * H;
+    double2* XUn = B.XUn + (size_t)c * N * N;
+    for (int idx = t; idx < NP * H; idx += T) {
+      const int p = idx / H, k = idx % H;
+      const double2 zk = SF[p * SS + C::kp(k)], zm = SF[p * SS + C::kp((N - k) & (N - 1))];
+      XU[(row0 + 2 * p) * H + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      XU[(row0 + 2 * p + 1) * H + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+    for (int p = t; p < NP; p += T) {
+      const double2 z = SF[p * SS + C::kp(H)];
+      XUn[row0 + 2 * p] = make_double2(z.x, 0.0);
+      XUn[row0 + 2 * p + 1] = make_double2(z.y, 0.0);
+    }
+    __syncthreads();  // SF is rewritten by the next tile
   }
 }
 
@@ -925,7 +1095,8 @@ struct M2 {
 
 template <int N, bool INV, bool SL>
 __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl,
-                                                             const __grid_constant__ CUtensorMap tmap, int nyq_only) {
+                                                             const __grid_constant__ CUtensorMap tmap, int nyq_only,
+                                                             const __grid_constant__ CUtensorMap tmap_xu) {
   using C = Cfg<N>;
   using K = M2<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
@@ -1058,21 +1229,41 @@ __global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __
       __syncthreads();
     } else {
     double2 x[A > BB ? A : BB];
+    const double db = INV ? 0.0 : ctrl->db;
     if (l < BB) {
 #pragma unroll
       for (int n1 = 0; n1 < A; ++n1) {
         const int e = BB * n1 + l;  // row e, column g: chunk g of the row, XOR-swizzled by e mod 8
         x[n1] = *reinterpret_cast<const double2*>(tile + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
       }
-      if (!INV) {
-        const double db = ctrl->db;
-        if (db != 0.0) {  // rare: b changed this iteration; XU holds X(u~') (k_rsfix)
+    }
+    if (!INV && db != 0.0 && !SL && !nyq) {
+      // rare: b changed this iteration; X(u~') (k_rsfix) comes in as a second TMA tile
+      // into the same region once the first has been read
+      __syncthreads();
+      if (t == 0) {
+        fence_async_smem();
+        mbar_expect(&mbar, (uint32_t)K::TILE);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                su32(S)),
+            "l"(reinterpret_cast<uint64_t>(&tmap_xu)), "r"(2 * ch * CM), "r"((c * l0 + i0) * N), "r"(su32(&mbar))
+            : "memory");
+      }
+      mbar_wait(&mbar, 1);
+      if (l < BB) {
 #pragma unroll
-          for (int n1 = 0; n1 < A; ++n1) {
-            const double2 vu = B.XU[off_of(BB * n1 + l, g)];
-            x[n1] = make_double2(x[n1].x + db * vu.x, x[n1].y + db * vu.y);
-          }
+        for (int n1 = 0; n1 < A; ++n1) {
+          const int e = BB * n1 + l;
+          const double2 vu = *reinterpret_cast<const double2*>(tile + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
+          x[n1] = make_double2(x[n1].x + db * vu.x, x[n1].y + db * vu.y);
         }
+      }
+    } else if (!INV && db != 0.0 && l < BB) {  // rare, slab layouts: per-element reads of X(u~')
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) {
+        const double2 vu = B.XU[off_of(BB * n1 + l, g)];
+        x[n1] = make_double2(x[n1].x + db * vu.x, x[n1].y + db * vu.y);
       }
     }
     __syncthreads();  // the tile is read: the padded sequences may now overwrite it
@@ -1167,7 +1358,8 @@ struct MP {
 
 template <int N, bool INV>
 __global__ void __launch_bounds__(MP<N>::T, MP<N>::MINB) k_m1_pipe(Bufs B, const Ctrl* __restrict__ ctrl,
-                                                         const __grid_constant__ CUtensorMap tmap) {
+                                                         const __grid_constant__ CUtensorMap tmap,
+                                                         const __grid_constant__ CUtensorMap tmap_xu) {
   using C = Cfg<N>;
   using K = MP<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T, NU = K::UNITS;
@@ -1178,6 +1370,7 @@ __global__ void __launch_bounds__(MP<N>::T, MP<N>::MINB) k_m1_pipe(Bufs B, const
   double2* S = (double2*)(base + K::STAGES * K::TILE);
   double2* tw = (double2*)(base + K::STAGES * K::TILE + K::SEQ);
   __shared__ uint64_t full[K::STAGES];
+  __shared__ uint64_t xbar;  // X(u~') tile (FWD, only when b changed this iteration)
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
   const double db = INV ? 0.0 : ctrl->db;
 
@@ -1204,6 +1397,7 @@ __global__ void __launch_bounds__(MP<N>::T, MP<N>::MINB) k_m1_pipe(Bufs B, const
 
   if (t == 0) {
     for (int s = 0; s < K::STAGES; ++s) mbar_init(&full[s]);
+    mbar_init(&xbar);
     for (int s = 0; s < K::STAGES; ++s)
       if ((int)blockIdx.x + s * (int)gridDim.x < NU) issue(blockIdx.x + s * gridDim.x, s);
   }
@@ -1223,10 +1417,24 @@ __global__ void __launch_bounds__(MP<N>::T, MP<N>::MINB) k_m1_pipe(Bufs B, const
         const int e = BB * n1 + l;  // row e, column g: chunk g of the row, XOR-swizzled by e mod 8
         x[n1] = *reinterpret_cast<const double2*>(tile + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
       }
-      if (!INV && db != 0.0) {  // rare: b changed this iteration; XU holds X(u~') (k_rsfix)
+    }
+    if (!INV && db != 0.0) {  // rare: b changed this iteration; X(u~') (k_rsfix) as a TMA tile into S
+      if (t == 0) {
+        fence_async_smem();
+        mbar_expect(&xbar, (uint32_t)K::TILE);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                su32(S)),
+            "l"(reinterpret_cast<uint64_t>(&tmap_xu)), "r"(2 * ch * CM), "r"((c * N + i0) * N), "r"(su32(&xbar))
+            : "memory");
+      }
+      mbar_wait(&xbar, it & 1);
+      const unsigned char* xu = reinterpret_cast<const unsigned char*>(S);
+      if (l < BB) {
 #pragma unroll
         for (int n1 = 0; n1 < A; ++n1) {
-          const double2 vu = B.XU[((size_t)(c * N + i0) * N + BB * n1 + l) * H + ch * CM + g];
+          const int e = BB * n1 + l;
+          const double2 vu = *reinterpret_cast<const double2*>(xu + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
           x[n1] = make_double2(x[n1].x + db * vu.x, x[n1].y + db * vu.y);
         }
       }
@@ -1523,8 +1731,11 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
     }
   }
   block_sum<3>(acc);
-  if (t == 0)
+  if (!SL && B.cpk && tile0 == 0 && (int)gridDim.x == nparts) {
+    group_reduce<3>(acc, B.part_pk, nparts, B.gpk, B.cpk, PF_GRP_PK);
+  } else if (t == 0) {
     for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * nparts + pbase + blockIdx.x] = acc[k];
+  }
 #if PF_PK_TMASTORE
   if (!SL && tma && C::M == 1 && t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #endif
@@ -1835,11 +2046,14 @@ struct FusedPlan {
   double lam_pore = 0.0;
   CUtensorMap tm_pk{};          // 3D map of Y for PK ([c i0][k1][k2] pencils)
   CUtensorMap tm_pkp{};         // the same with the pipelined PK's unit width (PF_PKP_CP columns)
+  CUtensorMap tm_xu{};          // 2D map of XU (MF's X(u~') tile when b changed)
   CUtensorMap tm_y{}, tm_xr{};  // 2D maps of Y and XR ([c][i0][e] rows x N/2 columns) for the axis-1 TMA loads
   void* ws = nullptr;        // cuFFT work area of plan2d
   double2* spec = nullptr;   // setup scratch: axes-(1, 2) transform of R, natural rows
   int nb_full = kSMs, nb_compact = kSMs;
   fz::Peers* peers = nullptr;  // device copy of the peer pointer table (P2P exchange)
+  void* grp = nullptr;         // grouped partials + counters (Bufs::gpk, grs, cpk, crs)
+  int rsfix_tma = 0, nb_rsfx = kSMs;  // TMA-staged RS-fix (k_rsfix_tma) and its persistent grid
   int m_pipe = 0;              // single GPU, N = 128 / 256: persistent pipelined MI / MF (k_m1_pipe)
   int nb_m1 = 0;
   int pk_pipe = 0;             // single GPU, N = 128 / 256: persistent pipelined PK (k_pk_pipe)
@@ -2071,6 +2285,17 @@ int fused_ensure(pf_plan* p) {
   f->b.Yxn = f->b.Yn;
   f->b.part_rs = (double*)m;
   f->b.part_pk = f->b.part_rs + 6 * (size_t)nb_rs;
+  {
+    const size_t ngp = (size_t)nb_pk / PF_GRP_PK + 1, ngr = (size_t)nb_rs / PF_GRP_RS + 1;
+    PF_CK_CUDA(cudaMalloc(&f->grp, sizeof(double) * (3 * ngp + 6 * ngr) + sizeof(unsigned) * (ngp + ngr)));
+    PF_CK_CUDA(cudaMemset(f->grp, 0, sizeof(double) * (3 * ngp + 6 * ngr) + sizeof(unsigned) * (ngp + ngr)));
+    f->b.gpk = (double*)f->grp;
+    f->b.grs = f->b.gpk + 3 * ngp;
+    f->b.cpk = (unsigned*)(f->b.grs + 6 * ngr);
+    f->b.crs = f->b.cpk + ngp;
+    const char* e = getenv("POREFLOW_B200_GROUPED");
+    if (e ? e[0] == '0' : !PF_GROUPED) f->b.cpk = f->b.crs = nullptr;
+  }
   std::vector<double2> tw(N == 64 ? fz::Cfg<64>::TWN : (N == 128 ? fz::Cfg<128>::TWN : (N == 256 ? fz::Cfg<256>::TWN : (N == 512 ? fz::Cfg<512>::TWN : fz::Cfg<1024>::TWN))));
   switch (N) {
     case 64: fz::pass1_twiddles<64>(tw.data()); break;
@@ -2098,6 +2323,7 @@ int fused_ensure(pf_plan* p) {
       PF_CK(encode_pk_map(&f->tm_pkp, f->b.Y, N, PF_PKP_CP, 3));
     }
     PF_CK(encode_axis1_map(&f->tm_xr, f->b.XR, N, cm, 3));
+    PF_CK(encode_axis1_map(&f->tm_xu, f->b.XU, N, cm, 3));
     f->b.tma = f->b.tma_yx = 1;
   }
   // 2D transform over axes (1, 2) batched over (component, i0): the Y-space
@@ -2144,6 +2370,7 @@ void fused_free(pf_plan* p) {
   cudaFree(f->ws);
   cudaFree(f->spec);
   cudaFree(f->peers);
+  cudaFree(f->grp);
   delete f;
   p->fused = nullptr;
 }
@@ -2214,6 +2441,15 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
     int o = 0;
     PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fz::k_rs_compact<N, false>, fz::RS2<N>::T,
                                                              fz::RSC<N>::bytes(f->c_cs)));
+  {
+    PF_CK_CUDA(smem_attr(fz::k_rsfix_tma<N>, fz::RSFX<N>::bytes(f->c_cs)));
+    int ox = 0;
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, fz::k_rsfix_tma<N>, fz::RS2<N>::T,
+                                                             fz::RSFX<N>::bytes(f->c_cs)));
+    f->nb_rsfx = (ox < 1 ? 1 : (ox > 8 ? 8 : ox)) * kSMs;
+    const char* e = getenv("POREFLOW_B200_RSFIX_TMA");
+    f->rsfix_tma = e ? e[0] == '1' : PF_RSFIX_TMA;
+  }
     f->nb_compact = (o < 1 ? 1 : (o > kRsMaxBlocks / kSMs ? kRsMaxBlocks / kSMs : o)) * kSMs;
     f->nb_rs = f->nb_compact;
   }
@@ -2291,7 +2527,7 @@ template <int N, bool INV>
 static cudaError_t launch_m1_pipe(pf_plan* p, FusedPlan* f, const CUtensorMap& tm) {
   if constexpr (N == 128 || N == 256) {
     return launch_k(fz::k_m1_pipe<N, INV>, f->nb_m1, fz::MP<N>::T, fz::MP<N>::BYTES, p->work, f->b,
-                    (const Ctrl*)p->ctrl, tm);
+                    (const Ctrl*)p->ctrl, tm, f->tm_xu);
   } else {
     (void)p, (void)f, (void)tm;
     return cudaErrorInvalidValue;
@@ -2345,10 +2581,10 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   if (f->m_pipe && f->b.tma) {  // persistent main tiles + k_maxis on the Nyquist tiles
     PF_CK_CUDA((launch_m1_pipe<N, true>(p, f, f->tm_y)));
     PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, 3 * (N / fz::M2<N>::CM), fz::M2<N>::T, smem_mi<N>(), p->work,
-                        f->b, (const Ctrl*)p->ctrl, f->tm_y, 1));
+                        f->b, (const Ctrl*)p->ctrl, f->tm_y, 1, f->tm_xu));
   } else {
     PF_CK_CUDA(launch_k(fz::k_maxis<N, true, false>, m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work, f->b,
-                        (const Ctrl*)p->ctrl, f->tm_y, 0));
+                        (const Ctrl*)p->ctrl, f->tm_y, 0, f->tm_xu));
   }
   PF_CK(mark(2));
   if (f->compact) {
@@ -2360,10 +2596,18 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   }
   PF_CK(mark(3));
 #if PF_ABL_NOFIN == 0
-  PF_CK_CUDA(k_stokes_finalize_launch_pdl(p, f->b.part_rs, nb_part, f->b.part_pk, pk_tiles));
+  if (f->b.crs && !(f->pk_pipe && f->b.tma)) {  // grouped partials (the pipelined PK keeps per-CTA rows)
+    PF_CK_CUDA(k_stokes_finalize_launch_pdl(p, f->b.grs, (nb_part + PF_GRP_RS - 1) / PF_GRP_RS, f->b.gpk,
+                                            (pk_tiles + PF_GRP_PK - 1) / PF_GRP_PK));
+  } else {
+    PF_CK_CUDA(k_stokes_finalize_launch_pdl(p, f->b.part_rs, nb_part, f->b.part_pk, pk_tiles));
+  }
 #endif
   PF_CK(mark(4));
   if (PF_ABL_NORSF) {
+  } else if (f->compact && f->rsfix_tma) {
+    PF_CK_CUDA(launch_k(fz::k_rsfix_tma<N>, f->nb_rsfx, fz::RS2<N>::T, fz::RSFX<N>::bytes(f->c_cs), p->work, f->b,
+                        (const double*)p->s_u, (const uint8_t*)p->s_solid, compact_of(f), (const Ctrl*)p->ctrl));
   } else if (f->compact) {
     PF_CK_CUDA(launch_k(fz::k_rsfix_compact<N, false>, f->nb_rs, fz::RS2<N>::T, smem_rsfix<N>(), p->work, f->b,
                         (const double*)p->s_u, (const uint8_t*)p->s_solid, compact_of(f), (const Ctrl*)p->ctrl));
@@ -2375,10 +2619,10 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   if (f->m_pipe && f->b.tma) {
     PF_CK_CUDA((launch_m1_pipe<N, false>(p, f, f->tm_xr)));
     PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, 3 * (N / fz::M2<N>::CM), fz::M2<N>::T, smem_mf<N>(),
-                        p->work, f->b, (const Ctrl*)p->ctrl, f->tm_xr, 1));
+                        p->work, f->b, (const Ctrl*)p->ctrl, f->tm_xr, 1, f->tm_xu));
   } else {
     PF_CK_CUDA(launch_k(fz::k_maxis<N, false, false>, m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work, f->b,
-                        (const Ctrl*)p->ctrl, f->tm_xr, 0));
+                        (const Ctrl*)p->ctrl, f->tm_xr, 0, f->tm_xu));
   }
   PF_CK(mark(6));
   return PF_OK;
@@ -2652,7 +2896,7 @@ static int fslab_rs_t(pf_plan* p, int c0, int nc, double* totals) {
   f->b.pst = nc == 3 ? f->nb_rs : 3 * f->nb_rs;
   f->b.poff = nc == 3 ? 0 : c0 * f->nb_rs;
   f->rs_rows = f->b.pst;
-  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl, f->tm_y, 0);
+  fz::k_maxis<N, true, true><<<m_tiles, fz::M2<N>::T, smem_mi<N>(), p->work>>>(f->b, p->ctrl, f->tm_y, 0, f->tm_y);
   PF_CK_CUDA(cudaGetLastError());
   if (f->compact) {
     fz::k_rs_compact<N, true><<<f->nb_rs, fz::RS2<N>::T, fz::RSC<N>::bytes(f->c_cs), p->work>>>(
@@ -2688,7 +2932,8 @@ static int fslab_mf_t(pf_plan* p, int c0, int nc, bool fix) {
   const int m_tiles = nc * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
   f->b.c0 = c0;
   f->b.nc = nc;
-  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_xr, 0);
+  fz::k_maxis<N, false, true><<<m_tiles, fz::M2<N>::T, smem_mf<N>(), p->work>>>(f->b, p->ctrl, f->tm_xr, 0,
+                                                                               f->tm_xr);
   PF_CK_CUDA(cudaGetLastError());
   f->b.c0 = 0;
   f->b.nc = 3;

@@ -20,6 +20,16 @@
 
 #include "pf_internal.cuh"
 
+#ifndef PF_ABL_FINTRIV
+#define PF_ABL_FINTRIV 0
+#endif
+#ifndef PF_ABL_NOADAPT
+#define PF_ABL_NOADAPT 0
+#endif
+#ifndef PF_ABL_NODB
+#define PF_ABL_NODB 0
+#endif
+
 namespace pf {
 
 struct Tables {
@@ -156,6 +166,10 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
     int nb1, double* __restrict__ hist, const StokesConst C, const double inv_n) {
   pdl_wait();
   if (ctrl->done) return;
+#if PF_ABL_FINTRIV  // measurement only: the launch without its work (results invalid)
+  if (threadIdx.x == 0) ctrl->iter += 1;
+  return;
+#endif
   double S[6], P[3];
   reduce_partials<6>(part3, nb3, S);
   reduce_partials<3>(part1, nb1, P);
@@ -209,10 +223,14 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
       else if (shrink > C.thr[k])
         v[k] = pymax(v[k] / C.growth[k], C.floor_[k]);
     }
+#if PF_ABL_NOADAPT  // measurement only: penalties frozen (results invalid)
+    (void)v;
+#else
     ctrl->alpha = v[0];
     ctrl->beta = v[1];
     ctrl->b = v[2];
-    ctrl->db = v[2] - b;
+    ctrl->db = PF_ABL_NODB ? 0.0 : v[2] - b;  // (NODB: measurement only, results invalid)
+#endif
   }
   if (it >= C.max_iter) ctrl->done = 1;
 }
