@@ -145,6 +145,23 @@ __device__ __forceinline__ size_t ymain(int yb, int c, int i0, int k1, int k2) {
             : (((size_t)(c * N + i0) * N + k1) * H + k2);
 }
 
+#ifndef PF_PART_EVICT_LAST
+#define PF_PART_EVICT_LAST 1  // per-block partials stored with an L2 evict_last hint (the finalize reads them)
+#endif
+// Partial sums are read by the one-block finalize after the next passes have
+// streamed gigabytes through L2; an evict_last store keeps them resident.
+__device__ __forceinline__ void st_part(double* p, double v) {
+#if PF_PART_EVICT_LAST
+  asm volatile(
+      "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+      " st.global.L2::cache_hint.f64 [%0], %1, pol;\n}" ::"l"(p),
+      "d"(v)
+      : "memory");
+#else
+  *p = v;
+#endif
+}
+
 #ifndef PF_GRP_PK
 #define PF_GRP_PK 64  // PK tiles per partial group
 #endif
@@ -419,7 +436,7 @@ __global__ void __launch_bounds__(RS2<N>::T) k_rs(Bufs B, State st, const Ctrl* 
     group_reduce<6>(acc, B.part_rs, gridDim.x, B.grs, B.crs, PF_GRP_RS);
   } else if (t == 0) {
     for (int k = 0; k < 6; ++k)
-      B.part_rs[SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x] = acc[k];
+      st_part(B.part_rs + (SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x), acc[k]);
   }
 }
 
@@ -727,7 +744,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     group_reduce<6>(acc, B.part_rs, gridDim.x, B.grs, B.crs, PF_GRP_RS);
   } else if (t == 0) {
     for (int k = 0; k < 6; ++k)
-      B.part_rs[SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x] = acc[k];
+      st_part(B.part_rs + (SL ? (size_t)k * B.pst + B.poff + blockIdx.x : (size_t)k * gridDim.x + blockIdx.x), acc[k]);
   }
 }
 
@@ -1734,7 +1751,7 @@ __global__ void __launch_bounds__(PK2<N>::T, PK2<N>::MINB) k_pk(Bufs B, SpecArgs
   if (!SL && B.cpk && tile0 == 0 && (int)gridDim.x == nparts) {
     group_reduce<3>(acc, B.part_pk, nparts, B.gpk, B.cpk, PF_GRP_PK);
   } else if (t == 0) {
-    for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * nparts + pbase + blockIdx.x] = acc[k];
+    for (int k = 0; k < 3; ++k) st_part(B.part_pk + (size_t)k * nparts + pbase + blockIdx.x, acc[k]);
   }
 #if PF_PK_TMASTORE
   if (!SL && tma && C::M == 1 && t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

@@ -23,6 +23,9 @@
 #ifndef PF_ABL_FINTRIV
 #define PF_ABL_FINTRIV 0
 #endif
+#ifndef PF_ABL_NORED
+#define PF_ABL_NORED 0
+#endif
 #ifndef PF_ABL_NOADAPT
 #define PF_ABL_NOADAPT 0
 #endif
@@ -171,8 +174,14 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
   return;
 #endif
   double S[6], P[3];
+#if PF_ABL_NORED  // measurement only: partial reductions skipped (results invalid)
+  for (int k = 0; k < 6; ++k) S[k] = 1.0 + k;
+  for (int k = 0; k < 3; ++k) P[k] = 1.0 + k;
+  (void)part3, (void)nb3, (void)part1, (void)nb1;
+#else
   reduce_partials<6>(part3, nb3, S);
   reduce_partials<3>(part1, nb1, P);
+#endif
   if (threadIdx.x != 0) return;
   const double alpha = ctrl->alpha, beta = ctrl->beta, b = ctrl->b;
   const double er = C.eps_rel;
