@@ -26,12 +26,19 @@
 // The real fields chi and grad chi are materialised only at the end (cuFFT
 // from chi^), exactly as Re ifftn of the spectra the reference inverts.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "pf_fft.cuh"
 
 #ifndef PF_TPK_TMA
 #define PF_TPK_TMA 1  // PK_T loads its two component pencils with 3D TMA tensor copies (N = 128/256)
+#endif
+#ifndef PF_TM_PIPE
+// persistent transport axis-1 passes (POREFLOW_B200_M_PIPE=0/1 overrides).  Measured at 128^3:
+// one solve 15.5 -> 14.95 Gvox-it/s (MI_T / MF_T slower alone: 0.0266 -> 0.0283, 0.0287 -> 0.0317 ms),
+// three concurrent load cases 17.7 -> 18.3; off by default (a single solve is the common call)
+#define PF_TM_PIPE(N) 0
 #endif
 #ifndef PF_TPK_TMASTORE
 #define PF_TPK_TMASTORE 1  // PK_T stores Y with TMA tensor stores from its boxes (N = 128/256)
@@ -300,7 +307,7 @@ struct TM {
 // FWD (MF_T): outputs oc = 0 Y_b <- FFT(X0) + i k1 FFT(X2); 1 Y_w0 <- FFT(X1).
 template <int N, bool INV>
 __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBufs B, const double* __restrict__ kap1, const Ctrl* __restrict__ ctrl,
-                                                                          const __grid_constant__ CUtensorMap tmap) {
+                                                                          const __grid_constant__ CUtensorMap tmap, int nyq_only) {
   using C = Cfg<N>;
   using K = TM<N>;
   constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T;
@@ -311,7 +318,9 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
   double2* S = (double2*)reg;
   double2* tw = (double2*)(reg + K::REGION);
   const int t = threadIdx.x, g = t / C::G, l = t % C::G;
-  const int oc = blockIdx.x / K::TPC, tile = blockIdx.x % K::TPC;
+  // nyq_only (beside k_taxis_pipe): block -> (output, Nyquist tile)
+  const int oc = nyq_only ? blockIdx.x / (N / CM) : blockIdx.x / K::TPC;
+  const int tile = nyq_only ? N * NCH + blockIdx.x % (N / CM) : blockIdx.x % K::TPC;
   const bool nyq = tile >= N * NCH;
   const int i0 = nyq ? 0 : tile / NCH, ch = nyq ? 0 : tile % NCH;
   const int i0b = nyq ? (tile - N * NCH) * CM : 0;
@@ -427,6 +436,116 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
     } else {
       if (nyq) B.Yn[o] = v; else B.Y[o] = v;
     }
+  }
+}
+
+// ------------------------------------------------------------------ MI_T / MF_T, persistent pipelined
+// N = 128 / 256 main tiles (the Nyquist tiles stay on k_taxis with nyq_only): one CTA
+// per slot walks the (output, tile) units with a two-stage TMA ring, as the Stokes
+// k_m1_pipe — at 128^3 the per-CTA fixed costs of the non-persistent passes show.
+// A unit's stage holds its input tile(s): MI_T one (Y0, Y1 or Y0 for i k1 Y0), MF_T
+// output 0 two (X2, X0: Y_b = FFT(X0) + i k1 FFT(X2)), output 1 one (X1).
+template <int N, bool INV>
+struct TMP {
+  using C = Cfg<N>;
+  static constexpr int T = TM<N>::T, CM = TM<N>::CM, NCH = TM<N>::NCH;
+  static constexpr size_t TILE = TM<N>::TILE;
+  static constexpr int TPS = INV ? 1 : 2;  // tiles per stage
+  static constexpr size_t STAGE = TPS * TILE;
+  static constexpr int STAGES = 2;
+  static constexpr size_t SEQ = TM<N>::SEQ;
+  static constexpr size_t BYTES = 1024 + STAGES * STAGE + SEQ + sizeof(double2) * C::TWN;
+  static constexpr int NOUT = INV ? 3 : 2;
+  static constexpr int UNITS = NOUT * N * NCH;
+  static_assert(C::M == 1 && CM * 16 == 128 && TILE % 1024 == 0, "pipelined transport axis-1 pass: N <= 256");
+};
+
+template <int N, bool INV>
+__global__ void __launch_bounds__(TMP<N, INV>::T, 1) k_taxis_pipe(TBufs B, const double* __restrict__ kap1,
+                                                                 const Ctrl* __restrict__ ctrl,
+                                                                 const __grid_constant__ CUtensorMap tmap) {
+  using C = Cfg<N>;
+  using K = TMP<N, INV>;
+  constexpr int H = C::H, SS = C::SS, CM = K::CM, NCH = K::NCH, T = K::T, NU = K::UNITS;
+  constexpr int IPT = TM<N>::IPT;
+  pdl_wait();
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char tpraw[];
+  unsigned char* base = tpraw + ((1024 - (fz::su32(tpraw) & 1023)) & 1023);
+  double2* S = (double2*)(base + K::STAGES * K::STAGE);
+  double2* tw = (double2*)(base + K::STAGES * K::STAGE + K::SEQ);
+  __shared__ uint64_t full[K::STAGES];
+  const int t = threadIdx.x, g = t / C::G, l = t % C::G;
+
+  auto ins = [&](int oc, int k) {  // input component of tile slot k of output oc
+    if (INV) return oc == 1 ? 1 : 0;
+    return oc == 0 ? (k == 0 ? 2 : 0) : 1;
+  };
+  auto issue = [&](int u, int s) {
+    const int oc = u / (N * NCH), r = u % (N * NCH), i0 = r / NCH, ch = r % NCH;
+    const int nt = (!INV && oc == 0) ? 2 : 1;
+    unsigned char* dst = base + (size_t)s * K::STAGE;
+    fz::fence_async_smem();
+    fz::mbar_expect(&full[s], (uint32_t)(nt * K::TILE));
+    for (int k = 0; k < nt; ++k)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              fz::su32(dst + k * K::TILE)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CM), "r"((ins(oc, k) * N + i0) * N), "r"(fz::su32(&full[s]))
+          : "memory");
+  };
+  if (t == 0) {
+    for (int s = 0; s < K::STAGES; ++s) fz::mbar_init(&full[s]);
+    for (int s = 0; s < K::STAGES; ++s)
+      if ((int)blockIdx.x + s * (int)gridDim.x < NU) issue(blockIdx.x + s * gridDim.x, s);
+  }
+  for (int j = t; j < C::TWN; j += T) tw[j] = B.tw[j];
+  __syncthreads();
+  constexpr int A = C::A, BB = C::B;
+  int it = 0;
+  for (int u = blockIdx.x; u < NU; u += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int oc = u / (N * NCH), r = u % (N * NCH), i0 = r / NCH, ch = r % NCH;
+    const unsigned char* st = base + (size_t)s * K::STAGE;
+    const bool two = !INV && oc == 0;
+    fz::mbar_wait(&full[s], (it >> 1) & 1);
+    double2 x[A > BB ? A : BB];
+    auto load = [&](int k) {  // tile slot k, column g -> x
+      if (l < BB) {
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {
+          const int e = BB * n1 + l;
+          x[n1] = *reinterpret_cast<const double2*>(st + k * K::TILE + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
+          if (INV && oc == 2) x[n1] = cik(__ldg(kap1 + e), x[n1]);
+        }
+      }
+    };
+    double2 v2[IPT];
+    load(0);
+    if (two) {  // i k1 FFT(X2) (slot 0), kept in registers, then FFT(X0) (slot 1)
+      fz::fft_seq_x<N, false>(x, S + g * SS, tw, l, true);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        const int idx = t + T * j, q = idx % CM, e = idx / CM;
+        v2[j] = cik(__ldg(kap1 + e), S[q * SS + C::kp(e)]);
+      }
+      load(1);
+    }
+    __syncthreads();  // stage s read (and S free): refill the stage two grid strides ahead
+    if (t == 0 && u + K::STAGES * (int)gridDim.x < NU) issue(u + K::STAGES * gridDim.x, s);
+    if (two) fz::fft_seq_x<N, false>(x, S + g * SS, tw, l, true);
+    else fz::fft_seq_x<N, INV>(x, S + g * SS, tw, l, true);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const int idx = t + T * j, q = idx % CM, e = idx / CM;
+      double2 v = S[q * SS + (INV ? C::sp(e) : C::kp(e))];
+      if (two) v = cadd(v, v2[j]);
+      const size_t o = ((size_t)(oc * N + i0) * N + e) * H + ch * CM + q;
+      if (INV) B.X[o] = v; else B.Y[o] = v;
+    }
+    __syncthreads();  // S is rewritten by the next unit
   }
 }
 
@@ -689,6 +808,7 @@ struct FusedTPlan {
   int nb_trs = kSMs;  // persistent RS grid: one wave of resident blocks (occupancy API)
   CUtensorMap tm_y{}, tm_x{};  // axis-1 TMA maps of Y (2 components) and X (3)
   CUtensorMap tm_pk{};         // PK_T pencil map of Y
+  int m_pipe = 0, nb_tmi = kSMs, nb_tmf = kSMs;  // persistent transport axis-1 passes (k_taxis_pipe)
 };
 
 static FusedTPlan* ftp(pf_plan* p) { return reinterpret_cast<FusedTPlan*>(p->tfused); }
@@ -702,6 +822,19 @@ static int tset_attrs(FusedTPlan* f) {
   int o = 0;
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ft::k_trs<N>, ft::TRS<N>::T, ft::TRS<N>::BYTES));
   f->nb_trs = (o < 1 ? 1 : o) * kSMs;
+  if constexpr (N == 128 || N == 256) {
+    PF_CK_CUDA(smem_attr(ft::k_taxis_pipe<N, true>, ft::TMP<N, true>::BYTES));
+    PF_CK_CUDA(smem_attr(ft::k_taxis_pipe<N, false>, ft::TMP<N, false>::BYTES));
+    int oi = 0, of = 0;
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oi, ft::k_taxis_pipe<N, true>, ft::TMP<N, true>::T,
+                                                             ft::TMP<N, true>::BYTES));
+    PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, ft::k_taxis_pipe<N, false>, ft::TMP<N, false>::T,
+                                                             ft::TMP<N, false>::BYTES));
+    f->nb_tmi = (oi < 1 ? 1 : oi) * kSMs;
+    f->nb_tmf = (of < 1 ? 1 : of) * kSMs;
+    const char* e = getenv("POREFLOW_B200_M_PIPE");
+    f->m_pipe = e ? e[0] == '1' : PF_TM_PIPE(N);
+  }
   return PF_OK;
 }
 
@@ -832,6 +965,17 @@ static int tfinish_t(pf_plan* p) {
   return PF_OK;
 }
 
+template <int N, bool INV>
+static cudaError_t launch_taxis_pipe(pf_plan* p, FusedTPlan* f, const CUtensorMap& tm) {
+  if constexpr (N == 128 || N == 256) {
+    return launch_k(ft::k_taxis_pipe<N, INV>, INV ? f->nb_tmi : f->nb_tmf, ft::TMP<N, INV>::T,
+                    ft::TMP<N, INV>::BYTES, p->work, f->b, (const double*)p->kap[1], (const Ctrl*)p->ctrl, tm);
+  } else {
+    (void)p, (void)f, (void)tm;
+    return cudaErrorInvalidValue;
+  }
+}
+
 template <int N>
 static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   FusedTPlan* f = ftp(p);
@@ -845,8 +989,14 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK_CUDA(launch_k(ft::k_tpk<N>, ft::TPK<N>::TILES, ft::TPK<N>::T, ft::TPK<N>::BYTES, p->work, f->b, P,
                       (const Ctrl*)p->ctrl, f->tm_pk));
   PF_CK(mark(1));
-  PF_CK_CUDA(launch_k(ft::k_taxis<N, true>, 3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
-                      (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_y));
+  if (f->m_pipe) {  // persistent main tiles + k_taxis on the Nyquist tiles
+    PF_CK_CUDA((launch_taxis_pipe<N, true>(p, f, f->tm_y)));
+    PF_CK_CUDA(launch_k(ft::k_taxis<N, true>, 3 * (N / ft::TM<N>::CM), ft::TM<N>::T, ft::TM<N>::BYTES, p->work,
+                        f->b, (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_y, 1));
+  } else {
+    PF_CK_CUDA(launch_k(ft::k_taxis<N, true>, 3 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
+                        (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_y, 0));
+  }
   PF_CK(mark(2));
   PF_CK_CUDA(launch_k(ft::k_trs<N>, f->nb_trs, ft::TRS<N>::T, ft::TRS<N>::BYTES, p->work, f->b, P,
                       (const double*)p->t_u, (const uint8_t*)p->s_solid, (const Ctrl*)p->ctrl));
@@ -854,8 +1004,14 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   transport_finalize_launch(p, f->b.part, ft::TPK<N>::TILES, p->g.inv_n);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
-                      (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_x));
+  if (f->m_pipe) {
+    PF_CK_CUDA((launch_taxis_pipe<N, false>(p, f, f->tm_x)));
+    PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * (N / ft::TM<N>::CM), ft::TM<N>::T, ft::TM<N>::BYTES, p->work,
+                        f->b, (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_x, 1));
+  } else {
+    PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
+                        (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_x, 0));
+  }
   PF_CK(mark(5));
   return PF_OK;
 }
