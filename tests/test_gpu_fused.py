@@ -35,8 +35,13 @@ def _hist_close(mine, ref, **kw):
 
 
 @pytest.mark.parametrize("compact", [True, False])
-@pytest.mark.parametrize("n,iters,geom", [(64, 30, "packing"), (64, 12, "sphere"), (128, 4, "packing")])
+@pytest.mark.parametrize("n,iters,geom", [(64, 30, "packing"), (64, 12, "sphere"), (128, 4, "packing"),
+                                          (128, 26, "packing")])
 def test_fused_truncated_vs_oracle(pf, n, iters, geom, compact):
+    """Truncated fused solves against the oracle.  The 26-iteration 128^3 case runs
+    through residual-balancing changes of b (asserted below), i.e. the
+    RS-fix pass and the axis-1 forward pass's X(u~') correction — at 128^3 on the
+    persistent axis-1 kernels (k_m1_pipe)."""
     from oracle import poreflow_oracle as O
 
     ind = (pf.random_packing_geometry(n, seed=3) if geom == "packing"
@@ -52,6 +57,8 @@ def test_fused_truncated_vs_oracle(pf, n, iters, geom, compact):
         assert rel_l2(getattr(h, k), ost[k]) <= FIELD_TOL, (k, rel_l2(getattr(h, k), ost[k]))
     _hist_close(rep.history, ohist)
     np.testing.assert_allclose(rep.meta["final_penalties"], ofp, rtol=1e-12)
+    if iters >= 20:  # the window must contain a change of b (the RS-fix path)
+        assert np.unique(rep.history[:-1, 14]).size > 1
 
 
 def test_fused_matches_cufft_pipeline_full_solve(pf):
