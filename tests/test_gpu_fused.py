@@ -35,13 +35,8 @@ def _hist_close(mine, ref, **kw):
 
 
 @pytest.mark.parametrize("compact", [True, False])
-@pytest.mark.parametrize("n,iters,geom", [(64, 30, "packing"), (64, 12, "sphere"), (128, 4, "packing"),
-                                          (128, 26, "packing")])
+@pytest.mark.parametrize("n,iters,geom", [(64, 30, "packing"), (64, 12, "sphere"), (128, 4, "packing")])
 def test_fused_truncated_vs_oracle(pf, n, iters, geom, compact):
-    """Truncated fused solves against the oracle.  The 26-iteration 128^3 case runs
-    through residual-balancing changes of b (asserted below), i.e. the
-    RS-fix pass and the axis-1 forward pass's X(u~') correction — at 128^3 on the
-    persistent axis-1 kernels (k_m1_pipe)."""
     from oracle import poreflow_oracle as O
 
     ind = (pf.random_packing_geometry(n, seed=3) if geom == "packing"
@@ -57,8 +52,28 @@ def test_fused_truncated_vs_oracle(pf, n, iters, geom, compact):
         assert rel_l2(getattr(h, k), ost[k]) <= FIELD_TOL, (k, rel_l2(getattr(h, k), ost[k]))
     _hist_close(rep.history, ohist)
     np.testing.assert_allclose(rep.meta["final_penalties"], ofp, rtol=1e-12)
-    if iters >= 20:  # the window must contain a change of b (the RS-fix path)
-        assert np.unique(rep.history[:-1, 14]).size > 1
+
+
+@pytest.mark.parametrize("compact", [True, False])
+def test_fused_128_through_b_changes_vs_oracle(pf, compact):
+    """26 iterations of the cfg-3 geometry at 128^3 (seed 0, e1, eps 1e-5, default
+    adaptive penalties): residual balancing changes b inside the window (asserted),
+    so the RS-fix pass and the axis-1 forward pass's X(u~') correction run — at
+    128^3 on the persistent axis-1 kernels (k_m1_pipe)."""
+    from oracle import poreflow_oracle as O
+
+    ind = pf.random_packing_geometry(128, seed=0)
+    g = (1.0, 0.0, 0.0)
+    cfg = pf.StokesConfig.with_tolerance(1e-5, pressure_gradient=g, max_iter=26)
+    st, rep = pf.solve_stokes_device(ind, cfg, pipeline="fused", compact=compact)
+    assert np.unique(rep.history[:-1, 14]).size > 1
+    ost, ohist, _, oit, ofp = O.solve_stokes(ind.values, g, 1e-5, 1e-5, max_iter=26)
+    assert rep.iterations == oit == 26
+    h = st.to_host()
+    for k in ("u", "u_tilde", "q", "a", "lam"):
+        assert rel_l2(getattr(h, k), ost[k]) <= FIELD_TOL, (k, rel_l2(getattr(h, k), ost[k]))
+    _hist_close(rep.history, ohist)
+    np.testing.assert_allclose(rep.meta["final_penalties"], ofp, rtol=1e-12)
 
 
 def test_fused_matches_cufft_pipeline_full_solve(pf):
