@@ -86,6 +86,9 @@
 #ifndef PF_MP_MINB
 #define PF_MP_MINB 1
 #endif
+#ifndef PF_RS_SPLIT
+#define PF_RS_SPLIT 1  // compact RS refills its X rows one step before the rest of its stage
+#endif
 #ifndef PF_RSFIX_TMA
 #define PF_RSFIX_TMA 1  // TMA-staged RS-fix on the single-GPU compact path (POREFLOW_B200_RSFIX_TMA=0/1)
 #endif
@@ -541,10 +544,14 @@ struct RSC {
 
 // o0 / o1 = compact offsets of the tile's first row and of the row after it
 // (loaded by the caller one tile ahead so the issue does not wait on them)
+// part: 0 = every staged input on mbar; 1 = the X rows only (on mbar); 2 = the state
+// rows, indicator and solid range only (on mbar).  The split lets k_rs_compact refill
+// its X rows as soon as they are packed into the inverse sequences, one step before
+// the rest of the stage is consumed.
 template <int N, bool SL>
 __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& st, const Compact& cp, double* su,
                                           double* sc, double2* sx, double2* sxn, uint8_t* sh, uint64_t* mbar,
-                                          uint32_t* ro_slot, const uint32_t* ro) {
+                                          uint32_t* ro_slot, const uint32_t* ro, int part = 0) {
   using K = RS2<N>;
   using C = Cfg<N>;
   const int TPC = (SL ? B.nl : N) * N / K::R;
@@ -552,14 +559,24 @@ __device__ __forceinline__ void rsc_issue(int tile, const Bufs& B, const State& 
   const int64_t row0 = ((int64_t)(tile % TPC) * K::R + (SL ? (int64_t)B.i0a * N : 0));
   const int64_t n = (int64_t)(SL ? B.l0 : N) * N * N;
   constexpr int R = K::R;
+  fence_async_smem();
+  if (part == 1) {
+    mbar_expect(mbar, (uint32_t)(K::XM + K::XN));
+    bulk_load(sx, B.XU + ((int64_t)c * (SL ? B.l0 : N) * N + row0) * C::H, (uint32_t)K::XM, mbar);
+    bulk_load(sxn, B.XUn + (int64_t)c * (SL ? B.l0 : N) * N + row0, (uint32_t)K::XN, mbar);
+    return;
+  }
   const uint32_t o0 = ro[0];
   const uint32_t cb = sizeof(double) * (ro[R] - o0);
   for (int r = 0; r <= R; ++r) ro_slot[r] = ro[r];  // read by the compute phase after the mbarrier wait
-  fence_async_smem();
-  mbar_expect(mbar, (uint32_t)(sizeof(double) * K::V + K::XM + K::XN + K::HB) + 3 * cb);
+  if (part == 2) {
+    mbar_expect(mbar, (uint32_t)(sizeof(double) * K::V + K::HB) + 3 * cb);
+  } else {
+    mbar_expect(mbar, (uint32_t)(sizeof(double) * K::V + K::XM + K::XN + K::HB) + 3 * cb);
+    bulk_load(sx, B.XU + ((int64_t)c * (SL ? B.l0 : N) * N + row0) * C::H, (uint32_t)K::XM, mbar);
+    bulk_load(sxn, B.XUn + (int64_t)c * (SL ? B.l0 : N) * N + row0, (uint32_t)K::XN, mbar);
+  }
   bulk_load(su, st.u + (int64_t)c * n + row0 * N, sizeof(double) * K::V, mbar);
-  bulk_load(sx, B.XU + ((int64_t)c * (SL ? B.l0 : N) * N + row0) * C::H, (uint32_t)K::XM, mbar);
-  bulk_load(sxn, B.XUn + (int64_t)c * (SL ? B.l0 : N) * N + row0, (uint32_t)K::XN, mbar);
   bulk_load(sh, st.H + row0 * N, (uint32_t)K::HB, mbar);
   if (cb) {
     const int64_t base = (int64_t)c * cp.ns + o0;
@@ -608,7 +625,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
   pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar, mbx;  // mbx: the X rows when PF_RS_SPLIT (refilled one step earlier)
   __shared__ uint32_t ros[2][R + 1];
   double2* tw = (double2*)sraw;
   double2* SI = (double2*)(sraw + K::TW);
@@ -629,11 +646,18 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
 #pragma unroll
     for (int r = 0; r <= R; ++r) ro[r] = cp.off[r0 + r];
   };
+  constexpr bool SPLIT = PF_RS_SPLIT;
   if (t == 0) {
     mbar_init(&mbar);
+    mbar_init(&mbx);
     if ((int)blockIdx.x < NT) {
       offs(blockIdx.x);
-      rsc_issue<N, SL>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[0], ro);
+      if (SPLIT) {
+        rsc_issue<N, SL>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbx, ros[0], ro, 1);
+        rsc_issue<N, SL>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[0], ro, 2);
+      } else {
+        rsc_issue<N, SL>(blockIdx.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[0], ro);
+      }
     }
   }
   __syncthreads();
@@ -647,6 +671,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     const bool has_next = tile + (int)gridDim.x < NT;
     if (t == 0 && has_next) offs(tile + gridDim.x);  // next tile's row offsets, loaded early
     mbar_wait(&mbar, phase);
+    if (SPLIT) mbar_wait(&mbx, phase);
     const uint32_t o0 = ros[phase][0];
     int sb[2 > SG ? 2 : SG];
 #pragma unroll
@@ -662,6 +687,8 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     }
     for (int p = t; p < NP; p += T) SI[p * SS + C::kp(H)] = make_double2(sxn[2 * p].x, sxn[2 * p + 1].x);
     __syncthreads();
+    if (SPLIT && t == 0 && has_next)  // the X rows are packed: refill them now
+      rsc_issue<N, SL>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbx, ros[phase ^ 1u], ro, 1);
     if constexpr (W32) {
       fft_units_w32<N, true>(SI, NP, SS, tw, t);
     } else {
@@ -715,7 +742,7 @@ __global__ void __launch_bounds__(RS2<N>::T, PF_RSC_MINB) PF_RSC_MAXNREG k_rs_co
     }
     __syncthreads();
     if (t == 0 && has_next)
-      rsc_issue<N, SL>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[phase ^ 1u], ro);
+      rsc_issue<N, SL>(tile + gridDim.x, B, st, cp, su, sc, sx, sxn, sh, &mbar, ros[phase ^ 1u], ro, SPLIT ? 2 : 0);
     if constexpr (C::M > 1) {
       radix_stage<N, false>(SF, NP, SS, tw, t, T);
       __syncthreads();
