@@ -34,6 +34,9 @@
 #ifndef PF_TPK_TMA
 #define PF_TPK_TMA 1  // PK_T loads its two component pencils with 3D TMA tensor copies (N = 128/256)
 #endif
+#ifndef PF_TRS_SPLIT
+#define PF_TRS_SPLIT 1  // RS_T refills its X rows as soon as they are packed (second mbarrier)
+#endif
 #ifndef PF_TM_PIPE
 // persistent transport axis-1 passes (POREFLOW_B200_M_PIPE=0/1 overrides).  Measured at 128^3:
 // one solve 15.5 -> 14.95 Gvox-it/s (MI_T / MF_T slower alone: 0.0266 -> 0.0283, 0.0287 -> 0.0317 ms),
@@ -581,22 +584,26 @@ struct TRS {
   static constexpr uint32_t TX = (uint32_t)(XM + XN + UB + HB);
 };
 
+// part: 0 = every staged input; 1 = the X rows only; 2 = u and the indicator only (the
+// X rows are packed into the inverse sequences one step before u / H are consumed).
 template <int N>
 __device__ __forceinline__ void trs_issue(int tile, const TBufs& B, const double* u, const uint8_t* Hs, double2* sx,
-                                          double2* sxn, double* su, uint8_t* sh, uint64_t* mbar) {
+                                          double2* sxn, double* su, uint8_t* sh, uint64_t* mbar, int part = 0) {
   using K = TRS<N>;
   using C = Cfg<N>;
   constexpr int R = K::R, H = C::H;
   const int64_t row0 = (int64_t)tile * R;
   const int64_t n = (int64_t)N * N * N, NN = (int64_t)N * N;
   fz::fence_async_smem();
-  fz::mbar_expect(mbar, K::TX);
+  fz::mbar_expect(mbar, part == 0 ? K::TX : (part == 1 ? (uint32_t)(K::XM + K::XN) : (uint32_t)(K::UB + K::HB)));
   for (int c = 0; c < 3; ++c) {
-    fz::bulk_load(sx + c * R * H, B.X + (c * NN + row0) * H, sizeof(double2) * R * H, mbar);
-    fz::bulk_load(sxn + c * R, B.Xn + c * NN + row0, sizeof(double2) * R, mbar);
-    fz::bulk_load(su + c * K::V, u + c * n + row0 * N, sizeof(double) * K::V, mbar);
+    if (part != 2) {
+      fz::bulk_load(sx + c * R * H, B.X + (c * NN + row0) * H, sizeof(double2) * R * H, mbar);
+      fz::bulk_load(sxn + c * R, B.Xn + c * NN + row0, sizeof(double2) * R, mbar);
+    }
+    if (part != 1) fz::bulk_load(su + c * K::V, u + c * n + row0 * N, sizeof(double) * K::V, mbar);
   }
-  fz::bulk_load(sh, Hs + row0 * N, (uint32_t)K::HB, mbar);
+  if (part != 1) fz::bulk_load(sh, Hs + row0 * N, (uint32_t)K::HB, mbar);
 }
 
 template <int N>
@@ -609,7 +616,8 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
   pdl_wait();
   if (ctrl->done) return;
   extern __shared__ __align__(128) unsigned char sraw[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar, mbx;  // mbx: the X rows (PF_TRS_SPLIT)
+  constexpr bool SPLIT = PF_TRS_SPLIT;
   double2* tw = (double2*)sraw;
   double2* SIq = (double2*)(sraw + K::TW);
   double2* SFq = SIq;  // aliased (see TRS::BYTES)
@@ -622,14 +630,23 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
   const double* kap2 = P.kap[2];
   if (t == 0) {
     fz::mbar_init(&mbar);
-    if ((int)blockIdx.x < NT) trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar);
+    fz::mbar_init(&mbx);
+    if ((int)blockIdx.x < NT) {
+      if (SPLIT) {
+        trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbx, 1);
+        trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar, 2);
+      } else {
+        trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar);
+      }
+    }
   }
   __syncthreads();
   const double pe = P.pe, eta = P.eta, a0 = P.a0, ubg = P.ubg;
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int64_t row0 = (int64_t)tile * R;
-    fz::mbar_wait(&mbar, phase);
+    if (SPLIT) fz::mbar_wait(&mbx, phase);
+    else fz::mbar_wait(&mbar, phase);
     // (1) inverse sequences: per row r  Z = X(d0) + i X(d1);  per pair p  Z = X(d2)_{2p} + i X(d2)_{2p+1}
     for (int idx = t; idx < (R + R / 2) * (H + 1); idx += T) {
       const int sq = idx / (H + 1), k = idx % (H + 1);
@@ -652,12 +669,15 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       }
     }
     __syncthreads();
+    if (SPLIT && t == 0 && tile + (int)gridDim.x < NT)  // the X rows are packed: refill them now
+      trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbx, 1);
     fz::fft_units<N, true>(SIq, K::NSI, SS, tw, g, l, T / C::G);
     if constexpr (C::M > 1) {
       __syncthreads();
       fz::radix_stage<N, true>(SIq, K::NSI, SS, tw, t, T);
     }
     __syncthreads();
+    if (SPLIT) fz::mbar_wait(&mbar, phase);  // u and H of this tile
     // (2) polarization (pure.py:71-87) with A, B, F from H and u (transport.py:112-121);
     // gradients to registers first: the forward sequences overwrite the inverse ones
     double gv[K::VPT][3];
@@ -690,7 +710,8 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       SFq[(2 * row + 1) * SS + C::sp(col)] = make_double2(s, w[2]);
     }
     __syncthreads();
-    if (t == 0 && tile + (int)gridDim.x < NT) trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbar);
+    if (t == 0 && tile + (int)gridDim.x < NT)
+      trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbar, SPLIT ? 2 : 0);
     if constexpr (C::M > 1) {
       fz::radix_stage<N, false>(SFq, K::NSF, SS, tw, t, T);
       __syncthreads();
