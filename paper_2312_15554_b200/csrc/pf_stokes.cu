@@ -89,11 +89,16 @@ __global__ void __launch_bounds__(kThreads) k_stokes_spectral(
       L = L + __ldg(T.ell[ax] + idx[ax]);
       ksq = ksq + kc[c] * kc[c];
     }
+    // every load of the mode first (the D^ load used to sit behind the U^ stores)
     const double2 q = Qh[m];
+    const double2 dprev = Dh[m];
+    double2 rin[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) rin[c] = Rh[(size_t)c * nh + m];
     double2 r[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      const double2 rc = Rh[(size_t)c * nh + m];
+      const double2 rc = rin[c];
       r[c] = make_double2(kc[c] * q.y + rc.x, -(kc[c] * q.x) + rc.y);  // -i k q + R^
       if (zero) r[c].x = r[c].x + g.dn * gp[c];                           // n g_p at k = 0
     }
@@ -114,7 +119,6 @@ __global__ void __launch_bounds__(kThreads) k_stokes_spectral(
     }
     double2 qn = csub(q, cscale(beta, dv));
     if (zero) qn = make_double2(0.0, 0.0);
-    const double2 dprev = Dh[m];
     const double w = parseval_w(g, i2);
     acc[0] += w * cabs2(dv);
     acc[1] += w * cabs2(csub(dv, dprev));
@@ -128,34 +132,114 @@ __global__ void __launch_bounds__(kThreads) k_stokes_spectral(
 }
 
 // ---------------------------------------------------------------------- S3
+// pure.py:59-68 per voxel in the reference's evaluation order (bit-exact with
+// --fmad=false) and the six squared norms of stokes.py:254-277.  Work items are
+// (component, voxel pair): 16-byte loads, and two items per loop trip with all ten
+// loads issued before any arithmetic, so a warp keeps 20 loads in flight — the
+// one-voxel-per-trip form sat at 20 % of DRAM bandwidth, latency-bound with its
+// loads issued behind the previous component's stores.
+struct LocalIn {
+  double2 u1, u0, t0, a0, l0;
+  double h0, h1;
+};
+
+__device__ __forceinline__ void local_load(LocalIn& v, int64_t i, int64_t x, const double* __restrict__ un,
+                                           const double* __restrict__ u, const double* __restrict__ ut,
+                                           const double* __restrict__ a, const double* __restrict__ lam,
+                                           const uint8_t* __restrict__ H) {
+  v.u1 = *reinterpret_cast<const double2*>(un + i);
+  v.u0 = *reinterpret_cast<const double2*>(u + i);
+  v.t0 = *reinterpret_cast<const double2*>(ut + i);
+  v.a0 = *reinterpret_cast<const double2*>(a + i);
+  v.l0 = *reinterpret_cast<const double2*>(lam + i);
+  const uchar2 hh = *reinterpret_cast<const uchar2*>(H + x);
+  v.h0 = (double)hh.x;
+  v.h1 = (double)hh.y;
+}
+
+__device__ __forceinline__ void local_one(double u1, double u0, double t0, double a0, double l0, double h,
+                                          double alpha, double b, double (&acc)[6], double& t1o, double& a1o,
+                                          double& l1o) {
+  const double t1 = ((a0 + b * u1) - h * l0) / (b + alpha * h);  // pure.py:61
+  const double a1 = a0 + b * (u1 - t1);                          // pure.py:66
+  const double l1 = l0 + alpha * (h * t1);                       // pure.py:67
+  const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
+  acc[0] += s0 * s0;   // |H u~'|           r_p1
+  acc[1] += s1 * s1;   // |H (u~' - u~)|    r_d1 / alpha
+  acc[2] += l1 * l1;   // |lam'|
+  acc[3] += s3 * s3;   // |u' - u~'|        r_p3
+  acc[4] += s4 * s4;   // |u' - u|          r_d3 / b
+  acc[5] += a1 * a1;   // |a'|
+  t1o = t1;
+  a1o = a1;
+  l1o = l1;
+}
+
+__device__ __forceinline__ void local_store(const LocalIn& v, int64_t i, double alpha, double b, double (&acc)[6],
+                                            double* __restrict__ u, double* __restrict__ ut, double* __restrict__ a,
+                                            double* __restrict__ lam) {
+  double2 t1, a1, l1;
+  local_one(v.u1.x, v.u0.x, v.t0.x, v.a0.x, v.l0.x, v.h0, alpha, b, acc, t1.x, a1.x, l1.x);
+  local_one(v.u1.y, v.u0.y, v.t0.y, v.a0.y, v.l0.y, v.h1, alpha, b, acc, t1.y, a1.y, l1.y);
+  *reinterpret_cast<double2*>(u + i) = v.u1;
+  *reinterpret_cast<double2*>(ut + i) = t1;
+  *reinterpret_cast<double2*>(a + i) = a1;
+  *reinterpret_cast<double2*>(lam + i) = l1;
+}
+
+#ifndef PF_LOCAL_MINB
+#define PF_LOCAL_MINB 4  // measured (256^3): S3 0.668 ms at 1 item x 2 per trip, 0.642 at 1 item and 4 CTAs/SM
+#endif
+#ifndef PF_LOCAL_TWO
+#define PF_LOCAL_TWO 0  // two work items per loop trip, all loads first (1) or one (0)
+#endif
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_stokes_local(
+__global__ void __launch_bounds__(kThreads, PF_LOCAL_MINB) k_stokes_local(
     const int64_t n, const double* __restrict__ un, double* __restrict__ u, double* __restrict__ ut,
     double* __restrict__ a, double* __restrict__ lam, const uint8_t* __restrict__ H,
     const Ctrl* __restrict__ ctrl, double* __restrict__ part) {
   if (ctrl->done) return;
   const double alpha = ctrl->alpha, b = ctrl->b;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
-    const double h = (double)H[x];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if ((n & 1) == 0) {  // voxel pairs (every field base is 16-byte aligned and c n is even)
+    const int64_t np = n >> 1, items = D * np;
+    int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    auto at = [&](int64_t k, int64_t& x) {
+      const int64_t c = k / np;
+      x = (k - c * np) << 1;
+      return c * n + x;
+    };
+    for (; PF_LOCAL_TWO && it + stride < items; it += 2 * stride) {
+      int64_t xa, xb;
+      const int64_t ia = at(it, xa), ib = at(it + stride, xb);
+      LocalIn va, vb;
+      local_load(va, ia, xa, un, u, ut, a, lam, H);
+      local_load(vb, ib, xb, un, u, ut, a, lam, H);
+      local_store(va, ia, alpha, b, acc, u, ut, a, lam);
+      local_store(vb, ib, alpha, b, acc, u, ut, a, lam);
+    }
+    for (; it < items; it += stride) {
+      int64_t xa;
+      const int64_t ia = at(it, xa);
+      LocalIn va;
+      local_load(va, ia, xa, un, u, ut, a, lam, H);
+      local_store(va, ia, alpha, b, acc, u, ut, a, lam);
+    }
+  } else {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += stride) {
+      const double h = (double)H[x];
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      const int64_t i = c * n + x;
-      const double u1 = un[i], u0 = u[i], t0 = ut[i], a0 = a[i], l0 = lam[i];
-      const double t1 = ((a0 + b * u1) - h * l0) / (b + alpha * h);  // pure.py:61
-      const double a1 = a0 + b * (u1 - t1);                          // pure.py:66
-      const double l1 = l0 + alpha * (h * t1);                       // pure.py:67
-      const double s0 = h * t1, s1 = h * (t1 - t0), s3 = u1 - t1, s4 = u1 - u0;
-      acc[0] += s0 * s0;   // |H u~'|           r_p1
-      acc[1] += s1 * s1;   // |H (u~' - u~)|    r_d1 / alpha
-      acc[2] += l1 * l1;   // |lam'|
-      acc[3] += s3 * s3;   // |u' - u~'|        r_p3
-      acc[4] += s4 * s4;   // |u' - u|          r_d3 / b
-      acc[5] += a1 * a1;   // |a'|
-      u[i] = u1;
-      ut[i] = t1;
-      a[i] = a1;
-      lam[i] = l1;
+      for (int c = 0; c < D; ++c) {
+        const int64_t i = c * n + x;
+        double t1, a1, l1;
+        const double u1 = un[i];
+        local_one(u1, u[i], ut[i], a[i], lam[i], h, alpha, b, acc, t1, a1, l1);
+        u[i] = u1;
+        ut[i] = t1;
+        a[i] = a1;
+        lam[i] = l1;
+      }
     }
   }
   block_sum<6>(acc);
