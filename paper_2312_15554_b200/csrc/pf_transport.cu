@@ -57,6 +57,25 @@ __device__ __forceinline__ void polarize(const Polar& P, double h, const double 
   W[D * n + x] = s;
 }
 
+// the same with the flow components already in registers
+template <int D>
+__device__ __forceinline__ void polarize_u(const Polar& P, double h, const double (&gr)[D], const double (&uu)[D],
+                                           int64_t x, int64_t n, double* __restrict__ W) {
+  const double pore = 1.0 - h;
+  const double A = pore + P.eta * h;
+  const double contrast = A - P.a0;
+  const double pep = P.pe * pore;
+  double s = pep * P.ubg;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const double tg = gr[c] + P.g[c];
+    W[c * n + x] = contrast * tg;
+    const double B = pep * uu[c];
+    s = s - (B - P.b0v[c]) * tg;
+  }
+  W[D * n + x] = s;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_polarize(const int64_t n, Polar P, const double* __restrict__ grad,
                                                        const double* __restrict__ u, const uint8_t* __restrict__ H,
@@ -83,12 +102,15 @@ __global__ void __launch_bounds__(kThreads) k_transport_modes(Geom g, TTables T,
     double kc[D];
     double L = 0.0, bk = 0.0;
     double2 f = WS[(size_t)D * nh + m];
+    double2 wv[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) wv[c] = WS[(size_t)c * nh + m];
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       const int ax = 3 - D + c;
       kc[c] = __ldg(T.kap[ax] + idx[ax]);
       L = L + __ldg(T.ell[ax] + idx[ax]);
-      f = cadd(f, cik(kc[c], WS[(size_t)c * nh + m]));
+      f = cadd(f, cik(kc[c], wv[c]));
       bk = bk + b0[c] * kc[c];
     }
     double2 chi = m == 0 ? make_double2(0.0, 0.0) : cdiv_np(f, make_double2(a0 * L, bk));
@@ -100,7 +122,7 @@ __global__ void __launch_bounds__(kThreads) k_transport_modes(Geom g, TTables T,
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_transport_local(const int64_t n, Polar P, const double* __restrict__ Xn,
+__global__ void __launch_bounds__(kThreads, 4) k_transport_local(const int64_t n, Polar P, const double* __restrict__ Xn,
                                                               double* __restrict__ chi, double* __restrict__ grad,
                                                               const double* __restrict__ u,
                                                               const uint8_t* __restrict__ H, double* __restrict__ W,
@@ -108,20 +130,27 @@ __global__ void __launch_bounds__(kThreads) k_transport_local(const int64_t n, P
   if (ctrl->done) return;
   double acc[2] = {0.0, 0.0};
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
-    const double c1 = Xn[x];
-    const double dc = c1 - chi[x];
-    acc[0] += dc * dc;
-    chi[x] = c1;
-    double gr[D];
+    // every load of the voxel before any store (they used to trail the stores of
+    // the previous field, leaving the kernel latency-bound)
+    const double c1 = Xn[x], c0 = chi[x];
+    const double h = (double)H[x];
+    double gr[D], g0[D], uu[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      const double g1 = Xn[(c + 1) * n + x];
-      const double dg = g1 - grad[c * n + x];
-      acc[1] += dg * dg;
-      grad[c * n + x] = g1;
-      gr[c] = g1;
+      gr[c] = Xn[(c + 1) * n + x];
+      g0[c] = grad[c * n + x];
+      uu[c] = u[c * n + x];
     }
-    polarize<D>(P, (double)H[x], gr, u, x, n, W);
+    const double dc = c1 - c0;
+    acc[0] += dc * dc;
+    chi[x] = c1;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double dg = gr[c] - g0[c];
+      acc[1] += dg * dg;
+      grad[c * n + x] = gr[c];
+    }
+    polarize_u<D>(P, h, gr, uu, x, n, W);
   }
   block_sum<2>(acc);
   if (threadIdx.x == 0) {
