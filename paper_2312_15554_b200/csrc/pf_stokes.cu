@@ -177,7 +177,7 @@ __device__ __forceinline__ void local_one(double u1, double u0, double t0, doubl
 
 __device__ __forceinline__ void local_store(const LocalIn& v, int64_t i, double alpha, double b, double (&acc)[6],
                                             double* __restrict__ u, double* __restrict__ ut, double* __restrict__ a,
-                                            double* __restrict__ lam) {
+                                            double* __restrict__ lam, double* __restrict__ R) {
   double2 t1, a1, l1;
   local_one(v.u1.x, v.u0.x, v.t0.x, v.a0.x, v.l0.x, v.h0, alpha, b, acc, t1.x, a1.x, l1.x);
   local_one(v.u1.y, v.u0.y, v.t0.y, v.a0.y, v.l0.y, v.h1, alpha, b, acc, t1.y, a1.y, l1.y);
@@ -185,8 +185,14 @@ __device__ __forceinline__ void local_store(const LocalIn& v, int64_t i, double 
   *reinterpret_cast<double2*>(ut + i) = t1;
   *reinterpret_cast<double2*>(a + i) = a1;
   *reinterpret_cast<double2*>(lam + i) = l1;
+  // the next right-hand side with the pre-adaptation b (k_form_r_fix adds (b' - b) u~'
+  // in the rare iterations where residual balancing changed b)
+  if (R) *reinterpret_cast<double2*>(R + i) = make_double2(b * t1.x - a1.x, b * t1.y - a1.y);
 }
 
+#ifndef PF_FUSED_FORM_R
+#define PF_FUSED_FORM_R 1  // the local kernel writes R = b u~' - a' (k_form_r_fix corrects a changed b)
+#endif
 #ifndef PF_LOCAL_MINB
 #define PF_LOCAL_MINB 4  // measured (256^3): S3 0.668 ms at 1 item x 2 per trip, 0.642 at 1 item and 4 CTAs/SM
 #endif
@@ -197,7 +203,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads, PF_LOCAL_MINB) k_stokes_local(
     const int64_t n, const double* __restrict__ un, double* __restrict__ u, double* __restrict__ ut,
     double* __restrict__ a, double* __restrict__ lam, const uint8_t* __restrict__ H,
-    const Ctrl* __restrict__ ctrl, double* __restrict__ part) {
+    const Ctrl* __restrict__ ctrl, double* __restrict__ part, double* __restrict__ R) {
   if (ctrl->done) return;
   const double alpha = ctrl->alpha, b = ctrl->b;
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -216,15 +222,15 @@ __global__ void __launch_bounds__(kThreads, PF_LOCAL_MINB) k_stokes_local(
       LocalIn va, vb;
       local_load(va, ia, xa, un, u, ut, a, lam, H);
       local_load(vb, ib, xb, un, u, ut, a, lam, H);
-      local_store(va, ia, alpha, b, acc, u, ut, a, lam);
-      local_store(vb, ib, alpha, b, acc, u, ut, a, lam);
+      local_store(va, ia, alpha, b, acc, u, ut, a, lam, R);
+      local_store(vb, ib, alpha, b, acc, u, ut, a, lam, R);
     }
     for (; it < items; it += stride) {
       int64_t xa;
       const int64_t ia = at(it, xa);
       LocalIn va;
       local_load(va, ia, xa, un, u, ut, a, lam, H);
-      local_store(va, ia, alpha, b, acc, u, ut, a, lam);
+      local_store(va, ia, alpha, b, acc, u, ut, a, lam, R);
     }
   } else {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += stride) {
@@ -239,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, PF_LOCAL_MINB) k_stokes_local(
         ut[i] = t1;
         a[i] = a1;
         lam[i] = l1;
+        if (R) R[i] = b * t1 - a1;
       }
     }
   }
@@ -341,6 +348,20 @@ __global__ void __launch_bounds__(kThreads) k_form_r(const int64_t n, const doub
   }
 }
 
+// R += (b' - b) u~' when the finalize's residual balancing changed b (the local
+// kernel formed R with the pre-adaptation b); a no-op otherwise.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_form_r_fix(const int64_t n, const double* __restrict__ ut,
+                                                         double* __restrict__ R, const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const double db = ctrl->db;
+  if (db == 0.0) return;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) R[c * n + x] = R[c * n + x] + db * ut[c * n + x];
+  }
+}
+
 // ---------------------------------------------------------------------- setup helpers
 // D^ = sum_c i k_c U^_c of the initial velocity (div_prev, stokes.py:370).
 template <int D>
@@ -406,13 +427,17 @@ static int enqueue_stokes_t(pf_plan* p, cudaEvent_t* ev = nullptr) {
   PF_CK(plan_fft(p, false, D, Uh, un));
   PF_CK(mark(2));
   k_stokes_local<D><<<nb3, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid, p->ctrl,
-                                                   part3);
+                                                   part3,
+                                                   PF_FUSED_FORM_R ? R : nullptr);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
   k_stokes_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, part3, nb3, part1, nb1, p->s_hist, C, g.inv_n);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  k_form_r<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 1);
+  if (PF_FUSED_FORM_R)
+    k_form_r_fix<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_ut, R, p->ctrl);
+  else
+    k_form_r<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 1);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(5));
   PF_CK(plan_fft(p, true, D, R, Rh));
@@ -452,7 +477,7 @@ int stokes_spectral_launch(pf_plan* p, const Geom& gs, double2* Qh, const double
 int stokes_local_launch(pf_plan* p, int64_t n, const double* un, double* part3, int* nb3) {
   const int nb = blocks_for(n);
   k_stokes_local<3><<<nb, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid, p->ctrl,
-                                                  part3);
+                                                  part3, nullptr);
   PF_CK_CUDA(cudaGetLastError());
   *nb3 = nb;
   return PF_OK;
