@@ -34,6 +34,9 @@
 #ifndef PF_TPK_TMA
 #define PF_TPK_TMA 1  // PK_T loads its two component pencils with 3D TMA tensor copies (N = 128/256)
 #endif
+#ifndef PF_TF_BOTH
+#define PF_TF_BOTH 1  // MF_T output 0 loads its two input tiles together (TM::TILE2_OFF)
+#endif
 #ifndef PF_TRS_SPLIT
 #define PF_TRS_SPLIT 1  // RS_T refills its X rows as soon as they are packed (second mbarrier)
 #endif
@@ -303,6 +306,10 @@ struct TM {
   static constexpr size_t TILE = sizeof(double2) * CM * N;
   static constexpr size_t REGION = SEQ > TILE ? SEQ : TILE;
   static constexpr size_t BYTES = sizeof(double2) * C::TWN + REGION + 1024;
+  // MF_T output 0 (Y_b) stages its second input tile (X0) beside the first from the
+  // start, so both loads are in flight together (1 KB-aligned, after the twiddles)
+  static constexpr size_t TILE2_OFF = ((REGION + sizeof(double2) * C::TWN + 1023) / 1024) * 1024;
+  static constexpr size_t BYTES_FWD = TMA_OK ? TILE2_OFF + TILE + 1024 : BYTES;
   static constexpr int IPT = N * CM / T;
 };
 
@@ -380,7 +387,45 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
     __syncthreads();
   };
   double2 v2[K::IPT];
-  if (two) {  // i k1 FFT(X2) first, kept in registers
+  const bool both = PF_TF_BOTH && two && tma;  // X2 and X0 loaded together
+  if (both) {
+    unsigned char* reg2 = reg + K::TILE2_OFF;
+    if (t == 0) {
+      fz::mbar_expect(&mbar, (uint32_t)(2 * K::TILE));
+      for (int k = 0; k < 2; ++k)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                fz::su32(k ? reg2 : reg)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CM), "r"(((k ? 0 : 2) * N + i0) * N),
+            "r"(fz::su32(&mbar))
+            : "memory");
+    }
+    __syncthreads();
+    fz::mbar_wait(&mbar, 0);
+    constexpr int A = C::A, BB = C::B;
+    double2 x[A > BB ? A : BB];
+    for (int k = 0; k < 2; ++k) {  // i k1 FFT(X2) into registers, then FFT(X0) into S
+      const unsigned char* src = k ? reg2 : reg;
+      if (l < BB) {
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {
+          const int e = BB * n1 + l;
+          x[n1] = *reinterpret_cast<const double2*>(src + (size_t)e * 128 + ((g ^ (e & 7)) << 4));
+        }
+      }
+      __syncthreads();  // (k = 0: the tile is read before the padded sequences overwrite it)
+      fz::fft_seq_x<N, false>(x, S + g * SS, tw, l, true);
+      __syncthreads();
+      if (k == 0) {
+#pragma unroll
+        for (int j = 0; j < K::IPT; ++j) {
+          const int idx = t + T * j;
+          const int q = idx % CM, e = idx / CM;
+          v2[j] = cik(__ldg(kap1 + e), S[q * SS + C::kp(e)]);
+        }
+      }
+    }
+  } else if (two) {  // i k1 FFT(X2) first, kept in registers
     if (tma) {
       tma_fft(2, false);
     } else {
@@ -400,7 +445,9 @@ __global__ void __launch_bounds__(128, INV ? PF_T_MINB : PF_TF_MINB) k_taxis(TBu
     }
     __syncthreads();
   }
-  if (tma) {
+  if (both) {
+    // (X0's transform is in S)
+  } else if (tma) {
     tma_fft(cin, INV && oc == 2);
   } else {
   stage(cin);
@@ -838,7 +885,7 @@ template <int N>
 static int tset_attrs(FusedTPlan* f) {
   PF_CK_CUDA(smem_attr(ft::k_tpk<N>, (int)ft::TPK<N>::BYTES));
   PF_CK_CUDA(smem_attr(ft::k_taxis<N, true>, (int)ft::TM<N>::BYTES));
-  PF_CK_CUDA(smem_attr(ft::k_taxis<N, false>, (int)ft::TM<N>::BYTES));
+  PF_CK_CUDA(smem_attr(ft::k_taxis<N, false>, (int)ft::TM<N>::BYTES_FWD));
   PF_CK_CUDA(smem_attr(ft::k_trs<N>, (int)ft::TRS<N>::BYTES));
   int o = 0;
   PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ft::k_trs<N>, ft::TRS<N>::T, ft::TRS<N>::BYTES));
@@ -1027,10 +1074,10 @@ static int tenqueue_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK(mark(4));
   if (f->m_pipe) {
     PF_CK_CUDA((launch_taxis_pipe<N, false>(p, f, f->tm_x)));
-    PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * (N / ft::TM<N>::CM), ft::TM<N>::T, ft::TM<N>::BYTES, p->work,
+    PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * (N / ft::TM<N>::CM), ft::TM<N>::T, ft::TM<N>::BYTES_FWD, p->work,
                         f->b, (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_x, 1));
   } else {
-    PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES, p->work, f->b,
+    PF_CK_CUDA(launch_k(ft::k_taxis<N, false>, 2 * ft::TM<N>::TPC, ft::TM<N>::T, ft::TM<N>::BYTES_FWD, p->work, f->b,
                         (const double*)p->kap[1], (const Ctrl*)p->ctrl, f->tm_x, 0));
   }
   PF_CK(mark(5));
