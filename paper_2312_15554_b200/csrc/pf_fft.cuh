@@ -347,6 +347,79 @@ __device__ __forceinline__ void fft256_w32_x(double2* x, double2* s, const doubl
   __syncwarp();
 }
 
+// fft256_w32_x whose result stays in registers (STORE = false: x[k] = X[j + 16 (k + 8 h)],
+// lane = 16 h + j) or goes to out(f, X[f]) (STORE = true) instead of the scratch
+// sequence; s is the warp's padded scratch for the one transpose.
+template <bool INV, bool STORE, typename Out>
+__device__ __forceinline__ void fft256_w32_r(double2* x, double2* s, const double2* __restrict__ tw, int lane,
+                                             Out&& out) {
+  using C = Cfg<256>;
+  const int j = lane & 15, h = lane >> 4;
+  auto merge = [&](void) {
+    Dft<8, INV>::run(x);
+    if (h) {
+#pragma unroll
+      for (int k = 1; k < 8; ++k) x[k] = rot16<INV>(x[k], k);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 y = shfl_xor2(x[k], 16);
+      x[k] = h ? csub(y, x[k]) : cadd(x[k], y);
+    }
+  };
+  merge();
+  {
+    double2 wb[4], wa[2];
+#pragma unroll
+    for (int b = 1; b < 4; ++b) wb[b] = tw[(b - 1) * C::B + j];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int a = 2 * h + q;
+      wa[q] = a == 0 ? make_double2(1.0, 0.0) : tw[(2 + a) * C::B + j];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = k / 4, b = k % 4;
+      if (h == 0 && k == 0) continue;
+      double2 w = b == 0 ? wa[q] : (h == 0 && q == 0 ? wb[b] : cmul(wa[q], wb[b]));
+      if (INV) w.y = -w.y;
+      x[k] = cmul(x[k], w);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[C::pad(k + 8 * h + 16 * j)] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int m = 0; m < 8; ++m) x[m] = s[C::pad(j + 16 * (2 * m + h))];
+  merge();
+  if constexpr (STORE) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out(j + 16 * (k + 8 * h), x[k]);
+  }
+  __syncwarp();  // (the scratch is reused by the caller's next transform)
+}
+
+// Registers of a forward transform (x[k] = X[j + 16 (k + 8 h)]) -> the input layout of
+// the next transform (x[m] = element 16 (2 m + h) + j): lanes j and j + 16 swap four
+// values through one shuffle exchange each.
+__device__ __forceinline__ void w32_regs_to_input(double2* x, int lane) {
+  const int h = lane >> 4;
+  double2 snd[4], rcv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) snd[i] = h ? x[2 * i] : x[2 * i + 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) rcv[i] = shfl_xor2(snd[i], 16);
+  double2 y[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    if (h == 0) y[m] = m < 4 ? x[2 * m] : rcv[m - 4];
+    else y[m] = m < 4 ? rcv[m] : x[2 * m - 7];
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) x[m] = y[m];
+}
+
 template <bool INV>
 __device__ __forceinline__ void fft256_w32(double2* s, const double2* __restrict__ tw, int lane, bool active) {
   using C = Cfg<256>;

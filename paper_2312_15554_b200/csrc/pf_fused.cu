@@ -95,6 +95,15 @@
 #ifndef PF_GROUPED
 #define PF_GROUPED 0  // grouped last-block partial reductions in PK / RS (measured slower at 64^3 / 128^3, neutral at 256^3)
 #endif
+#ifndef PF_PK3
+#define PF_PK3 0  // N = 256 single GPU: register-resident PK (k_pk3; POREFLOW_B200_PK3=0/1)
+#endif
+#ifndef PF_PK3_MINB
+#define PF_PK3_MINB 3
+#endif
+#ifndef PF_PK3_CARVE
+#define PF_PK3_CARVE 100
+#endif
 #ifndef PF_PK_TMASTORE
 #define PF_PK_TMASTORE 1  // k_pk stores Y with TMA tensor stores from its boxes (single GPU, N = 128/256)
 #endif
@@ -2001,6 +2010,158 @@ __global__ void __launch_bounds__(PKP<N>::T, 1) k_pk_pipe(Bufs B, SpecArgs P, co
     for (int k = 0; k < 3; ++k) B.part_pk[(size_t)k * (gridDim.x + N / CPT) + blockIdx.x] = acc[k];
 }
 
+// ------------------------------------------------------------------ PK, register-resident
+// Single GPU, N = 256, main tiles (Nyquist tiles on k_pk).  One warp per column q
+// of the tile transforms that column's three components with whole-warp 256-point
+// transforms (fft256_w32_r), keeping all three spectra in registers (8 modes per
+// lane), so the Green's operator runs on registers — no shared-memory staging of
+// the spectra — and the inverse transforms write straight into the TMA store boxes.
+// Shared memory: the three boxes (48 KB, loaded and stored by TMA) plus one padded
+// transpose scratch per warp.
+template <int N>
+struct PK3 {
+  using C = Cfg<N>;
+  static constexpr int CP = PK2<N>::CP;  // 4 columns: one warp each
+  static constexpr int T = 32 * CP;
+  static constexpr int ROWB = CP * 16;
+  static constexpr size_t BOX = sizeof(double2) * CP * N;
+  static constexpr size_t SCR = sizeof(double2) * C::SS;  // one warp's transpose scratch
+  static constexpr size_t BYTES = 1024 + 3 * BOX + CP * SCR + sizeof(double2) * C::TWN;
+  static_assert(N == 256 && ROWB == 64, "register-resident PK: N = 256, 64-byte box rows");
+};
+
+template <int N>
+__global__ void __launch_bounds__(PK3<N>::T, PF_PK3_MINB) k_pk3(Bufs B, SpecArgs P, const Ctrl* __restrict__ ctrl,
+                                                             const __grid_constant__ CUtensorMap tmap, int nparts) {
+  using C = Cfg<N>;
+  using K = PK3<N>;
+  constexpr int CP = K::CP, NCH = PK2<N>::NCH;
+  pdl_wait();
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char p3raw[];
+  unsigned char* box = p3raw + ((1024 - (su32(p3raw) & 1023)) & 1023);
+  double2* scr = (double2*)(box + 3 * K::BOX);
+  double2* tw = (double2*)(box + 3 * K::BOX + CP * K::SCR);
+  __shared__ uint64_t mbar;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31, j = lane & 15, h = lane >> 4;
+  const int tile = blockIdx.x, k1 = tile / NCH, ch = tile % NCH;
+  const int q = w, k2 = ch * CP + q;
+  const double beta = ctrl->beta, b = ctrl->b;
+  if (t == 0) {
+    mbar_init(&mbar);
+    mbar_expect(&mbar, (uint32_t)(3 * K::BOX));
+    for (int c = 0; c < 3; ++c) {
+      if (B.yb)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+            "%5}], [%6];" ::"r"(su32(box + c * K::BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(0), "r"(k1), "r"(c * (N / 4)),
+            "r"(su32(&mbar))
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(su32(box + c * K::BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * ch * CP), "r"(k1), "r"(c * N), "r"(su32(&mbar))
+            : "memory");
+    }
+  }
+  for (int i = t; i < C::TWN; i += K::T) tw[i] = B.tw[i];
+  // this lane's modes: k0 = j + 16 (k + 8 h), k = 0..7 ([q][k0] in the tile-major Q^, D^)
+  const size_t qd = (size_t)tile * CP * N + (size_t)q * N;
+  auto cell = [&](const unsigned char* bx, int e) {  // column q of box row e (64B swizzle)
+    return reinterpret_cast<double2*>(const_cast<unsigned char*>(bx) + (size_t)e * K::ROWB +
+                                      ((q ^ swz16<K::ROWB>(e)) << 4));
+  };
+  double2* ws = scr + w * C::SS;
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+  double2 X[3][8];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const unsigned char* bx = box + c * K::BOX;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) X[c][m] = *cell(bx, 16 * (2 * m + h) + j);
+    fft256_w32_r<false, false>(X[c], ws, tw, lane, [](int, double2) {});
+  }
+  // Green's operator per mode (pure.py:26-56), D^ = i k.U^, Q^' = Q^ - beta D^, norms
+  double acc[3] = {0.0, 0.0, 0.0};
+  const double kc1 = __ldg(P.kap[1] + k1), kc2 = __ldg(P.kap[2] + k2);
+  const double l12 = __ldg(P.ell[1] + k1) + __ldg(P.ell[2] + k2);
+  const double wgt = (k2 == 0) ? 1.0 : 2.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int k0 = j + 16 * (k + 8 * h);
+    const double2 qq = B.Q[qd + k0];
+    const double2 dpj = B.D[qd + k0];
+    const double kc[3] = {__ldg(P.kap[0] + k0), kc1, kc2};
+    const double L = (__ldg(P.ell[0] + k0) + __ldg(P.ell[1] + k1)) + __ldg(P.ell[2] + k2);
+    const double ksq = (kc[0] * kc[0] + kc[1] * kc[1]) + kc[2] * kc[2];
+    (void)l12;
+    const bool zero = (k0 | k1 | k2) == 0;
+    double2 r[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double2 rc = X[c][k];
+      r[c] = make_double2(kc[c] * qq.y + rc.x, -(kc[c] * qq.x) + rc.y);
+      if (zero) r[c].x = r[c].x + P.dn * P.g[c];
+    }
+    const double A = P.nu * L + b;
+    double2 kr = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) kr = cadd(kr, cscale(kc[c], r[c]));
+    const double Dn = A + beta * ksq;
+    const double rAD = 1.0 / (A * Dn);
+    const double f = beta * A * rAD;
+    const double2 corr = cscale(f, kr);
+    const double invA = Dn * rAD;
+    double2 dv = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double2 u = csub(r[c], cscale(kc[c], corr));
+      u = make_double2(u.x * invA, u.y * invA);
+      dv = cadd(dv, cik(kc[c], u));
+      X[c][k] = make_double2(u.x * P.inv_n, u.y * P.inv_n);
+    }
+    double2 qn = csub(qq, cscale(beta, dv));
+    if (zero) qn = make_double2(0.0, 0.0);
+    acc[0] += wgt * cabs2(dv);
+    acc[1] += wgt * cabs2(csub(dv, dpj));
+    acc[2] += wgt * cabs2(qn);
+    B.Q[qd + k0] = qn;
+    B.D[qd + k0] = dv;
+  }
+  // inverse FFT_0 per component straight into its box (this warp's column only)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    w32_regs_to_input(X[c], lane);
+    unsigned char* bx = box + c * K::BOX;
+    fft256_w32_r<true, true>(X[c], ws, tw, lane, [&](int e, double2 v) { *cell(bx, e) = v; });
+  }
+  fence_async_smem();
+  __syncthreads();
+  if (t == 0) {
+    for (int c = 0; c < 3; ++c) {
+      if (B.yb)
+        asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmap)),
+                     "r"(2 * ch * CP), "r"(0), "r"(k1), "r"(c * (N / 4)), "r"(su32(box + c * K::BOX))
+                     : "memory");
+      else
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmap)),
+                     "r"(2 * ch * CP), "r"(k1), "r"(c * N), "r"(su32(box + c * K::BOX))
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  block_sum<3>(acc);
+  if (t == 0) {
+    for (int k = 0; k < 3; ++k) st_part(B.part_pk + (size_t)k * nparts + blockIdx.x, acc[k]);
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 // natural full spectrum [k0][k1][N/2+1] <-> PK tile-major [tile][q][k0]
 template <int N>
 __global__ void k_tilemajor(const double2* __restrict__ nat, double2* __restrict__ tm, double scale, int to_tm,
@@ -2101,6 +2262,7 @@ struct FusedPlan {
   int m_pipe = 0;              // single GPU, N = 128 / 256: persistent pipelined MI / MF (k_m1_pipe)
   int nb_m1 = 0;
   int pk_pipe = 0;             // single GPU, N = 128 / 256: persistent pipelined PK (k_pk_pipe)
+  int pk3 = 0;                 // single GPU, N = 256: register-resident PK (k_pk3)
   int nb_pkp = 0;              // its grid (resident CTAs)
 };
 
@@ -2159,6 +2321,12 @@ static int set_attrs(FusedPlan* f) {
     if (f->nb_pkp > fz::PKP<N>::UNITS) f->nb_pkp = fz::PKP<N>::UNITS;
     const char* e = getenv("POREFLOW_B200_PK_PIPE");
     f->pk_pipe = e ? e[0] == '1' : PF_PK_PIPE;
+    if constexpr (N == 256) {
+      PF_CK_CUDA(smem_attr(fz::k_pk3<N>, fz::PK3<N>::BYTES));
+      PF_CK_CUDA(cudaFuncSetAttribute(fz::k_pk3<N>, cudaFuncAttributePreferredSharedMemoryCarveout, PF_PK3_CARVE));
+      const char* e3 = getenv("POREFLOW_B200_PK3");
+      f->pk3 = e3 ? e3[0] == '1' : PF_PK3;
+    }
     for (int inv = 0; inv < 2; ++inv) {
       auto kern = inv ? fz::k_m1_pipe<N, true> : fz::k_m1_pipe<N, false>;
       PF_CK_CUDA(smem_attr(kern, (int)fz::MP<N>::BYTES));
@@ -2579,6 +2747,17 @@ static cudaError_t launch_m1_pipe(pf_plan* p, FusedPlan* f, const CUtensorMap& t
 }
 
 template <int N>
+static cudaError_t launch_pk3(pf_plan* p, FusedPlan* f, const fz::SpecArgs& sa, int nparts) {
+  if constexpr (N == 256) {
+    return launch_k(fz::k_pk3<N>, N * fz::PK2<N>::NCH, fz::PK3<N>::T, fz::PK3<N>::BYTES, p->work, f->b, sa,
+                    (const Ctrl*)p->ctrl, f->tm_pk, nparts);
+  } else {
+    (void)p, (void)f, (void)sa, (void)nparts;
+    return cudaErrorInvalidValue;
+  }
+}
+
+template <int N>
 static cudaError_t launch_pk_pipe(pf_plan* p, FusedPlan* f, const fz::SpecArgs& sa) {
   if constexpr (N == 128 || N == 256) {
     return launch_k(fz::k_pk_pipe<N>, f->nb_pkp, fz::PKP<N>::T, fz::PKP<N>::BYTES, p->work, f->b, sa,
@@ -2610,7 +2789,13 @@ static int enqueue_fused_t(pf_plan* p, cudaEvent_t* ev) {
   PF_CK(mark(0));
   int pk_tiles = f->b.l1 * fz::PK2<N>::NCH + f->b.l1 / fz::PK2<N>::CP;
   const int m_tiles = 3 * (f->b.l0 * fz::M2<N>::NCH + f->b.l0 / fz::M2<N>::CM);
-  if (f->pk_pipe && f->b.tma) {  // persistent pipelined PK on the main tiles + k_pk on the N / CP Nyquist tiles
+  if (f->pk3 && f->b.tma) {  // register-resident PK on the main tiles + k_pk on the Nyquist tiles
+    const int main_tiles = N * fz::PK2<N>::NCH, nyq = N / fz::PK2<N>::CP;
+    PF_CK_CUDA((launch_pk3<N>(p, f, sa, main_tiles + nyq)));
+    PF_CK_CUDA(launch_k(fz::k_pk<N, false>, nyq, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
+                        (const Ctrl*)p->ctrl, f->tm_pk, main_tiles, main_tiles, main_tiles + nyq));
+    pk_tiles = main_tiles + nyq;
+  } else if (f->pk_pipe && f->b.tma) {  // persistent pipelined PK on the main tiles + k_pk on the N / CP Nyquist tiles
     const int main_tiles = N * fz::PK2<N>::NCH, nyq = N / fz::PK2<N>::CP;
     PF_CK_CUDA(launch_pk_pipe<N>(p, f, sa));
     PF_CK_CUDA(launch_k(fz::k_pk<N, false>, nyq, fz::PK2<N>::T, smem_pk<N>(), p->work, f->b, sa,
