@@ -146,7 +146,7 @@ def cpu_stokes_rate(n, seed, g, budget_s, max_iters):
 
 
 def run_reference(args):
-    rank, _, world = dist_env()
+    rank, _, _ = dist_env()
     if rank != 0:
         return 0
     n = args.n

@@ -50,7 +50,6 @@ def out_like(x_dev, host: bool):
 
 
 def kappa_tables(symbols, dev):
-    t = torch()
     return [real(np.asarray(k, dtype=np.float64) if not is_tensor(k) else k, dev) for k in symbols.kappa]
 
 
