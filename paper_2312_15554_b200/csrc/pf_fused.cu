@@ -2654,7 +2654,9 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
     PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fz::k_rs_compact<N, false>, fz::RS2<N>::T,
                                                              fz::RSC<N>::bytes(f->c_cs)));
   {
-    PF_CK_CUDA(smem_attr(fz::k_rsfix_tma<N>, fz::RSFX<N>::bytes(f->c_cs)));
+    // (the limit is per function, not per plan: set the worst case so every cell's
+    // staging capacity fits — several cells with different geometries share it)
+    PF_CK_CUDA(smem_attr(fz::k_rsfix_tma<N>, fz::RSFX<N>::bytes(fz::RSC<N>::CS)));
     int ox = 0;
     PF_CK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, fz::k_rsfix_tma<N>, fz::RS2<N>::T,
                                                              fz::RSFX<N>::bytes(f->c_cs)));
