@@ -343,9 +343,17 @@ __device__ __forceinline__ double pymax(double a, double b) { return b > a ? b :
 #ifndef PF_PDL
 #define PF_PDL 1  // measured: +4 % at 64^3, neutral at 128^3 and 256^3
 #endif
+#ifndef PF_PDL_EARLY
+#define PF_PDL_EARLY 0  // trigger the dependent launch right after the wait (instead of at CTA exit)
+#endif
 __device__ __forceinline__ void pdl_wait() {
 #if PF_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if PF_PDL_EARLY
+  // every dependent pass waits on griddepcontrol.wait before touching our outputs,
+  // so letting it launch (and become resident where it fits) early is safe
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 #endif
 }
 
