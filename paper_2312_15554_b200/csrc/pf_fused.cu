@@ -110,6 +110,9 @@
 #ifndef PF_YBLOCK
 #define PF_YBLOCK 1  // single GPU, N <= 256: i0-blocked Y layout (Bufs::yb; POREFLOW_B200_YBLOCK=0 disables)
 #endif
+#ifndef PF_PK128_MINB
+#define PF_PK128_MINB 4  // 128^3: 4 CTAs/SM (128 regs): cell 12.80 -> 12.94, 16-cell ensemble 14.26 -> 14.51 Gvox-it/s
+#endif
 #ifndef PF_PK_THREADS
 #define PF_PK_THREADS 128
 #endif
@@ -1086,7 +1089,7 @@ template <int N>
 struct PK2 {
   using C = Cfg<N>;
   static constexpr int T = N == 512 ? PF_PK512_T : (N == 1024 ? PF_PK1024_T : PF_PK_THREADS);
-  static constexpr int MINB = N == 512 ? PF_PK512_MINB : (N == 1024 ? PF_PK1024_MINB : PF_PK_MINB);
+  static constexpr int MINB = N == 512 ? PF_PK512_MINB : (N == 1024 ? PF_PK1024_MINB : (N == 128 ? PF_PK128_MINB : PF_PK_MINB));
   static constexpr int NGP = T / C::G;
   // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
 #ifdef PF_PK_CP
