@@ -55,6 +55,9 @@
 #ifndef PF_TPK_PREFETCH
 #define PF_TPK_PREFETCH 1  // previous chi^ loaded into registers under the forward FFT (needs 4 CTAs/SM of regs)
 #endif
+#ifndef PF_TPK128_MINB
+#define PF_TPK128_MINB PF_TPK_MINB
+#endif
 #ifndef PF_TPK_MINB
 #define PF_TPK_MINB 4
 #endif
@@ -111,7 +114,7 @@ struct TPK {
 };
 
 template <int N>
-__global__ void __launch_bounds__(128, PF_TPK_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl,
+__global__ void __launch_bounds__(128, N == 128 ? PF_TPK128_MINB : PF_TPK_MINB) k_tpk(TBufs B, TP P, const Ctrl* __restrict__ ctrl,
                                                          const __grid_constant__ CUtensorMap tmap) {
   using C = Cfg<N>;
   using K = TPK<N>;
