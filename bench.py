@@ -229,7 +229,7 @@ def run_ours(args):
     prof_iters = 3
     rows = args.warmup + args.steps + prof_iters + 1
     state = pf.DeviceAdmmState.zeros(ind.grid, dev)
-    solver = pf.StokesSolver(ind, cfg, pen, state, dev, history_rows=rows)
+    solver = pf.StokesSolver(ind, cfg, pen, state, dev, history_rows=rows, cold=True)
     solver.begin()
     solver.iterate(args.warmup, poll=False)
     torch.cuda.synchronize()

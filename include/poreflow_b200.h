@@ -64,6 +64,13 @@ int pf_plan_set_fused(pf_plan* plan, int enable);
  * Stokes path (used when a = 0 on pore voxels, e.g. cold starts): on pore
  * voxels the local step is exactly u~' = u', a' = 0, lam' = lam. */
 int pf_plan_set_compact(pf_plan* plan, int enable);
+/* Promise (cold != 0) that the state passed to the NEXT pf_stokes_begin is all
+ * zero — the reference's default initial state (stokes.py:362) created by the
+ * caller.  The fused pipeline then builds its spectral state, right-hand side and
+ * solid-only storage without transforms (about 2 ms less setup at 256^3).  The
+ * flag is consumed by that begin.  Passing it with a non-zero state is an error
+ * the library does not detect. */
+int pf_plan_set_cold_start(pf_plan* plan, int cold);
 /* Replace the symbol tables of one logical axis (host arrays of dims[axis]
  * doubles: kappa_j and the 1D Laplacian term, spectral.py:78-86).  The
  * Python host layer passes numpy's own tables so the device sees the

@@ -84,6 +84,7 @@ SIGNATURES = {
     "pf_plan_set_stream": [_P, _P],
     "pf_plan_set_fused": [_P, ctypes.c_int],
     "pf_plan_set_compact": [_P, ctypes.c_int],
+    "pf_plan_set_cold_start": [_P, ctypes.c_int],
     "pf_plan_set_symbol_tables": [_P, ctypes.c_int, _P, _P],
     "pf_plan_device_bytes": [_P, ctypes.POINTER(ctypes.c_size_t)],
     "pf_stokes_solve": [_P, ctypes.POINTER(StokesParams), _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(StokesResult)],

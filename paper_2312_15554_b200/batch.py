@@ -73,7 +73,7 @@ def solve_stokes_many_device(indicators: Sequence, cfgs: Sequence[StokesConfig],
         st.wait_stream(main)
         with t.cuda.stream(st):
             state = DeviceAdmmState.zeros(grid, dev)
-            solver = StokesSolver(ind, cfg, pen, state, dev, plan_slot=k).begin()
+            solver = StokesSolver(ind, cfg, pen, state, dev, plan_slot=k, cold=True).begin()
         jobs.append((solver, st))
         owners.append((k, state))
     if jobs:

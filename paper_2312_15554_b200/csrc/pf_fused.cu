@@ -2618,16 +2618,20 @@ static fz::Compact compact_of(FusedPlan* f) {
 }
 
 template <int N>
-static int compact_setup_t(pf_plan* p, FusedPlan* f) {
+static int compact_setup_t(pf_plan* p, FusedPlan* f, bool cold = false) {
   const int64_t rows = (int64_t)f->b.l0 * N, n = rows * N;
   // eligibility (a = 0 on pore voxels: cold starts and states this path produced)
-  // and the constant pore part of |lam'|^2
-  const int nb = blocks_for(3 * n);
-  fz::k_pore_a_lam<<<nb, kThreads, 0, p->work>>>(n, p->s_solid, p->s_a, p->s_lam, p->partials);
-  double* out = p->partials + 24 * kMaxBlocks;
-  PF_CK(reduce_rows_to(p, p->partials, 2, nb, out));
-  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->work));
-  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  // and the constant pore part of |lam'|^2 (a cold start: both zero, no pass)
+  if (cold) {
+    p->h_small[0] = p->h_small[1] = 0.0;
+  } else {
+    const int nb = blocks_for(3 * n);
+    fz::k_pore_a_lam<<<nb, kThreads, 0, p->work>>>(n, p->s_solid, p->s_a, p->s_lam, p->partials);
+    double* out = p->partials + 24 * kMaxBlocks;
+    PF_CK(reduce_rows_to(p, p->partials, 2, nb, out));
+    PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->work));
+    PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  }
   // (solid-only storage: RS tiles of 1024 or 2048 voxels)
   f->compact = (p->compact_enable && p->h_small[0] == 0.0 && fz::RS2<N>::V <= 2048) ? 1 : 0;
   f->nb_rs = f->compact ? f->nb_compact : f->nb_full;
@@ -2677,6 +2681,10 @@ static int compact_setup_t(pf_plan* p, FusedPlan* f) {
     PF_CK_CUDA(cudaMalloc(&f->c_data, sizeof(double) * (size_t)need));
     f->c_cap = need;
   }
+  if (cold) {  // solid u~, a, lam of a zero state: zeros
+    PF_CK_CUDA(cudaMemsetAsync(f->c_data, 0, sizeof(double) * (size_t)need, p->work));
+    return PF_OK;
+  }
   fz::k_compact_move<N><<<blocks_for(3 * rows * 32), kThreads, 0, p->work>>>(p->s_solid, compact_of(f), p->s_ut,
                                                                              p->s_a, p->s_lam, p->s_u, 0, rows);
   PF_CK_CUDA(cudaGetLastError());
@@ -2689,6 +2697,22 @@ int fused_setup(pf_plan* p) {
   const int N = f->N;
   const int64_t n = p->g.nr, nh = p->g.nh, NN = (int64_t)N * N;
   const int grid = blocks_for(nh * 3);
+  if (p->cold_start) {
+    // zero state (pf_plan_set_cold_start): Q^ = D^ = 0 and the Y-space right-hand side
+    // FFT(b*0 - 0) = 0 — no transforms; the solid-only storage starts at zero
+    const size_t H = N / 2, main1 = (size_t)N * N * H, nyq1 = (size_t)N * N;
+    PF_CK_CUDA(cudaMemsetAsync(f->b.Q, 0, sizeof(double2) * (main1 + nyq1), p->work));
+    PF_CK_CUDA(cudaMemsetAsync(f->b.D, 0, sizeof(double2) * (main1 + nyq1), p->work));
+    PF_CK_CUDA(cudaMemsetAsync(f->b.Y, 0, sizeof(double2) * 3 * main1, p->work));
+    PF_CK_CUDA(cudaMemsetAsync(f->b.Yn, 0, sizeof(double2) * 3 * nyq1, p->work));
+    switch (N) {
+      case 64: return compact_setup_t<64>(p, f, true);
+      case 128: return compact_setup_t<128>(p, f, true);
+      case 256: return compact_setup_t<256>(p, f, true);
+      case 512: return compact_setup_t<512>(p, f, true);
+      default: return compact_setup_t<1024>(p, f, true);
+    }
+  }
   // Q^ = FFT(q), gauge Q^(0) = 0
   PF_CK(plan_fft(p, true, 1, p->s_q, p->specB));
   PF_CK(to_tilemajor(N, p->specB, f->b.Q, 1.0, true, p->work));

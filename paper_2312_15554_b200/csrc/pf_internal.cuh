@@ -170,6 +170,7 @@ struct pf_plan {
   void* fused;       // FusedPlan*
   int fused_enable;  // 1 = use the fused pipeline when the grid supports it
   int compact_enable;  // 1 = solid-only multiplier storage on the fused path when eligible
+  int cold_start;      // 1 = the next pf_stokes_begin's state is all zero (pf_plan_set_cold_start)
   int pipeline;      // pipeline of the active Stokes solve: 0 cuFFT, 1 fused
   void* tfused;      // FusedTPlan* (pf_fused_transport.cu)
   int t_pipeline;    // pipeline of the active transport solve: 0 cuFFT, 1 fused

@@ -318,6 +318,12 @@ int pf_plan_set_fused(pf_plan* p, int enable) {
   return PF_OK;
 }
 
+int pf_plan_set_cold_start(pf_plan* p, int cold) {
+  PF_ARG(p, "null plan");
+  p->cold_start = cold ? 1 : 0;
+  return PF_OK;
+}
+
 int pf_plan_set_compact(pf_plan* p, int enable) {
   PF_ARG(p, "null plan");
   p->compact_enable = enable ? 1 : 0;

@@ -600,9 +600,11 @@ int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid,
   p->pipeline = (p->fused_enable && fused_supported(p)) ? 1 : 0;
   if (p->pipeline == 1) {
     PF_CK(fused_ensure(p));
-    PF_CK(fused_setup(p));
-    return PF_OK;
+    const int st = fused_setup(p);
+    p->cold_start = 0;  // consumed
+    return st;
   }
+  p->cold_start = 0;
   switch (d) {
     case 1: PF_CK(stokes_setup_t<1>(p, P->b)); break;
     case 2: PF_CK(stokes_setup_t<2>(p, P->b)); break;

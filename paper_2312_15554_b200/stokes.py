@@ -213,8 +213,12 @@ class StokesSolver:
 
     def __init__(self, indicator: IndicatorField, cfg: StokesConfig, penalties: PenaltyParams,
                  state: DeviceAdmmState, device=None, history_rows: int | None = None,
-                 pipeline: str | None = None, plan_slot: int = 0, compact: bool | None = None):
+                 pipeline: str | None = None, plan_slot: int = 0, compact: bool | None = None,
+                 cold: bool = False):
+        """``cold``: the caller created ``state`` as zeros (the reference's default
+        initial state), so the setup may skip its transforms (pf_plan_set_cold_start)."""
         self.device = require_cuda(device)
+        self.cold = bool(cold)
         self.indicator, self.cfg, self.penalties, self.state = indicator, cfg, penalties, state
         grid = indicator.grid
         self.plan = get_plan(grid.dims, cfg.symbol_mode, self.device, plan_slot)
@@ -241,6 +245,7 @@ class StokesSolver:
         h = self.plan.bind_stream()
         N.check(lib.pf_plan_set_fused(h, 0 if self.pipeline_request == "cufft" else 1))
         N.check(lib.pf_plan_set_compact(h, 1 if self.compact else 0))
+        N.check(lib.pf_plan_set_cold_start(h, 1 if self.cold else 0))
         N.check(lib.pf_stokes_begin(h, ctypes.byref(self._params), self.solid.data_ptr(), s.u.data_ptr(),
                                     s.u_tilde.data_ptr(), s.q.data_ptr(), s.a.data_ptr(), s.lam.data_ptr(),
                                     self.history.data_ptr()))
@@ -296,7 +301,8 @@ def solve_stokes_device(indicator: IndicatorField, cfg: StokesConfig | None = No
             state = DeviceAdmmState.from_host(init, dev)
     else:
         state = DeviceAdmmState.zeros(grid, dev)
-    solver = StokesSolver(indicator, cfg, penalties, state, dev, pipeline=pipeline, compact=compact)
+    solver = StokesSolver(indicator, cfg, penalties, state, dev, pipeline=pipeline, compact=compact,
+                          cold=init is None)
     solver.begin()
     solver.iterate(cfg.max_iter, poll=True)
     solver.end()
