@@ -281,6 +281,31 @@ __device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
   return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
 
+// Radix-2 merge of the lane pair (j, j + 16) after each lane's 8-point DFT (x = E on
+// h = 0, O on h = 1): X[k] = E + w16^k O on h = 0, X[k + 8] = E - w16^k O on h = 1.
+// Every lane runs the same instructions — the rotation by a per-lane factor (1 on
+// h = 0, rot16's (c, s) on h = 1) and the butterfly as one signed FMA — so the warp
+// issues no selects; bitwise the results of the branch / select form (up to the sign
+// of zeros).
+template <bool INV>
+__device__ __forceinline__ void w32_merge(double2* x, int h) {
+  Dft<8, INV>::run(x);
+  const bool odd = h != 0;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    const double c = odd ? c16(k) : 1.0;
+    const double s0 = odd ? c16(k - 4) : 0.0;  // sin(2 pi k / 16)
+    const double s = INV ? s0 : -s0;
+    x[k] = make_double2(__fma_rn(x[k].x, c, -(x[k].y * s)), __fma_rn(x[k].x, s, x[k].y * c));
+  }
+  const double sg = odd ? -1.0 : 1.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 y = shfl_xor2(x[k], 16);
+    x[k] = make_double2(__fma_rn(sg, x[k].x, y.x), __fma_rn(sg, x[k].y, y.y));
+  }
+}
+
 // One 256-point FFT (unnormalised; same input / output positions and padding as
 // fft_seq<256>) by a whole warp: each 16-point DFT of the two passes is split
 // over a lane pair (j, j + 16) as an 8-point DFT of its even / odd inputs and a
@@ -294,18 +319,7 @@ __device__ __forceinline__ void fft256_w32_x(double2* x, double2* s, const doubl
                                              bool active) {
   using C = Cfg<256>;
   const int j = lane & 15, h = lane >> 4;
-  auto merge = [&](void) {
-    Dft<8, INV>::run(x);
-    if (h) {
-#pragma unroll
-      for (int k = 1; k < 8; ++k) x[k] = rot16<INV>(x[k], k);  // O'[k] = w16^k O[k]
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double2 y = shfl_xor2(x[k], 16);
-      x[k] = h ? csub(y, x[k]) : cadd(x[k], y);  // X[k] = E + O' (h = 0), X[k + 8] = E - O' (h = 1)
-    }
-  };
+  auto merge = [&](void) { w32_merge<INV>(x, h); };
   // pass 1: sub-DFT j over n1 (elements 16 n1 + j); this lane's half n1 = 2 m + h
   merge();
   {
@@ -355,18 +369,7 @@ __device__ __forceinline__ void fft256_w32_r(double2* x, double2* s, const doubl
                                              Out&& out) {
   using C = Cfg<256>;
   const int j = lane & 15, h = lane >> 4;
-  auto merge = [&](void) {
-    Dft<8, INV>::run(x);
-    if (h) {
-#pragma unroll
-      for (int k = 1; k < 8; ++k) x[k] = rot16<INV>(x[k], k);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double2 y = shfl_xor2(x[k], 16);
-      x[k] = h ? csub(y, x[k]) : cadd(x[k], y);
-    }
-  };
+  auto merge = [&](void) { w32_merge<INV>(x, h); };
   merge();
   {
     double2 wb[4], wa[2];
