@@ -2606,6 +2606,13 @@ static int to_tilemajor(int N, const double2* src, double2* dst, double scale, b
   return PF_OK;
 }
 
+// exclusive scan of n counts into off[0..n] (one block; setup only)
+int scan_counts(cudaStream_t s, const uint32_t* cnt, uint32_t* off, int64_t n) {
+  fz::k_scan<<<1, 1024, 0, s>>>(cnt, off, n);
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
 static fz::Compact compact_of(FusedPlan* f) {
   fz::Compact c;
   c.off = f->c_off;

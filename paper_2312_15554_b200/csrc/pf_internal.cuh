@@ -172,6 +172,12 @@ struct pf_plan {
   int compact_enable;  // 1 = solid-only multiplier storage on the fused path when eligible
   int cold_start;      // 1 = the next pf_stokes_begin's state is all zero (pf_plan_set_cold_start)
   int pipeline;      // pipeline of the active Stokes solve: 0 cuFFT, 1 fused
+  // solid-only multiplier storage of the cuFFT pipeline (pf_stokes.cu): per-64-voxel
+  // segment counts / bases, [3][d][ns] data (u~, a, lam), on for the active solve
+  uint32_t *gc_cnt, *gc_base;
+  double* gc_data;
+  int64_t gc_ns, gc_cap, gc_nseg;
+  int gc_on;
   void* tfused;      // FusedTPlan* (pf_fused_transport.cu)
   int t_pipeline;    // pipeline of the active transport solve: 0 cuFFT, 1 fused
   void* slab;        // SlabPlan* (pf_slab.cu) for slab-decomposed plans
@@ -228,6 +234,7 @@ int fused_slab_set_peers(pf_plan* p, const uint64_t* yy, const uint64_t* yyn, co
                          const uint64_t* yxn, int npeers);
 int fused_slab_end(pf_plan* p, double2* Tq);
 int fused_is_compact(const pf_plan* p);
+int scan_counts(cudaStream_t s, const uint32_t* cnt, uint32_t* off, int64_t n);
 // fused transport pipeline (pf_fused_transport.cu)
 int tfused_setup(pf_plan* p, bool warm);
 int tfused_finish(pf_plan* p);

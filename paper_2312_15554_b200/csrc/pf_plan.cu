@@ -366,6 +366,9 @@ int pf_plan_destroy(pf_plan* p) {
   cudaFree(p->realA);
   cudaFree(p->realB);
   cudaFree(p->partials);
+  cudaFree(p->gc_cnt);
+  cudaFree(p->gc_base);
+  cudaFree(p->gc_data);
   cudaFree(p->ctrl);
   cudaFreeHost(p->h_ctrl);
   cudaFreeHost(p->h_small);

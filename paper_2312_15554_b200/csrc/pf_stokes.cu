@@ -17,6 +17,8 @@
 //   S5 cuFFT D2Z (batch d): R -> R^
 // Every kernel returns immediately once ctrl->done is set.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "pf_internal.cuh"
 
@@ -362,6 +364,284 @@ __global__ void __launch_bounds__(kThreads) k_form_r_fix(const int64_t n, const 
   }
 }
 
+// ---------------------------------------------------------------------- S3 / S4, solid-only storage
+// On pore voxels (H = 0) the local step is u~' = u', a' = 0, lam' = lam (the fused
+// compact RS, pf_fused.cu), so once a = 0 there (a cold start, or any state this path
+// produced) u~, a and lam need storage and traffic on solid voxels only: [c][ns]
+// arrays in voxel order, addressed through exclusive per-64-voxel segment bases and a
+// warp ballot.  A warp takes one 64-voxel segment of one component per trip, two
+// voxels per lane (16-byte loads of u' and u).  S3 then moves u' (r), u (r+w), R (w)
+// and H for every voxel and the multipliers only for the solid fraction.
+#ifndef PF_GLOCAL_MINB
+// measured (256^3, cuFFT pipeline forced): S3 0.565 ms at one segment per trip and 4
+// CTAs/SM; two segments per trip (loads of both first) 0.598 at 2 CTAs/SM, 0.621 at 3
+#define PF_GLOCAL_MINB 4
+#endif
+struct GCompact {
+  const uint32_t* base;  // [nseg + 1]
+  double *ut, *a, *lam;  // [D][ns]
+  int64_t ns;
+};
+
+// segment w of component c: voxel pair (x, x + 1) of this lane and the compact
+// index of x (of x + 1: + s0)
+struct GSeg {
+  int64_t i, x, ci;
+  bool s0, s1;
+};
+
+__device__ __forceinline__ GSeg gseg(int64_t w, int64_t nseg, int64_t n, const uint8_t* __restrict__ H,
+                                     const GCompact& cp) {
+  const int lane = threadIdx.x & 31;
+  const int c = (int)(w / nseg);
+  const int64_t seg = w - (int64_t)c * nseg;
+  GSeg s;
+  s.x = (seg << 6) + 2 * lane;
+  s.i = (int64_t)c * n + s.x;
+  const uchar2 hh = *reinterpret_cast<const uchar2*>(H + s.x);
+  s.s0 = hh.x != 0;
+  s.s1 = hh.y != 0;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned m0 = __ballot_sync(0xffffffffu, s.s0), m1 = __ballot_sync(0xffffffffu, s.s1);
+  s.ci = (int64_t)c * cp.ns + cp.base[seg] + __popc(m0 & lt) + __popc(m1 & lt);
+  return s;
+}
+
+// one voxel: solid -> pure.py:59-68 with H = 1 (local_one's evaluation order), compact
+// multipliers updated; pore -> u~' = u', a' = 0, lam' = lam (its |lam|^2 is the
+// constant StokesConst::lam_pore_sq).  Returns R = b u~' - a'.
+struct CIn {
+  double t0, a0, l0;
+};
+__device__ __forceinline__ CIn cload(bool solid, const GCompact& cp, int64_t ci) {
+  CIn v{0.0, 0.0, 0.0};
+  if (solid) {
+    v.t0 = cp.ut[ci];
+    v.a0 = cp.a[ci];
+    v.l0 = cp.lam[ci];
+  }
+  return v;
+}
+__device__ __forceinline__ double local_c(bool solid, double u1, double u0, const CIn& v, double alpha, double b,
+                                          double (&acc)[6], const GCompact& cp, int64_t ci) {
+  if (solid) {
+    double t1, a1, l1;
+    local_one(u1, u0, v.t0, v.a0, v.l0, 1.0, alpha, b, acc, t1, a1, l1);
+    cp.ut[ci] = t1;
+    cp.a[ci] = a1;
+    cp.lam[ci] = l1;
+    return b * t1 - a1;
+  }
+  const double s4 = u1 - u0;
+  acc[4] += s4 * s4;
+  return b * u1 - 0.0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, PF_GLOCAL_MINB) k_stokes_local_c(
+    const int64_t n, const double* __restrict__ un, double* __restrict__ u, const uint8_t* __restrict__ H,
+    GCompact cp, const Ctrl* __restrict__ ctrl, double* __restrict__ part, double* __restrict__ R) {
+  if (ctrl->done) return;
+  const double alpha = ctrl->alpha, b = ctrl->b;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  const int64_t nseg = n >> 6, items = D * nseg;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  for (; w < items; w += nw) {
+    const GSeg s = gseg(w, nseg, n, H, cp);
+    const double2 u1 = *reinterpret_cast<const double2*>(un + s.i);
+    const double2 u0 = *reinterpret_cast<const double2*>(u + s.i);
+    const CIn va = cload(s.s0, cp, s.ci), vb = cload(s.s1, cp, s.ci + (s.s0 ? 1 : 0));
+    double2 r;
+    r.x = local_c(s.s0, u1.x, u0.x, va, alpha, b, acc, cp, s.ci);
+    r.y = local_c(s.s1, u1.y, u0.y, vb, alpha, b, acc, cp, s.ci + (s.s0 ? 1 : 0));
+    *reinterpret_cast<double2*>(u + s.i) = u1;
+    *reinterpret_cast<double2*>(R + s.i) = r;
+  }
+  block_sum<6>(acc);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) part[(size_t)k * gridDim.x + blockIdx.x] = acc[k];
+}
+
+// R += (b' - b) u~' with u~' = u' on pore voxels, the compact u~ on solid ones
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_form_r_fix_c(const int64_t n, const double* __restrict__ u,
+                                                           const uint8_t* __restrict__ H, GCompact cp,
+                                                           double* __restrict__ R, const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const double db = ctrl->db;
+  if (db == 0.0) return;
+  const int64_t nseg = n >> 6, items = D * nseg;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
+    const GSeg s = gseg(w, nseg, n, H, cp);
+    double2 r = *reinterpret_cast<const double2*>(R + s.i);
+    const double2 uu = *reinterpret_cast<const double2*>(u + s.i);
+    r.x = r.x + db * (s.s0 ? cp.ut[s.ci] : uu.x);
+    r.y = r.y + db * (s.s1 ? cp.ut[s.ci + (s.s0 ? 1 : 0)] : uu.y);
+    *reinterpret_cast<double2*>(R + s.i) = r;
+  }
+}
+
+// dir = 0: full -> compact (solid voxels); dir = 1: compact -> full, pore u~ = u, a = 0,
+// lam left untouched
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_gcompact_move(const int64_t n, const uint8_t* __restrict__ H,
+                                                            GCompact cp, double* ut, double* a, double* lam,
+                                                            const double* __restrict__ u, int dir) {
+  const int64_t nseg = n >> 6, items = D * nseg;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
+    const GSeg s = gseg(w, nseg, n, H, cp);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool solid = h ? s.s1 : s.s0;
+      const int64_t fi = s.i + h, ci = s.ci + (h && s.s0 ? 1 : 0);
+      if (dir == 0) {
+        if (solid) {
+          cp.ut[ci] = ut[fi];
+          cp.a[ci] = a[fi];
+          cp.lam[ci] = lam[fi];
+        }
+      } else if (solid) {
+        ut[fi] = cp.ut[ci];
+        a[fi] = cp.a[ci];
+        lam[fi] = cp.lam[ci];
+      } else {
+        ut[fi] = u[fi];
+        a[fi] = 0.0;
+      }
+    }
+  }
+}
+
+__global__ void k_seg_counts(const int64_t nseg, const uint8_t* __restrict__ H, uint32_t* __restrict__ cnt) {
+  for (int64_t sg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sg < nseg; sg += (int64_t)gridDim.x * blockDim.x) {
+    const uint4* w = reinterpret_cast<const uint4*>(H + (sg << 6));
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 v = w[k];
+      c += __popc(__vcmpne4(v.x, 0u)) + __popc(__vcmpne4(v.y, 0u)) + __popc(__vcmpne4(v.z, 0u)) +
+           __popc(__vcmpne4(v.w, 0u));
+    }
+    cnt[sg] = c >> 3;  // (__vcmpne4 sets all 8 bits of each differing byte)
+  }
+}
+
+// pore sums over the D components: |a| (eligibility: must be 0) and lam^2
+__global__ void __launch_bounds__(kThreads) k_pore_a_lam_d(int64_t n, int D, const uint8_t* __restrict__ H,
+                                                           const double* __restrict__ a,
+                                                           const double* __restrict__ lam, double* __restrict__ part) {
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < D * n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (H[i % n] == 0) {
+      acc[0] += fabs(a[i]);
+      acc[1] += lam[i] * lam[i];
+    }
+  }
+  block_sum<2>(acc);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = acc[0];
+    part[gridDim.x + blockIdx.x] = acc[1];
+  }
+}
+
+static GCompact gcompact_of(const pf_plan* p) {
+  GCompact c;
+  const int64_t m = (int64_t)p->g.d * p->gc_ns;
+  c.base = p->gc_base;
+  c.ut = p->gc_data;
+  c.a = p->gc_data + m;
+  c.lam = p->gc_data + 2 * m;
+  c.ns = p->gc_ns;
+  return c;
+}
+
+#ifndef PF_GCOMPACT
+#define PF_GCOMPACT 1  // solid-only multipliers on the cuFFT pipeline when eligible
+#endif
+
+// Decide and set up the cuFFT pipeline's solid-only storage for the solve being begun
+// (p->s_* bound; cold = the state is all zero).
+static int gcompact_setup(pf_plan* p, bool cold) {
+  const int64_t n = p->g.nr;
+  const int d = p->g.d;
+  p->gc_on = 0;
+  p->sc.lam_pore_sq = 0.0;
+  const char* e = getenv("POREFLOW_B200_GCOMPACT");
+  const bool want = p->compact_enable && (e ? e[0] == '1' : PF_GCOMPACT);
+  if (!want || (n & 63) != 0 || n < 64) return PF_OK;
+  if (cold) {
+    p->h_small[0] = p->h_small[1] = 0.0;
+  } else {
+    const int nb = blocks_for(d * n);
+    k_pore_a_lam_d<<<nb, kThreads, 0, p->work>>>(n, d, p->s_solid, p->s_a, p->s_lam, p->partials);
+    PF_CK_CUDA(cudaGetLastError());
+    double* out = p->partials + 24 * kMaxBlocks;
+    PF_CK(reduce_rows_to(p, p->partials, 2, nb, out));
+    PF_CK_CUDA(cudaMemcpyAsync(p->h_small, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->work));
+    PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  }
+  if (p->h_small[0] != 0.0) return PF_OK;  // a != 0 on some pore voxel: full storage
+  const double lam_pore_sq = p->h_small[1];
+  const int64_t nseg = n >> 6;
+  if (nseg > p->gc_nseg) {
+    cudaFree(p->gc_cnt);
+    cudaFree(p->gc_base);
+    p->gc_cnt = nullptr;
+    p->gc_base = nullptr;
+    PF_CK_CUDA(cudaMalloc(&p->gc_cnt, sizeof(uint32_t) * nseg));
+    PF_CK_CUDA(cudaMalloc(&p->gc_base, sizeof(uint32_t) * (nseg + 1)));
+    p->gc_nseg = nseg;
+  }
+  k_seg_counts<<<blocks_for(nseg), kThreads, 0, p->work>>>(nseg, p->s_solid, p->gc_cnt);
+  PF_CK_CUDA(cudaGetLastError());
+  PF_CK(scan_counts(p->work, p->gc_cnt, p->gc_base, nseg));
+  uint32_t ns = 0;
+  PF_CK_CUDA(cudaMemcpyAsync(p->h_small, p->gc_base + nseg, sizeof(uint32_t), cudaMemcpyDeviceToHost, p->work));
+  PF_CK_CUDA(cudaStreamSynchronize(p->work));
+  std::memcpy(&ns, p->h_small, sizeof(uint32_t));
+  p->gc_ns = ns;
+  const int64_t need = 3 * (int64_t)d * (ns > 0 ? ns : 1);
+  if (need > p->gc_cap) {
+    cudaFree(p->gc_data);
+    p->gc_data = nullptr;
+    PF_CK_CUDA(cudaMalloc(&p->gc_data, sizeof(double) * (size_t)need));
+    p->gc_cap = need;
+  }
+  if (cold) {
+    PF_CK_CUDA(cudaMemsetAsync(p->gc_data, 0, sizeof(double) * (size_t)need, p->work));
+  } else {
+    const GCompact cp = gcompact_of(p);
+    const int nb = blocks_for(d * n / 2);
+    switch (d) {
+      case 1: k_gcompact_move<1><<<nb, kThreads, 0, p->work>>>(n, p->s_solid, cp, p->s_ut, p->s_a, p->s_lam, p->s_u, 0); break;
+      case 2: k_gcompact_move<2><<<nb, kThreads, 0, p->work>>>(n, p->s_solid, cp, p->s_ut, p->s_a, p->s_lam, p->s_u, 0); break;
+      default: k_gcompact_move<3><<<nb, kThreads, 0, p->work>>>(n, p->s_solid, cp, p->s_ut, p->s_a, p->s_lam, p->s_u, 0); break;
+    }
+    PF_CK_CUDA(cudaGetLastError());
+  }
+  p->gc_on = 1;
+  p->sc.lam_pore_sq = lam_pore_sq;
+  return PF_OK;
+}
+
+// u~, a, lam back into the caller's full arrays (pore: u~ = u, a = 0, lam unchanged)
+static int gcompact_finish(pf_plan* p) {
+  if (!p->gc_on) return PF_OK;
+  const int64_t n = p->g.nr;
+  const GCompact cp = gcompact_of(p);
+  const int nb = blocks_for(p->g.d * n / 2);
+  switch (p->g.d) {
+    case 1: k_gcompact_move<1><<<nb, kThreads, 0, p->work>>>(n, p->s_solid, cp, p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+    case 2: k_gcompact_move<2><<<nb, kThreads, 0, p->work>>>(n, p->s_solid, cp, p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+    default: k_gcompact_move<3><<<nb, kThreads, 0, p->work>>>(n, p->s_solid, cp, p->s_ut, p->s_a, p->s_lam, p->s_u, 1); break;
+  }
+  PF_CK_CUDA(cudaGetLastError());
+  return PF_OK;  // (gc_on stays set: pf_stokes_pipeline reports the finished solve's pipeline)
+}
+
 // ---------------------------------------------------------------------- setup helpers
 // D^ = sum_c i k_c U^_c of the initial velocity (div_prev, stokes.py:370).
 template <int D>
@@ -426,15 +706,19 @@ static int enqueue_stokes_t(pf_plan* p, cudaEvent_t* ev = nullptr) {
   PF_CK(mark(1));
   PF_CK(plan_fft(p, false, D, Uh, un));
   PF_CK(mark(2));
-  k_stokes_local<D><<<nb3, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid, p->ctrl,
-                                                   part3,
-                                                   PF_FUSED_FORM_R ? R : nullptr);
+  if (p->gc_on)
+    k_stokes_local_c<D><<<nb3, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_solid, gcompact_of(p), p->ctrl, part3, R);
+  else
+    k_stokes_local<D><<<nb3, kThreads, 0, p->work>>>(n, un, p->s_u, p->s_ut, p->s_a, p->s_lam, p->s_solid, p->ctrl,
+                                                     part3, PF_FUSED_FORM_R ? R : nullptr);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(3));
   k_stokes_finalize<<<1, kFinalizeThreads, 0, p->work>>>(p->ctrl, part3, nb3, part1, nb1, p->s_hist, C, g.inv_n);
   PF_CK_CUDA(cudaGetLastError());
   PF_CK(mark(4));
-  if (PF_FUSED_FORM_R)
+  if (p->gc_on)
+    k_form_r_fix_c<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_u, p->s_solid, gcompact_of(p), R, p->ctrl);
+  else if (PF_FUSED_FORM_R)
     k_form_r_fix<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_ut, R, p->ctrl);
   else
     k_form_r<D><<<nb3, kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, R, p->ctrl, 1);
@@ -537,9 +821,15 @@ void k_stokes_finalize_launch(pf_plan* p, const double* part3, int nb3, const do
 }
 
 template <int D>
-static int stokes_setup_t(pf_plan* p, double b0) {
+static int stokes_setup_t(pf_plan* p, bool cold) {
   const Geom& g = p->g;
   const int64_t n = g.nr, nh = g.nh;
+  if (cold) {  // zero state: Q^ = D^ = 0 and R^ = FFT(b 0 - 0) = 0, no transforms
+    PF_CK_CUDA(cudaMemsetAsync(p->spec1, 0, sizeof(double2) * nh, p->work));
+    PF_CK_CUDA(cudaMemsetAsync(p->spec2, 0, sizeof(double2) * nh, p->work));
+    PF_CK_CUDA(cudaMemsetAsync(p->specA, 0, sizeof(double2) * D * nh, p->work));
+    return gcompact_setup(p, true);
+  }
   // Q^ = FFT(q), gauge Q^(0) = 0 (stokes.py:363, 367)
   PF_CK(plan_fft(p, true, 1, p->s_q, p->spec1));
   k_zero_mode<<<1, 1, 0, p->work>>>(p->spec1);
@@ -550,8 +840,7 @@ static int stokes_setup_t(pf_plan* p, double b0) {
   k_form_r<D><<<blocks_for(n), kThreads, 0, p->work>>>(n, p->s_ut, p->s_a, p->realB, p->ctrl, 0);
   PF_CK(plan_fft(p, true, D, p->realB, p->specA));
   PF_CK_CUDA(cudaGetLastError());
-  (void)b0;
-  return PF_OK;
+  return gcompact_setup(p, false);
 }
 
 }  // namespace pf
@@ -598,17 +887,19 @@ int pf_stokes_begin(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid,
   k_ctrl_init<<<1, 1, 0, p->work>>>(p->ctrl, P->alpha, P->beta, P->b);
   PF_CK_CUDA(cudaGetLastError());
   p->pipeline = (p->fused_enable && fused_supported(p)) ? 1 : 0;
+  p->gc_on = 0;
   if (p->pipeline == 1) {
     PF_CK(fused_ensure(p));
     const int st = fused_setup(p);
     p->cold_start = 0;  // consumed
     return st;
   }
+  const bool cold = p->cold_start != 0;
   p->cold_start = 0;
   switch (d) {
-    case 1: PF_CK(stokes_setup_t<1>(p, P->b)); break;
-    case 2: PF_CK(stokes_setup_t<2>(p, P->b)); break;
-    default: PF_CK(stokes_setup_t<3>(p, P->b)); break;
+    case 1: PF_CK(stokes_setup_t<1>(p, cold)); break;
+    case 2: PF_CK(stokes_setup_t<2>(p, cold)); break;
+    default: PF_CK(stokes_setup_t<3>(p, cold)); break;
   }
   return PF_OK;
 }
@@ -650,6 +941,7 @@ int pf_stokes_end(pf_plan* p, pf_stokes_result* res) {
     k_scale_copy<<<blocks_for(nh), kThreads, 0, p->work>>>(nh, p->spec1, p->specB, p->g.inv_n);
     PF_CK_CUDA(cudaGetLastError());
     PF_CK(plan_fft(p, false, 1, p->specB, p->s_q));
+    PF_CK(gcompact_finish(p));
   }
   PF_CK_CUDA(cudaMemcpyAsync(&p->h_ctrl[0], p->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, p->work));
   PF_CK_CUDA(cudaStreamSynchronize(p->work));
@@ -700,7 +992,8 @@ int pf_stokes_profile(pf_plan* p, int64_t n_iter, double* stage_ms) {
 
 int pf_stokes_pipeline(const pf_plan* p) {
   if (!p) return -1;
-  return (p->pipeline == 1 && fused_is_compact(p)) ? 2 : p->pipeline;
+  if (p->pipeline == 1) return fused_is_compact(p) ? 2 : 1;
+  return p->gc_on ? 3 : 0;
 }
 
 int pf_stokes_solve(pf_plan* p, const pf_stokes_params* P, const uint8_t* solid, double* u, double* ut, double* q,
