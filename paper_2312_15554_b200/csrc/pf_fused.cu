@@ -2221,8 +2221,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_fslab_totals(const double*
                                                                    const double* __restrict__ ppk, int npk,
                                                                    double lam_pore, double* __restrict__ totals) {
   double S[6], Q[3];
-  reduce_partials<6>(prs, nrs, S);
-  reduce_partials<3>(ppk, npk, Q);
+  reduce_partials2<6, 3>(prs, nrs, S, ppk, npk, Q);
   if (threadIdx.x == 0) {
     S[2] += lam_pore;
     for (int k = 0; k < 6; ++k) totals[k] = S[k];

@@ -312,7 +312,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
 // thread keeps four independent running sums per quantity (loads in flight),
 // combined in a fixed order, then a fixed-shape block tree.
 template <int NQ>
-__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nblk, double (&tot)[NQ]) {
+__device__ __forceinline__ void thread_partials(const double* __restrict__ part, int nblk, double* tot) {
   constexpr int U = PF_REDUCE_UNROLL;
   double s4[NQ][U];
 #pragma unroll
@@ -340,7 +340,27 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ part,
     x = s4[q][0];
     tot[q] = x;
   }
+}
+
+template <int NQ>
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nblk, double (&tot)[NQ]) {
+  thread_partials<NQ>(part, nblk, tot);
   block_sum<NQ>(tot);
+}
+
+// Two partial arrays in one pass: both arrays' loads in flight together and one block
+// tree (per quantity the same order and tree shape as two reduce_partials calls).
+template <int NA, int NB>
+__device__ __forceinline__ void reduce_partials2(const double* __restrict__ pa, int na, double (&ta)[NA],
+                                                 const double* __restrict__ pb, int nb, double (&tb)[NB]) {
+  double tot[NA + NB];
+  thread_partials<NA>(pa, na, tot);
+  thread_partials<NB>(pb, nb, tot + NA);
+  block_sum<NA + NB>(tot);
+#pragma unroll
+  for (int q = 0; q < NA; ++q) ta[q] = tot[q];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) tb[q] = tot[NA + q];
 }
 
 __device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }

@@ -88,8 +88,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_slab_totals(const double* 
                                                                   const double* __restrict__ part1, int nb1,
                                                                   double* __restrict__ totals) {
   double S[6], Q[3];
-  reduce_partials<6>(part3, nb3, S);
-  reduce_partials<3>(part1, nb1, Q);
+  reduce_partials2<6, 3>(part3, nb3, S, part1, nb1, Q);
   if (threadIdx.x == 0) {
     for (int k = 0; k < 6; ++k) totals[k] = S[k];
     for (int k = 0; k < 3; ++k) totals[6 + k] = Q[k];

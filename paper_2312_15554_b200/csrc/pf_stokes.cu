@@ -272,8 +272,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
   for (int k = 0; k < 3; ++k) P[k] = 1.0 + k;
   (void)part3, (void)nb3, (void)part1, (void)nb1;
 #else
-  reduce_partials<6>(part3, nb3, S);
-  reduce_partials<3>(part1, nb1, P);
+  reduce_partials2<6, 3>(part3, nb3, S, part1, nb1, P);
 #endif
   if (threadIdx.x != 0) return;
   const double alpha = ctrl->alpha, beta = ctrl->beta, b = ctrl->b;
