@@ -720,7 +720,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="stokes", choices=("stokes", "transport", "ensemble", "slab", "pipeline"),
                     help="stokes = the headline metric; transport / ensemble = secondary lines")
-    ap.add_argument("--cells", type=int, default=8, help="cells per GPU for --workload ensemble")
+    ap.add_argument("--cells", type=int, default=16, help="cells per GPU for --workload ensemble")
     ap.add_argument("--slab-cufft", action="store_true", help="--workload slab: the cuFFT slab pipeline")
     ap.add_argument("--exchange", default="a2a", choices=("a2a", "p2p"),
                     help="--workload slab: all_to_all exchange or the transpose fused into the passes over P2P")
