@@ -603,6 +603,9 @@ __global__ void __launch_bounds__(TMP<N, INV>::T, 1) k_taxis_pipe(TBufs B, const
 }
 
 // ------------------------------------------------------------------ RS_T
+#ifndef PF_TRS_UREG
+#define PF_TRS_UREG 1
+#endif
 template <int N>
 struct TRS {
   using C = Cfg<N>;
@@ -625,7 +628,13 @@ struct TRS {
   // the forward sequences overwrite the inverse ones (the local step reads its
   // gradients into registers first), so one buffer of max(SI, SF) bytes
   static constexpr size_t SQ = SI > SF ? SI : SF;
-  static constexpr size_t BYTES = TW + SQ + XM + XN + UB + HB;
+  // UREG: u and the indicator go straight from global memory into registers at the
+  // start of each tile (consumed after the inverse transforms), so only the X rows
+  // are staged: less shared memory per CTA, more CTAs per SM
+  // (measured: 256^3 RS_T 0.338 -> 0.324 ms with 2-row tiles, 0.334 with 4-row ones;
+  // 128^3 0.058 -> 0.066, so staged there)
+  static constexpr bool UREG = PF_TRS_UREG && N == 256;
+  static constexpr size_t BYTES = TW + SQ + XM + XN + (UREG ? 0 : UB + HB);
 #ifdef PF_TRS_MINB
   static constexpr int MINB = PF_TRS_MINB;
 #else
@@ -682,9 +691,9 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
     fz::mbar_init(&mbar);
     fz::mbar_init(&mbx);
     if ((int)blockIdx.x < NT) {
-      if (SPLIT) {
+      if (SPLIT || K::UREG) {
         trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbx, 1);
-        trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar, 2);
+        if (!K::UREG) trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar, 2);
       } else {
         trs_issue<N>(blockIdx.x, B, u, Hs, sx, sxn, su, sh, &mbar);
       }
@@ -692,10 +701,22 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
   }
   __syncthreads();
   const double pe = P.pe, eta = P.eta, a0 = P.a0, ubg = P.ubg;
+  const int64_t nvox = (int64_t)N * N * N;
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < NT; tile += gridDim.x, phase ^= 1u) {
     const int64_t row0 = (int64_t)tile * R;
-    if (SPLIT) fz::mbar_wait(&mbx, phase);
+    double ur[K::UREG ? K::VPT : 1][3];
+    double hr[K::UREG ? K::VPT : 1];
+    if constexpr (K::UREG) {  // this tile's u and H, in flight under the packing and inverse transforms
+#pragma unroll
+      for (int j = 0; j < K::VPT; ++j) {
+        const int64_t x = row0 * N + t + T * j;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ur[j][c] = __ldcs(u + c * nvox + x);
+        hr[j] = (double)__ldcs(Hs + x);
+      }
+    }
+    if (SPLIT || K::UREG) fz::mbar_wait(&mbx, phase);
     else fz::mbar_wait(&mbar, phase);
     // (1) inverse sequences: per row r  Z = X(d0) + i X(d1);  per pair p  Z = X(d2)_{2p} + i X(d2)_{2p+1}
     for (int idx = t; idx < (R + R / 2) * (H + 1); idx += T) {
@@ -719,7 +740,7 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       }
     }
     __syncthreads();
-    if (SPLIT && t == 0 && tile + (int)gridDim.x < NT)  // the X rows are packed: refill them now
+    if ((SPLIT || K::UREG) && t == 0 && tile + (int)gridDim.x < NT)  // the X rows are packed: refill them now
       trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbx, 1);
     fz::fft_units<N, true>(SIq, K::NSI, SS, tw, g, l, T / C::G);
     if constexpr (C::M > 1) {
@@ -727,7 +748,7 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       fz::radix_stage<N, true>(SIq, K::NSI, SS, tw, t, T);
     }
     __syncthreads();
-    if (SPLIT) fz::mbar_wait(&mbar, phase);  // u and H of this tile
+    if (SPLIT && !K::UREG) fz::mbar_wait(&mbar, phase);  // u and H of this tile
     // (2) polarization (pure.py:71-87) with A, B, F from H and u (transport.py:112-121);
     // gradients to registers first: the forward sequences overwrite the inverse ones
     double gv[K::VPT][3];
@@ -744,7 +765,7 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
     for (int j = 0; j < K::VPT; ++j) {
       const int v = t + T * j, row = v / N, col = v % N;
       const double* gr = gv[j];
-      const double h = (double)sh[v];
+      const double h = K::UREG ? hr[j] : (double)sh[v];
       const double pore = 1.0 - h;
       const double contrast = (pore + eta * h) - a0;
       const double pep = pe * pore;
@@ -754,13 +775,13 @@ __global__ void __launch_bounds__(TRS<N>::T, TRS<N>::MINB) k_trs(TBufs B, TP P, 
       for (int c = 0; c < 3; ++c) {
         const double tg = gr[c] + P.g[c];
         w[c] = contrast * tg;
-        s = s - (pep * su[c * V + v] - P.b0v[c]) * tg;
+        s = s - (pep * (K::UREG ? ur[j][c] : su[c * V + v]) - P.b0v[c]) * tg;
       }
       SFq[(2 * row) * SS + C::sp(col)] = make_double2(w[0], w[1]);
       SFq[(2 * row + 1) * SS + C::sp(col)] = make_double2(s, w[2]);
     }
     __syncthreads();
-    if (t == 0 && tile + (int)gridDim.x < NT)
+    if (!K::UREG && t == 0 && tile + (int)gridDim.x < NT)
       trs_issue<N>(tile + gridDim.x, B, u, Hs, sx, sxn, su, sh, &mbar, SPLIT ? 2 : 0);
     if constexpr (C::M > 1) {
       fz::radix_stage<N, false>(SFq, K::NSF, SS, tw, t, T);
