@@ -116,6 +116,12 @@
 #ifndef PF_PK_THREADS
 #define PF_PK_THREADS 128
 #endif
+#ifndef PF_PK64_T
+#define PF_PK64_T PF_PK_THREADS  // PK threads at N = 64 (tile shape: CP columns from T / 8-lane groups)
+#endif
+#ifndef PF_M64_T
+#define PF_M64_T 128  // axis-1 passes' threads at N = 64 (columns per tile = T / 8)
+#endif
 #ifndef PF_PK512_T  // PK at N = 512: threads, columns per tile, min blocks per SM (measured:
 #define PF_PK512_T 192  // 3.85 ms vs 4.06 at 128 threads / 2 columns / 3 blocks)
 #endif
@@ -1088,7 +1094,7 @@ __global__ void __launch_bounds__(kThreads) k_pore_a_lam(int64_t n, const uint8_
 template <int N>
 struct PK2 {
   using C = Cfg<N>;
-  static constexpr int T = N == 512 ? PF_PK512_T : (N == 1024 ? PF_PK1024_T : PF_PK_THREADS);
+  static constexpr int T = N == 512 ? PF_PK512_T : (N == 1024 ? PF_PK1024_T : (N == 64 ? PF_PK64_T : PF_PK_THREADS));
   static constexpr int MINB = N == 512 ? PF_PK512_MINB : (N == 1024 ? PF_PK1024_MINB : (N == 128 ? PF_PK128_MINB : PF_PK_MINB));
   static constexpr int NGP = T / C::G;
   // 3 components x CP columns = NGP sequences: one FFT round per direction, no idle groups
@@ -1130,7 +1136,7 @@ struct PK2 {
 template <int N>
 struct M2 {
   using C = Cfg<N>;
-  static constexpr int T = 128;
+  static constexpr int T = N == 64 ? PF_M64_T : 128;
   static constexpr int NGM = T / C::G;        // groups = block transforms per tile
   static constexpr int CM = NGM / C::M;       // columns (sequences) per tile
   static constexpr int NCH = C::H / CM;
@@ -1150,7 +1156,7 @@ struct M2 {
 };
 
 template <int N, bool INV, bool SL>
-__global__ void __launch_bounds__(128, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl,
+__global__ void __launch_bounds__(M2<N>::T, PF_M_MINB) k_maxis(Bufs B, const Ctrl* __restrict__ ctrl,
                                                              const __grid_constant__ CUtensorMap tmap, int nyq_only,
                                                              const __grid_constant__ CUtensorMap tmap_xu) {
   using C = Cfg<N>;
