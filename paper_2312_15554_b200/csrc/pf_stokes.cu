@@ -261,11 +261,14 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
     Ctrl* __restrict__ ctrl, const double* __restrict__ part3, int nb3, const double* __restrict__ part1,
     int nb1, double* __restrict__ hist, const StokesConst C, const double inv_n) {
   pdl_wait();
-  if (ctrl->done) return;
 #if PF_ABL_FINTRIV  // measurement only: the launch without its work (results invalid)
+  if (ctrl->done) return;
   if (threadIdx.x == 0) ctrl->iter += 1;
   return;
 #endif
+  // the done flag is read together with the partials (a finished solve's finalize
+  // reduces stale partials and discards them) so the two loads overlap
+  const int32_t done = ctrl->done;
   double S[6], P[3];
 #if PF_ABL_NORED  // measurement only: partial reductions skipped (results invalid)
   for (int k = 0; k < 6; ++k) S[k] = 1.0 + k;
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_stokes_finalize(
 #else
   reduce_partials2<6, 3>(part3, nb3, S, part1, nb1, P);
 #endif
-  if (threadIdx.x != 0) return;
+  if (done || threadIdx.x != 0) return;
   const double alpha = ctrl->alpha, beta = ctrl->beta, b = ctrl->b;
   const double er = C.eps_rel;
   double rp[3], rd[3], tp[3], td[3];

@@ -166,10 +166,10 @@ __global__ void __launch_bounds__(kFinalizeThreads) k_transport_finalize(Ctrl* _
                                                                          const double t2, const int64_t max_iter,
                                                                          const double scale) {
   pdl_wait();
-  if (ctrl->done) return;
+  const int32_t done = ctrl->done;  // (read together with the partials, see k_stokes_finalize)
   double S[2];
   reduce_partials<2>(part, nb, S);
-  if (threadIdx.x != 0) return;
+  if (done || threadIdx.x != 0) return;
   const double r1 = sqrt(S[0] * scale), r2 = sqrt(S[1] * scale);
   const int64_t it = ctrl->iter + 1;
   double* row = hist + (it - 1) * PF_TRANSPORT_COLUMNS;
