@@ -236,7 +236,8 @@ class StokesSolver:
 
     @property
     def pipeline(self) -> str:
-        """Pipeline the device chose: 'fused' / 'fused-compact' (N^3, N in 64/128/256) or 'cufft'."""
+        """Pipeline the device chose: 'fused' / 'fused-compact' (power-of-two cubes) or 'cufft' /
+        'cufft-compact' (other grids; '-compact' = solid-only multiplier storage)."""
         return {0: "cufft", 1: "fused", 2: "fused-compact", 3: "cufft-compact"}.get(
             N.load().pf_stokes_pipeline(self.plan.handle), "none")
 
