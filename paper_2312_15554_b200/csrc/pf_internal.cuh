@@ -68,11 +68,16 @@ const char* cufft_name(cufftResult r);
 constexpr int kThreads = 256;
 constexpr int kSMs = 148;
 constexpr int kMaxBlocks = kSMs * 8;  // 8 x 256-thread CTAs fill an SM (2048 threads)
+// Finalize / partial-reduction shape, measured (r02e; Gvox-it/s at 64^3 / 128^3 / 256^3):
+// 1024 threads x 4 running sums 7.43 / 13.06 / 16.37, x 2 7.59 / 13.15 / 16.38,
+// x 1 7.65 / 13.14 / 16.41; 512 x 1 7.70 / 13.17 / 16.40; 256 x 1 7.59 / 13.09 / 16.34
+// (the partial counts are a few thousand: the serial combine of the unrolled sums
+// cost more than the loads it kept in flight)
 #ifndef PF_FINALIZE_THREADS
-#define PF_FINALIZE_THREADS 1024
+#define PF_FINALIZE_THREADS 512
 #endif
 #ifndef PF_REDUCE_UNROLL
-#define PF_REDUCE_UNROLL 4  // independent running sums (loads in flight) per thread in reduce_partials
+#define PF_REDUCE_UNROLL 1  // independent running sums (loads in flight) per thread in reduce_partials
 #endif
 constexpr int kFinalizeThreads = PF_FINALIZE_THREADS;
 
