@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -185,6 +186,35 @@ def _np_dtype(dt):
 # staged ring below, whose output is ordinary pageable memory.
 _PINNED_OUT_BYTES = int(float(os.environ.get("POREFLOW_B200_PINNED_OUT_GB", "8")) * (1 << 30))
 
+# A dropped result's pinned blocks go back to torch's caching host allocator and are
+# reused by the next result, but blocks still held by live results cannot be:
+# pinning fresh memory costs ~0.6 s per GB (page locking), several times what the
+# staged ring needs for the whole copy.  So after the first large result, a large
+# result comes back pinned only when at least as many pinned result bytes have been
+# released since (the caller dropped earlier results); otherwise through the ring.
+# (A caller that keeps every load case's state pays the page locking once, not per
+# solve; a loop that drops each state before the next keeps the direct DMA path.)
+_pin_lock = threading.Lock()
+_pin_state = {"used": False, "released": 0}
+
+
+def _pinned_ok(total: int) -> bool:
+    if total <= (64 << 20):
+        return True
+    with _pin_lock:
+        if not _pin_state["used"]:
+            _pin_state["used"] = True
+            return True
+        if _pin_state["released"] >= total:
+            _pin_state["released"] -= total
+            return True
+        return False
+
+
+def _pinned_released(nbytes: int) -> None:
+    with _pin_lock:
+        _pin_state["released"] += nbytes
+
 
 def to_host_many(xs) -> list:
     """CUDA tensors -> new numpy arrays.
@@ -199,13 +229,17 @@ def to_host_many(xs) -> list:
     t = torch()
     xs = [x.contiguous() for x in xs]
     total = sum(x.numel() * x.element_size() for x in xs)
-    if total <= _PINNED_OUT_BYTES:
+    if total <= _PINNED_OUT_BYTES and _pinned_ok(total):
         hs = [t.empty(tuple(x.shape), dtype=x.dtype, pin_memory=True) for x in xs]
         for h, x in zip(hs, xs):
             h.copy_(x, non_blocking=True)
         if xs:
             t.cuda.current_stream(xs[0].device).synchronize()
-        return [h.numpy() for h in hs]
+        outs = [h.numpy() for h in hs]
+        if total > (64 << 20):  # (the array, and every view of it, holds the pinned block)
+            for o in outs:
+                weakref.finalize(o, _pinned_released, o.nbytes)
+        return outs
     outs = [np.empty(tuple(x.shape), dtype=_np_dtype(x.dtype)) for x in xs]
     big = [i for i, o in enumerate(outs) if o.nbytes > (4 << 20)]
     for i, o in enumerate(outs):
