@@ -153,3 +153,26 @@ def test_packing_slab_rasterization_equals_full_cell():
     full = rasterize_packing(pk, dims).values
     for lo, hi in [(0, 8), (8, 16), (24, 32), (31, 32)]:
         assert np.array_equal(rasterize_packing_slab(pk, dims, lo, hi), full[lo:hi]), (lo, hi)
+
+
+def test_pinned_output_policy():
+    """device.to_host_many's choice between pinned outputs and the staged ring: the
+    first large result is pinned, a later one only when as many pinned result bytes
+    have been released (the caller dropped earlier results); small ones always."""
+    from paper_2312_15554_b200 import device as D
+
+    saved = dict(D._pin_state)
+    try:
+        D._pin_state.update(used=False, released=0)
+        big = 1 << 30
+        assert D._pinned_ok(1 << 20)               # small: always pinned
+        assert D._pinned_ok(big)                   # first large result
+        assert not D._pinned_ok(big)               # the first still alive: ring
+        D._pinned_released(big // 2)
+        assert not D._pinned_ok(big)               # not enough released yet
+        D._pinned_released(big // 2)
+        assert D._pinned_ok(big)                   # the dropped result's blocks are reused
+        assert D._pin_state["released"] == 0
+    finally:
+        D._pin_state.clear()
+        D._pin_state.update(saved)
